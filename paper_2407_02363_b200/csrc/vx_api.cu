@@ -1,0 +1,856 @@
+// C-ABI layer of libvx.so (include/vx.h): contexts, device-resident grids and
+// fields, host<->device staging, the camera-tick pipeline.  No CPU compute
+// path exists here: every numeric result comes from the sm_100a kernels in
+// vx_edt.cu / vx_map.cu / vx_query.cu.
+#include "vx.h"
+#include "vx_internal.cuh"
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+using namespace vx;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char *fmt, ...) __attribute__((format(printf, 2, 3)));
+int fail(int code, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char *what) {
+    return fail(e == cudaErrorMemoryAllocation ? VX_ENOMEM : VX_ECUDA, "%s: %s (%s)", what,
+                cudaGetErrorString(e), cudaGetErrorName(e));
+}
+
+#define VX_CUDA(call)                                   \
+    do {                                                \
+        cudaError_t _e = (call);                        \
+        if (_e != cudaSuccess) return cuda_fail(_e, #call); \
+    } while (0)
+
+// growable device buffer
+struct DevBuf {
+    void *p = nullptr;
+    size_t n = 0;
+    cudaError_t ensure(size_t bytes) {
+        if (bytes <= n) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+        size_t want = bytes + bytes / 8 + 256;
+        cudaError_t e = cudaMalloc(&p, want);
+        if (e == cudaSuccess) n = want;
+        return e;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+};
+
+inline double logit(double p) { return std::log(p / (1.0 - p)); }  // grids.py:24-25
+
+constexpr float kLMin = -2.0f, kLMax = 3.5f;
+constexpr float kOccThr = 0.0f;  // float32(logit(0.5)): the cached occupancy threshold
+
+}  // namespace
+
+struct vx_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    DevBuf scratch, staging, staging2, temp;
+    long long launches = 0;
+};
+
+struct vx_grid {
+    vx_ctx *ctx = nullptr;
+    GridGeom g{};
+    long long n = 0;
+    float *cells = nullptr;
+    uint8_t *occ = nullptr;         // cells > 0 (threshold 0.5), kept in sync by the kernels
+    uint32_t *counts = nullptr;     // bincount scratch, all zero between inserts
+    int32_t *touched = nullptr;     // voxels written since the last clear (may repeat)
+    DevCounters *ctr = nullptr;
+    unsigned long long *set_oob = nullptr;
+    int set_oob_cap = 0;
+    int capacity = 0;
+    bool sparse_ok = true;          // touched list covers every non-zero cell
+    bool maybe_oor = false;         // host wrote cells outside [L_MIN, L_MAX] or NaN
+};
+
+struct vx_field {
+    vx_ctx *ctx = nullptr;
+    int nx = 0, ny = 0, nz = 0;
+    int32_t *site = nullptr;
+    bool owned = true;
+};
+
+// ----------------------------------------------------------------------------
+extern "C" int vx_abi_version(void) { return VX_ABI_VERSION; }
+extern "C" const char *vx_last_error(void) { return g_err.c_str(); }
+
+extern "C" int vx_ctx_create(int device, vx_ctx **out) {
+    if (!out) return fail(VX_EINVAL, "out is NULL");
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0)
+        return fail(VX_ENODEV, "no CUDA device available (%s); libvx has no CPU fallback",
+                    e == cudaSuccess ? "0 devices" : cudaGetErrorString(e));
+    if (device < 0 || device >= ndev) return fail(VX_EINVAL, "device %d out of range", device);
+    VX_CUDA(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    VX_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10)
+        return fail(VX_ENODEV, "device %d is sm_%d%d; libvx is built for sm_100a", device, prop.major,
+                    prop.minor);
+    vx_ctx *c = new vx_ctx;
+    c->device = device;
+    e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+        delete c;
+        return cuda_fail(e, "cudaStreamCreate");
+    }
+    *out = c;
+    return VX_OK;
+}
+
+extern "C" int vx_ctx_destroy(vx_ctx *c) {
+    if (!c) return VX_OK;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    c->scratch.release();
+    c->staging.release();
+    c->staging2.release();
+    c->temp.release();
+    cudaStreamDestroy(c->stream);
+    delete c;
+    return VX_OK;
+}
+
+extern "C" int vx_ctx_stream(vx_ctx *c, void **s) {
+    if (!c || !s) return fail(VX_EINVAL, "NULL argument");
+    *s = (void *)c->stream;
+    return VX_OK;
+}
+
+extern "C" int vx_ctx_synchronize(vx_ctx *c) {
+    if (!c) return fail(VX_EINVAL, "NULL ctx");
+    VX_CUDA(cudaStreamSynchronize(c->stream));
+    return VX_OK;
+}
+
+extern "C" int64_t vx_ctx_launches(const vx_ctx *c) { return c ? c->launches : 0; }
+
+extern "C" int vx_host_alloc(size_t bytes, void **out) {
+    if (!out) return fail(VX_EINVAL, "NULL out");
+    VX_CUDA(cudaHostAlloc(out, bytes ? bytes : 1, cudaHostAllocPortable));
+    return VX_OK;
+}
+
+extern "C" int vx_host_free(void *p) {
+    if (p) VX_CUDA(cudaFreeHost(p));
+    return VX_OK;
+}
+
+// ---- grids ------------------------------------------------------------------
+static int check_geom(int nx, int ny, int nz, double vs) {
+    if (nx <= 0 || ny <= 0 || nz <= 0)
+        return fail(VX_EINVAL, "dims must be three positive integers, got (%d, %d, %d)", nx, ny, nz);
+    if (!(vs > 0.0)) return fail(VX_EINVAL, "voxel_size must be > 0");
+    if ((long long)nx * ny * nz >= (1LL << 31))
+        return fail(VX_EINVAL, "grid too large for 32-bit voxel addressing");
+    return VX_OK;
+}
+
+extern "C" int vx_grid_create(vx_ctx *ctx, int nx, int ny, int nz, double vs, const double origin[3],
+                              vx_grid **out) {
+    if (!ctx || !out) return fail(VX_EINVAL, "NULL argument");
+    int rc = check_geom(nx, ny, nz, vs);
+    if (rc) return rc;
+    VX_CUDA(cudaSetDevice(ctx->device));
+    vx_grid *g = new vx_grid;
+    g->ctx = ctx;
+    g->g = GridGeom{nx, ny, nz, vs, origin ? origin[0] : 0.0, origin ? origin[1] : 0.0,
+                    origin ? origin[2] : 0.0};
+    g->n = (long long)nx * ny * nz;
+    g->capacity = (int)g->n;
+    cudaError_t e = cudaSuccess;
+    if (e == cudaSuccess) e = cudaMalloc(&g->cells, g->n * sizeof(float));
+    if (e == cudaSuccess) e = cudaMalloc(&g->occ, (g->n + 15) & ~15LL);
+    if (e == cudaSuccess) e = cudaMalloc(&g->counts, g->n * sizeof(uint32_t));
+    if (e == cudaSuccess) e = cudaMalloc(&g->touched, g->n * sizeof(int32_t));
+    if (e == cudaSuccess) e = cudaMalloc(&g->ctr, sizeof(DevCounters));
+    if (e == cudaSuccess) e = cudaMemsetAsync(g->cells, 0, g->n * sizeof(float), ctx->stream);
+    if (e == cudaSuccess) e = cudaMemsetAsync(g->occ, 0, (g->n + 15) & ~15LL, ctx->stream);
+    if (e == cudaSuccess) e = cudaMemsetAsync(g->counts, 0, g->n * sizeof(uint32_t), ctx->stream);
+    if (e == cudaSuccess) e = cudaMemsetAsync(g->ctr, 0, sizeof(DevCounters), ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) {
+        vx_grid_destroy(g);
+        return cuda_fail(e, "vx_grid_create");
+    }
+    *out = g;
+    return VX_OK;
+}
+
+extern "C" int vx_grid_destroy(vx_grid *g) {
+    if (!g) return VX_OK;
+    if (g->ctx) cudaStreamSynchronize(g->ctx->stream);
+    cudaFree(g->cells);
+    cudaFree(g->occ);
+    cudaFree(g->counts);
+    cudaFree(g->touched);
+    cudaFree(g->ctr);
+    cudaFree(g->set_oob);
+    delete g;
+    return VX_OK;
+}
+
+static int grid_clear_async(vx_grid *g) {
+    cudaError_t e = launch_reset(g->cells, g->occ, g->touched, g->ctr, g->n, g->capacity,
+                                 !g->sparse_ok, g->ctx->stream);
+    g->ctx->launches += 2;
+    if (e != cudaSuccess) return cuda_fail(e, "reset");
+    g->sparse_ok = true;
+    g->maybe_oor = false;
+    return VX_OK;
+}
+
+extern "C" int vx_grid_clear(vx_grid *g) {
+    if (!g) return fail(VX_EINVAL, "NULL grid");
+    return grid_clear_async(g);
+}
+
+static bool same_geometry(const vx_grid *a, const vx_grid *b) {  // grids.py:214-217
+    return a->g.nx == b->g.nx && a->g.ny == b->g.ny && a->g.nz == b->g.nz && a->g.vs == b->g.vs &&
+           a->g.ox == b->g.ox && a->g.oy == b->g.oy && a->g.oz == b->g.oz;
+}
+
+static int insert_device(vx_grid *g, const double *d_xyz, long long n, const long long *n_dev,
+                         float hit, double thr, const vx_grid *mask) {
+    if (mask && !same_geometry(g, mask))
+        return fail(VX_EINVAL, "robot_mask geometry does not match this grid");
+    cudaStream_t st = g->ctx->stream;
+    VX_CUDA(cudaMemsetAsync(g->ctr, 0, 3 * sizeof(unsigned long long), st));
+    const float thr32 = (float)logit(thr);  // numpy compares in float32
+    cudaError_t e = launch_scatter(d_xyz, n, (const int64_t *)n_dev, g->g, mask ? mask->cells : nullptr,
+                                   thr32, g->counts, g->touched, g->ctr, g->capacity, st);
+    if (e != cudaSuccess) return cuda_fail(e, "scatter");
+    g->ctx->launches += 1;
+    if (g->maybe_oor) {
+        e = launch_dense_clip(g->cells, g->counts, g->n, g->ctr, st);
+        if (e != cudaSuccess) return cuda_fail(e, "dense_clip");
+        g->ctx->launches += 1;
+    }
+    e = launch_finalize(g->cells, g->occ, g->counts, g->touched, g->ctr, g->n, g->capacity,
+                        n > 0 ? n : 1, hit, kOccThr, st);
+    if (e != cudaSuccess) return cuda_fail(e, "finalize");
+    g->ctx->launches += 2;
+    return VX_OK;
+}
+
+extern "C" int vx_grid_last_stats(vx_grid *g, vx_insert_stats *stats) {
+    if (!g || !stats) return fail(VX_EINVAL, "NULL argument");
+    DevCounters h;
+    VX_CUDA(cudaMemcpyAsync(&h, g->ctr, sizeof h, cudaMemcpyDeviceToHost, g->ctx->stream));
+    VX_CUDA(cudaStreamSynchronize(g->ctx->stream));
+    stats->inserted = (int64_t)h.inserted;
+    stats->outliers_removed = 0;
+    stats->robot_skipped = (int64_t)h.skipped;
+    stats->out_of_bounds = (int64_t)h.oob;
+    return VX_OK;
+}
+
+extern "C" int vx_grid_insert_points_device(vx_grid *g, const double *d_xyz, int64_t n, float hit,
+                                            double thr, const vx_grid *mask) {
+    if (!g || (n > 0 && !d_xyz)) return fail(VX_EINVAL, "NULL argument");
+    if (n < 0) return fail(VX_EINVAL, "negative point count");
+    return insert_device(g, d_xyz, n, nullptr, hit, thr, mask);
+}
+
+extern "C" int vx_grid_insert_points(vx_grid *g, const double *xyz, int64_t n, float hit, double thr,
+                                     const vx_grid *mask, vx_insert_stats *stats) {
+    if (!g || (n > 0 && !xyz)) return fail(VX_EINVAL, "NULL argument");
+    if (n < 0) return fail(VX_EINVAL, "negative point count");
+    if (mask && !same_geometry(g, mask))
+        return fail(VX_EINVAL, "robot_mask geometry does not match this grid");
+    if (n == 0) {  // grids.py:163-164
+        if (stats) *stats = vx_insert_stats{0, 0, 0, 0};
+        return VX_OK;
+    }
+    vx_ctx *c = g->ctx;
+    VX_CUDA(c->staging.ensure((size_t)n * 3 * sizeof(double)));
+    VX_CUDA(cudaMemcpyAsync(c->staging.p, xyz, (size_t)n * 3 * sizeof(double), cudaMemcpyHostToDevice,
+                            c->stream));
+    int rc = insert_device(g, (const double *)c->staging.p, n, nullptr, hit, thr, mask);
+    if (rc) return rc;
+    vx_insert_stats s;
+    rc = vx_grid_last_stats(g, &s);
+    if (rc) return rc;
+    if (s.inserted > 0) g->maybe_oor = false;  // the dense clip ran
+    if (stats) *stats = s;
+    return VX_OK;
+}
+
+static int stamp_sets(vx_grid *g, int nsets, const int32_t *d_ijk, const int64_t *d_offsets,
+                      const double *d_origins, const double *d_vs, const double *d_T, float value,
+                      int64_t total) {
+    vx_ctx *c = g->ctx;
+    if (g->set_oob_cap < nsets) {
+        cudaFree(g->set_oob);
+        g->set_oob = nullptr;
+        VX_CUDA(cudaMalloc(&g->set_oob, sizeof(unsigned long long) * nsets));
+        g->set_oob_cap = nsets;
+    }
+    VX_CUDA(cudaMemsetAsync(g->set_oob, 0, sizeof(unsigned long long) * nsets, c->stream));
+    cudaError_t e = launch_stamp(d_ijk, d_offsets, nsets, d_origins, d_vs, d_T, g->g, g->cells, g->occ,
+                                 value, kOccThr, g->touched, g->ctr, g->set_oob, g->capacity, total,
+                                 c->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "stamp");
+    c->launches += total > 0 ? 2 : 1;
+    return VX_OK;
+}
+
+extern "C" int vx_grid_insert_voxel_sets(vx_grid *g, int nsets, const int32_t *const *ijk,
+                                         const int64_t *counts, const double *set_origins,
+                                         const double *set_vs, const double *T, float value,
+                                         int64_t *oob_out) {
+    if (!g || nsets < 0 || (nsets && (!ijk || !counts || !set_origins || !set_vs)))
+        return fail(VX_EINVAL, "NULL argument");
+    if (nsets == 0) return VX_OK;
+    vx_ctx *c = g->ctx;
+    std::vector<int64_t> off(nsets + 1, 0);
+    for (int s = 0; s < nsets; ++s) {
+        if (counts[s] < 0) return fail(VX_EINVAL, "negative voxel count");
+        if (!(set_vs[s] > 0.0)) return fail(VX_EINVAL, "voxel_size must be > 0");
+        off[s + 1] = off[s] + counts[s];
+    }
+    const int64_t total = off[nsets];
+    // one staging block: ijk | offsets | origins | vs | T
+    const size_t b_ijk = ((size_t)total * 3 * sizeof(int32_t) + 15) & ~(size_t)15;
+    const size_t b_off = (sizeof(int64_t) * (nsets + 1) + 15) & ~(size_t)15;
+    const size_t b_org = sizeof(double) * 3 * nsets, b_vs = sizeof(double) * nsets;
+    const size_t b_T = T ? sizeof(double) * 16 * nsets : 0;
+    std::vector<unsigned char> host(b_ijk + b_off + b_org + b_vs + b_T);
+    size_t pos = 0;
+    for (int s = 0; s < nsets; ++s) {
+        if (counts[s]) std::memcpy(host.data() + pos, ijk[s], counts[s] * 3 * sizeof(int32_t));
+        pos += counts[s] * 3 * sizeof(int32_t);
+    }
+    std::memcpy(host.data() + b_ijk, off.data(), sizeof(int64_t) * (nsets + 1));
+    std::memcpy(host.data() + b_ijk + b_off, set_origins, b_org);
+    std::memcpy(host.data() + b_ijk + b_off + b_org, set_vs, b_vs);
+    if (T) std::memcpy(host.data() + b_ijk + b_off + b_org + b_vs, T, b_T);
+    VX_CUDA(c->staging2.ensure(host.size()));
+    unsigned char *d = (unsigned char *)c->staging2.p;
+    VX_CUDA(cudaMemcpyAsync(d, host.data(), host.size(), cudaMemcpyHostToDevice, c->stream));
+    int rc = stamp_sets(g, nsets, (const int32_t *)d, (const int64_t *)(d + b_ijk),
+                        (const double *)(d + b_ijk + b_off), (const double *)(d + b_ijk + b_off + b_org),
+                        T ? (const double *)(d + b_ijk + b_off + b_org + b_vs) : nullptr, value, total);
+    if (rc) return rc;
+    std::vector<unsigned long long> oob(nsets);
+    VX_CUDA(cudaMemcpyAsync(oob.data(), g->set_oob, sizeof(unsigned long long) * nsets,
+                            cudaMemcpyDeviceToHost, c->stream));
+    VX_CUDA(cudaStreamSynchronize(c->stream));
+    if (oob_out)
+        for (int s = 0; s < nsets; ++s) oob_out[s] = (int64_t)oob[s];
+    return VX_OK;
+}
+
+extern "C" int vx_grid_read_cells(vx_grid *g, float *out) {
+    if (!g || !out) return fail(VX_EINVAL, "NULL argument");
+    VX_CUDA(cudaMemcpyAsync(out, g->cells, g->n * sizeof(float), cudaMemcpyDeviceToHost, g->ctx->stream));
+    VX_CUDA(cudaStreamSynchronize(g->ctx->stream));
+    return VX_OK;
+}
+
+extern "C" int vx_grid_write_cells(vx_grid *g, const float *in) {
+    if (!g || !in) return fail(VX_EINVAL, "NULL argument");
+    bool oor = false;
+    for (long long v = 0; v < g->n && !oor; ++v) oor = !(in[v] >= kLMin && in[v] <= kLMax);
+    VX_CUDA(cudaMemcpyAsync(g->cells, in, g->n * sizeof(float), cudaMemcpyHostToDevice, g->ctx->stream));
+    cudaError_t e = launch_occupancy(g->cells, g->occ, g->n, kOccThr, g->ctx->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "occupancy");
+    g->ctx->launches += 1;
+    g->sparse_ok = false;  // non-zero cells are no longer all on the touched list
+    g->maybe_oor = g->maybe_oor || oor;
+    VX_CUDA(cudaStreamSynchronize(g->ctx->stream));
+    return VX_OK;
+}
+
+// device occupancy at `thr` (cached array when thr is the 0.5 default)
+static int grid_occ_device(vx_grid *g, double thr, const uint8_t **out) {
+    const float thr32 = (float)logit(thr);
+    if (thr32 == kOccThr) {
+        *out = g->occ;
+        return VX_OK;
+    }
+    vx_ctx *c = g->ctx;
+    VX_CUDA(c->temp.ensure(g->n));
+    cudaError_t e = launch_occupancy(g->cells, (uint8_t *)c->temp.p, g->n, thr32, c->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "occupancy");
+    c->launches += 1;
+    *out = (const uint8_t *)c->temp.p;
+    return VX_OK;
+}
+
+extern "C" int vx_grid_occupancy(vx_grid *g, double thr, uint8_t *out) {
+    if (!g || !out) return fail(VX_EINVAL, "NULL argument");
+    const uint8_t *d = nullptr;
+    int rc = grid_occ_device(g, thr, &d);
+    if (rc) return rc;
+    VX_CUDA(cudaMemcpyAsync(out, d, g->n, cudaMemcpyDeviceToHost, g->ctx->stream));
+    VX_CUDA(cudaStreamSynchronize(g->ctx->stream));
+    return VX_OK;
+}
+
+// ---- EDT ----------------------------------------------------------------------
+static int check_edt_dims(int nx, int ny, int nz) {
+    if (nx <= 0 || ny <= 0 || nz <= 0) return fail(VX_EINVAL, "occupancy must be a non-empty 3D array");
+    if (nx > (1 << 20) || ny > (1 << 20) || nz > (1 << 20))   // edt.py:29, 459-460
+        return fail(VX_EINVAL, "grid extent too large for integer-exact transform");
+    if ((long long)nx * ny * nz >= (1LL << 31))
+        return fail(VX_EINVAL, "grid too large for 32-bit site indices");
+    return VX_OK;
+}
+
+static int field_new(vx_ctx *c, int nx, int ny, int nz, vx_field **out) {
+    vx_field *f = new vx_field;
+    f->ctx = c;
+    f->nx = nx; f->ny = ny; f->nz = nz;
+    cudaError_t e = cudaMalloc(&f->site, (size_t)nx * ny * nz * sizeof(int32_t));
+    if (e != cudaSuccess) {
+        delete f;
+        return cuda_fail(e, "cudaMalloc(site)");
+    }
+    *out = f;
+    return VX_OK;
+}
+
+static int edt_run(vx_ctx *c, const uint8_t *d_occ, int nx, int ny, int nz, int nscenes, int32_t *d_site,
+                   void *scratch, size_t scratch_bytes) {
+    EdtPlan p;
+    if (!make_plan(nx, ny, nz, &p, 0)) return fail(VX_EINVAL, "bad EDT shape");
+    const size_t need = scratch_bytes_for(p, nscenes);
+    if (!scratch) {
+        VX_CUDA(c->scratch.ensure(need));
+        scratch = c->scratch.p;
+    } else if (scratch_bytes < need) {
+        return fail(VX_EINVAL, "EDT scratch too small: %zu < %zu", scratch_bytes, need);
+    }
+    cudaError_t e = edt_device_batched(d_occ, d_site, scratch, p, nscenes, c->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "edt");
+    c->launches += 3;
+    return VX_OK;
+}
+
+extern "C" size_t vx_edt_scratch_bytes(int nx, int ny, int nz, int nscenes) {
+    EdtPlan p;
+    if (!make_plan(nx, ny, nz, &p, 0) || nscenes <= 0) return 0;
+    return scratch_bytes_for(p, nscenes);
+}
+
+extern "C" int vx_edt(vx_ctx *c, const uint8_t *occ, int nx, int ny, int nz, double vs, vx_field **out) {
+    (void)vs;
+    if (!c || !occ || !out) return fail(VX_EINVAL, "NULL argument");
+    int rc = check_edt_dims(nx, ny, nz);
+    if (rc) return rc;
+    const size_t n = (size_t)nx * ny * nz;
+    VX_CUDA(c->staging.ensure(n));
+    VX_CUDA(cudaMemcpyAsync(c->staging.p, occ, n, cudaMemcpyHostToDevice, c->stream));
+    vx_field *f = nullptr;
+    rc = field_new(c, nx, ny, nz, &f);
+    if (rc) return rc;
+    rc = edt_run(c, (const uint8_t *)c->staging.p, nx, ny, nz, 1, f->site, nullptr, 0);
+    if (rc) {
+        vx_field_destroy(f);
+        return rc;
+    }
+    *out = f;
+    return VX_OK;
+}
+
+extern "C" int vx_edt_grid(vx_grid *g, double thr, vx_field **out) {
+    if (!g || !out) return fail(VX_EINVAL, "NULL argument");
+    const uint8_t *d = nullptr;
+    int rc = grid_occ_device(g, thr, &d);
+    if (rc) return rc;
+    vx_field *f = nullptr;
+    rc = field_new(g->ctx, g->g.nx, g->g.ny, g->g.nz, &f);
+    if (rc) return rc;
+    rc = edt_run(g->ctx, d, g->g.nx, g->g.ny, g->g.nz, 1, f->site, nullptr, 0);
+    if (rc) {
+        vx_field_destroy(f);
+        return rc;
+    }
+    *out = f;
+    return VX_OK;
+}
+
+extern "C" int vx_line_nearest_sites(vx_ctx *c, const uint8_t *occ, int nx, int ny, int nz, int32_t *s1) {
+    if (!c || !occ || !s1) return fail(VX_EINVAL, "NULL argument");
+    int rc = check_edt_dims(nx, ny, nz);
+    if (rc) return rc;
+    const size_t n = (size_t)nx * ny * nz;
+    VX_CUDA(c->staging.ensure(n));
+    VX_CUDA(c->temp.ensure(n * 4 + 16));
+    VX_CUDA(cudaMemcpyAsync(c->staging.p, occ, n, cudaMemcpyHostToDevice, c->stream));
+    cudaError_t e = launch_pass1((const uint8_t *)c->staging.p, (int32_t *)c->temp.p, nx, ny, nz, c->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "pass1");
+    c->launches += 1;
+    VX_CUDA(cudaMemcpyAsync(s1, c->temp.p, n * 4, cudaMemcpyDeviceToHost, c->stream));
+    VX_CUDA(cudaStreamSynchronize(c->stream));
+    return VX_OK;
+}
+
+extern "C" int vx_field_destroy(vx_field *f) {
+    if (!f) return VX_OK;
+    if (f->owned) {
+        if (f->ctx) cudaStreamSynchronize(f->ctx->stream);
+        cudaFree(f->site);
+        delete f;
+    }
+    return VX_OK;
+}
+
+extern "C" int vx_field_dims(const vx_field *f, int dims[3]) {
+    if (!f || !dims) return fail(VX_EINVAL, "NULL argument");
+    dims[0] = f->nx; dims[1] = f->ny; dims[2] = f->nz;
+    return VX_OK;
+}
+
+extern "C" int vx_field_read_site(vx_field *f, int32_t *out) {
+    if (!f || !out) return fail(VX_EINVAL, "NULL argument");
+    const size_t n = (size_t)f->nx * f->ny * f->nz;
+    VX_CUDA(cudaMemcpyAsync(out, f->site, n * 4, cudaMemcpyDeviceToHost, f->ctx->stream));
+    VX_CUDA(cudaStreamSynchronize(f->ctx->stream));
+    return VX_OK;
+}
+
+extern "C" int vx_field_site_at(vx_field *f, int64_t i, int64_t j, int64_t k, int32_t *out) {
+    if (!f || !out) return fail(VX_EINVAL, "NULL argument");
+    if (!(0 <= i && i < f->nx && 0 <= j && j < f->ny && 0 <= k && k < f->nz))
+        return fail(VX_ERANGE, "voxel (%lld, %lld, %lld) outside grid (%d, %d, %d)", (long long)i,
+                    (long long)j, (long long)k, f->nx, f->ny, f->nz);
+    const size_t off = ((size_t)i * f->ny + j) * f->nz + k;
+    VX_CUDA(cudaMemcpyAsync(out, f->site + off, 4, cudaMemcpyDeviceToHost, f->ctx->stream));
+    VX_CUDA(cudaStreamSynchronize(f->ctx->stream));
+    return VX_OK;
+}
+
+extern "C" int vx_field_site_world(vx_field *f, const double origin[3], double vs, const double *centers,
+                                   int64_t s, int32_t *lin, double *world, double *dist) {
+    if (!f || !origin || (s > 0 && (!centers || !lin || !world || !dist)))
+        return fail(VX_EINVAL, "NULL argument");
+    if (s <= 0) return VX_OK;
+    vx_ctx *c = f->ctx;
+    const size_t bc = (size_t)s * 3 * sizeof(double);
+    const size_t bl = ((size_t)s * 4 + 15) & ~(size_t)15;
+    VX_CUDA(c->temp.ensure(bc + bl + bc + (size_t)s * 8));
+    unsigned char *d = (unsigned char *)c->temp.p;
+    VX_CUDA(cudaMemcpyAsync(d, centers, bc, cudaMemcpyHostToDevice, c->stream));
+    GridGeom g{f->nx, f->ny, f->nz, vs, origin[0], origin[1], origin[2]};
+    cudaError_t e = launch_site_world(f->site, g, (const double *)d, (int)s, (int32_t *)(d + bc),
+                                      (double *)(d + bc + bl), (double *)(d + bc + bl + bc), c->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "site_world");
+    c->launches += 1;
+    VX_CUDA(cudaMemcpyAsync(lin, d + bc, (size_t)s * 4, cudaMemcpyDeviceToHost, c->stream));
+    VX_CUDA(cudaMemcpyAsync(world, d + bc + bl, bc, cudaMemcpyDeviceToHost, c->stream));
+    VX_CUDA(cudaMemcpyAsync(dist, d + bc + bl + bc, (size_t)s * 8, cudaMemcpyDeviceToHost, c->stream));
+    VX_CUDA(cudaStreamSynchronize(c->stream));
+    return VX_OK;
+}
+
+// ---- device-pointer entry points -------------------------------------------------
+extern "C" int vx_edt_device(vx_ctx *c, const uint8_t *d_occ, int nx, int ny, int nz, int nscenes,
+                             int32_t *d_site, void *d_scratch, size_t scratch_bytes) {
+    if (!c || !d_occ || !d_site || nscenes <= 0) return fail(VX_EINVAL, "bad argument");
+    int rc = check_edt_dims(nx, ny, nz);
+    if (rc) return rc;
+    return edt_run(c, d_occ, nx, ny, nz, nscenes, d_site, d_scratch, scratch_bytes);
+}
+
+extern "C" int vx_edt_s2_bytes(int nx, int ny, int nz) {
+    EdtPlan p;
+    if (!make_plan(nx, ny, nz, &p, 0)) return 0;
+    return p.s2_wide ? 8 : 4;
+}
+
+extern "C" int vx_edt_pass12_device(vx_ctx *c, const uint8_t *d_occ, int nx, int ny, int nz, int nxl,
+                                    void *d_s2, void *d_scratch, size_t scratch_bytes) {
+    if (!c || !d_occ || !d_s2 || nxl < 0 || nxl > nx) return fail(VX_EINVAL, "bad argument");
+    int rc = check_edt_dims(nx, ny, nz);
+    if (rc) return rc;
+    EdtPlan p;
+    make_plan(nx, ny, nz, &p, 0);
+    const size_t s1b = ((size_t)nxl * ny * nz * 4 + 255) & ~(size_t)255;
+    const size_t need = s1b + p.gstack_bytes;
+    if (!d_scratch) {
+        VX_CUDA(c->scratch.ensure(need));
+        d_scratch = c->scratch.p;
+    } else if (scratch_bytes < need) {
+        return fail(VX_EINVAL, "scratch too small");
+    }
+    int32_t *s1 = (int32_t *)d_scratch;
+    cudaError_t e = launch_pass1(d_occ, s1, nxl, ny, nz, c->stream);
+    if (e == cudaSuccess) e = launch_pass2(s1, d_s2, (unsigned char *)d_scratch + s1b, p, nxl, c->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "pass12");
+    c->launches += 2;
+    return VX_OK;
+}
+
+extern "C" int vx_edt_pass3_device(vx_ctx *c, const void *d_s2, int nx, int ny, int nz, int j0, int nyl,
+                                   int32_t *d_site, void *d_scratch, size_t scratch_bytes) {
+    if (!c || !d_s2 || !d_site || j0 < 0 || nyl < 0 || j0 + nyl > ny) return fail(VX_EINVAL, "bad argument");
+    int rc = check_edt_dims(nx, ny, nz);
+    if (rc) return rc;
+    EdtPlan p;
+    make_plan(nx, ny, nz, &p, 0);
+    if (p.gstack_bytes) {
+        if (!d_scratch) {
+            VX_CUDA(c->scratch.ensure(p.gstack_bytes));
+            d_scratch = c->scratch.p;
+        } else if (scratch_bytes < p.gstack_bytes) {
+            return fail(VX_EINVAL, "scratch too small");
+        }
+    }
+    cudaError_t e = launch_pass3(d_s2, d_site, d_scratch, p, 1, j0, nyl, c->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "pass3");
+    c->launches += 1;
+    return VX_OK;
+}
+
+// ---- camera-tick pipeline (engine.py:233-280) ----------------------------------------
+struct vx_cycle {
+    vx_ctx *ctx = nullptr;
+    vx_grid *env = nullptr, *self = nullptr, *mask = nullptr;
+    vx_field env_f, self_f;
+    int nlinks = 0, nself = 0;
+    int64_t total_all = 0, total_self = 0, max_points = 0;
+    int max_spheres = 0;
+    // device tables: all links, then the self-obstacle subset
+    unsigned char *tab = nullptr;
+    int32_t *ijk_all = nullptr, *ijk_self = nullptr;
+    int64_t *off_all = nullptr, *off_self = nullptr;
+    double *org_all = nullptr, *org_self = nullptr, *vs_all = nullptr, *vs_self = nullptr;
+    double *T_all = nullptr, *T_self = nullptr;
+    std::vector<int> self_links;
+    // per-step buffers
+    double *d_pts = nullptr, *d_centers = nullptr;
+    int32_t *d_lin = nullptr;
+    double *d_world = nullptr, *d_dist = nullptr;
+    void *scratch = nullptr;
+    size_t scratch_bytes = 0;
+    EdtPlan plan{};
+    std::vector<double> last_self_T;
+    bool self_valid = false;
+    int last_s = 0;
+    int self_recomputed = 0;
+};
+
+extern "C" int vx_cycle_create(vx_ctx *c, int nx, int ny, int nz, double vs, const double origin[3],
+                               int nlinks, const int32_t *const *link_ijk, const int64_t *link_counts,
+                               const double *link_origins, double link_vs, const int32_t *self_links,
+                               int n_self, int64_t max_points, int max_spheres, vx_cycle **out) {
+    if (!c || !out || nlinks < 0 || n_self < 0 || max_points < 0 || max_spheres < 0)
+        return fail(VX_EINVAL, "bad argument");
+    int rc = check_geom(nx, ny, nz, vs);
+    if (rc) return rc;
+    for (int s = 0; s < n_self; ++s)
+        if (self_links[s] < 0 || self_links[s] >= nlinks) return fail(VX_EINVAL, "bad self link index");
+    vx_cycle *cy = new vx_cycle;
+    cy->ctx = c;
+    cy->nlinks = nlinks;
+    cy->nself = n_self;
+    cy->self_links.assign(self_links, self_links + n_self);
+    cy->max_points = max_points;
+    cy->max_spheres = max_spheres;
+    auto bail = [&](int code) {
+        vx_cycle_destroy(cy);
+        return code;
+    };
+    if ((rc = vx_grid_create(c, nx, ny, nz, vs, origin, &cy->env))) return bail(rc);
+    if ((rc = vx_grid_create(c, nx, ny, nz, vs, origin, &cy->self))) return bail(rc);
+    if ((rc = vx_grid_create(c, nx, ny, nz, vs, origin, &cy->mask))) return bail(rc);
+    // link tables
+    std::vector<int64_t> off_all(nlinks + 1, 0), off_self(n_self + 1, 0);
+    for (int l = 0; l < nlinks; ++l) off_all[l + 1] = off_all[l] + link_counts[l];
+    for (int s = 0; s < n_self; ++s) off_self[s + 1] = off_self[s] + link_counts[self_links[s]];
+    cy->total_all = off_all[nlinks];
+    cy->total_self = off_self[n_self];
+    auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
+    const size_t b_ia = al(cy->total_all * 12), b_is = al(cy->total_self * 12);
+    const size_t b_oa = al(8 * (nlinks + 1)), b_os = al(8 * (n_self + 1));
+    const size_t b_ga = al(24 * nlinks + 8), b_gs = al(24 * n_self + 8);
+    const size_t b_va = al(8 * nlinks + 8), b_vs = al(8 * n_self + 8);
+    const size_t b_Ta = al(128 * nlinks + 8), b_Ts = al(128 * n_self + 8);
+    const size_t tab_bytes = b_ia + b_is + b_oa + b_os + b_ga + b_gs + b_va + b_vs + b_Ta + b_Ts;
+    std::vector<unsigned char> h(tab_bytes, 0);
+    size_t p = 0;
+    auto place = [&](size_t bytes) { size_t q = p; p += bytes; return q; };
+    const size_t o_ia = place(b_ia), o_is = place(b_is), o_oa = place(b_oa), o_os = place(b_os);
+    const size_t o_ga = place(b_ga), o_gs = place(b_gs), o_va = place(b_va), o_vs = place(b_vs);
+    const size_t o_Ta = place(b_Ta), o_Ts = place(b_Ts);
+    for (int l = 0; l < nlinks; ++l) {
+        if (link_counts[l]) std::memcpy(&h[o_ia + off_all[l] * 12], link_ijk[l], link_counts[l] * 12);
+        std::memcpy(&h[o_ga + 24 * l], link_origins + 3 * l, 24);
+        std::memcpy(&h[o_va + 8 * l], &link_vs, 8);
+    }
+    for (int s = 0; s < n_self; ++s) {
+        const int l = self_links[s];
+        if (link_counts[l]) std::memcpy(&h[o_is + off_self[s] * 12], link_ijk[l], link_counts[l] * 12);
+        std::memcpy(&h[o_gs + 24 * s], link_origins + 3 * l, 24);
+        std::memcpy(&h[o_vs + 8 * s], &link_vs, 8);
+    }
+    std::memcpy(&h[o_oa], off_all.data(), 8 * (nlinks + 1));
+    std::memcpy(&h[o_os], off_self.data(), 8 * (n_self + 1));
+    cudaError_t e = cudaMalloc(&cy->tab, tab_bytes);
+    if (e == cudaSuccess) e = cudaMemcpy(cy->tab, h.data(), tab_bytes, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return bail(cuda_fail(e, "cycle tables"));
+    cy->ijk_all = (int32_t *)(cy->tab + o_ia); cy->ijk_self = (int32_t *)(cy->tab + o_is);
+    cy->off_all = (int64_t *)(cy->tab + o_oa); cy->off_self = (int64_t *)(cy->tab + o_os);
+    cy->org_all = (double *)(cy->tab + o_ga); cy->org_self = (double *)(cy->tab + o_gs);
+    cy->vs_all = (double *)(cy->tab + o_va); cy->vs_self = (double *)(cy->tab + o_vs);
+    cy->T_all = (double *)(cy->tab + o_Ta); cy->T_self = (double *)(cy->tab + o_Ts);
+    // per-step buffers
+    const size_t S = (size_t)(max_spheres > 0 ? max_spheres : 1);
+    if (e == cudaSuccess) e = cudaMalloc(&cy->d_pts, (size_t)(max_points > 0 ? max_points : 1) * 24);
+    if (e == cudaSuccess) e = cudaMalloc(&cy->d_centers, S * 24);
+    if (e == cudaSuccess) e = cudaMalloc(&cy->d_lin, 2 * S * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&cy->d_world, 2 * S * 24);
+    if (e == cudaSuccess) e = cudaMalloc(&cy->d_dist, 2 * S * 8);
+    for (vx_field *f : {&cy->env_f, &cy->self_f}) {
+        f->ctx = c;
+        f->nx = nx; f->ny = ny; f->nz = nz;
+        f->owned = false;
+        if (e == cudaSuccess) e = cudaMalloc(&f->site, (size_t)nx * ny * nz * 4);
+    }
+    if (e != cudaSuccess) return bail(cuda_fail(e, "cycle buffers"));
+    make_plan(nx, ny, nz, &cy->plan, 0);
+    cy->scratch_bytes = scratch_bytes_for(cy->plan, 1);
+    e = cudaMalloc(&cy->scratch, cy->scratch_bytes);
+    if (e != cudaSuccess) return bail(cuda_fail(e, "cycle scratch"));
+    *out = cy;
+    return VX_OK;
+}
+
+extern "C" int vx_cycle_destroy(vx_cycle *cy) {
+    if (!cy) return VX_OK;
+    if (cy->ctx) cudaStreamSynchronize(cy->ctx->stream);
+    vx_grid_destroy(cy->env);
+    vx_grid_destroy(cy->self);
+    vx_grid_destroy(cy->mask);
+    cudaFree(cy->tab);
+    cudaFree(cy->d_pts);
+    cudaFree(cy->d_centers);
+    cudaFree(cy->d_lin);
+    cudaFree(cy->d_world);
+    cudaFree(cy->d_dist);
+    cudaFree(cy->env_f.site);
+    cudaFree(cy->self_f.site);
+    cudaFree(cy->scratch);
+    delete cy;
+    return VX_OK;
+}
+
+extern "C" int vx_cycle_step(vx_cycle *cy, const double *pts, int64_t npts, const double *link_T, float hit,
+                             double thr, const double *centers, int s, int sync) {
+    if (!cy || npts < 0 || npts > cy->max_points || s < 0 || s > cy->max_spheres ||
+        (npts && !pts) || (s && !centers) || (cy->nlinks && !link_T))
+        return fail(VX_EINVAL, "bad argument (npts %lld of max %lld, spheres %d of max %d)",
+                    (long long)npts, (long long)cy->max_points, s, cy->max_spheres);
+    vx_ctx *c = cy->ctx;
+    cudaStream_t st = c->stream;
+    int rc;
+    // H2D: FK frames of every link, the self subset, the cloud, the centres
+    if (cy->nlinks) VX_CUDA(cudaMemcpyAsync(cy->T_all, link_T, 128 * cy->nlinks, cudaMemcpyHostToDevice, st));
+    std::vector<double> Ts(16 * cy->nself);
+    for (int q = 0; q < cy->nself; ++q) std::memcpy(&Ts[16 * q], link_T + 16 * cy->self_links[q], 128);
+    if (npts) VX_CUDA(cudaMemcpyAsync(cy->d_pts, pts, (size_t)npts * 24, cudaMemcpyHostToDevice, st));
+    if (s) VX_CUDA(cudaMemcpyAsync(cy->d_centers, centers, (size_t)s * 24, cudaMemcpyHostToDevice, st));
+    // self map: memo on the self-obstacle transforms (engine.py:259-268 skips
+    // the EDT when the occupancy is unchanged; equal transforms => equal
+    // occupancy, since the stamp is deterministic)
+    cy->self_recomputed = 0;
+    if (!cy->self_valid || Ts != cy->last_self_T) {
+        if (cy->nself) VX_CUDA(cudaMemcpyAsync(cy->T_self, Ts.data(), 128 * cy->nself, cudaMemcpyHostToDevice, st));
+        if ((rc = grid_clear_async(cy->self))) return rc;
+        if (cy->nself && (rc = stamp_sets(cy->self, cy->nself, cy->ijk_self, cy->off_self, cy->org_self,
+                                          cy->vs_self, cy->T_self, kLMax, cy->total_self)))
+            return rc;
+        cudaError_t e = edt_device(cy->self->occ, cy->self_f.site, cy->scratch, cy->plan, st);
+        if (e != cudaSuccess) return cuda_fail(e, "edt(self)");
+        c->launches += 3;
+        cy->last_self_T = Ts;
+        cy->self_valid = true;
+        cy->self_recomputed = 1;
+    }
+    // mask <- all links; env <- cloud minus mask  (engine.py:236-254)
+    if ((rc = grid_clear_async(cy->mask))) return rc;
+    if (cy->nlinks && (rc = stamp_sets(cy->mask, cy->nlinks, cy->ijk_all, cy->off_all, cy->org_all, cy->vs_all,
+                                       cy->T_all, kLMax, cy->total_all)))
+        return rc;
+    if ((rc = grid_clear_async(cy->env))) return rc;
+    if (npts && (rc = insert_device(cy->env, cy->d_pts, npts, nullptr, hit, thr, cy->mask))) return rc;
+    if (!npts) VX_CUDA(cudaMemsetAsync(cy->env->ctr, 0, 3 * sizeof(unsigned long long), st));
+    cudaError_t e = edt_device(cy->env->occ, cy->env_f.site, cy->scratch, cy->plan, st);
+    if (e != cudaSuccess) return cuda_fail(e, "edt(env)");
+    c->launches += 3;
+    // per-sphere gather on both fields (engine.py:272-280)
+    const GridGeom g = cy->env->g;
+    e = launch_site_world(cy->env_f.site, g, cy->d_centers, s, cy->d_lin, cy->d_world, cy->d_dist, st);
+    if (e == cudaSuccess)
+        e = launch_site_world(cy->self_f.site, g, cy->d_centers, s, cy->d_lin + s, cy->d_world + 3 * s,
+                              cy->d_dist + s, st);
+    if (e != cudaSuccess) return cuda_fail(e, "site_world");
+    c->launches += s ? 2 : 0;
+    cy->last_s = s;
+    if (sync) VX_CUDA(cudaStreamSynchronize(st));
+    return VX_OK;
+}
+
+extern "C" int vx_cycle_wait(vx_cycle *cy, vx_cycle_result *res, int32_t *lin, double *world, double *dist) {
+    if (!cy) return fail(VX_EINVAL, "NULL cycle");
+    cudaStream_t st = cy->ctx->stream;
+    const int s = cy->last_s;
+    if (s && lin) VX_CUDA(cudaMemcpyAsync(lin, cy->d_lin, (size_t)2 * s * 4, cudaMemcpyDeviceToHost, st));
+    if (s && world) VX_CUDA(cudaMemcpyAsync(world, cy->d_world, (size_t)2 * s * 24, cudaMemcpyDeviceToHost, st));
+    if (s && dist) VX_CUDA(cudaMemcpyAsync(dist, cy->d_dist, (size_t)2 * s * 8, cudaMemcpyDeviceToHost, st));
+    if (res) {
+        DevCounters h;
+        VX_CUDA(cudaMemcpyAsync(&h, cy->env->ctr, sizeof h, cudaMemcpyDeviceToHost, st));
+        VX_CUDA(cudaStreamSynchronize(st));
+        res->stats = vx_insert_stats{(int64_t)h.inserted, 0, (int64_t)h.skipped, (int64_t)h.oob};
+        res->self_recomputed = cy->self_recomputed;
+    }
+    VX_CUDA(cudaStreamSynchronize(st));
+    return VX_OK;
+}
+
+extern "C" int vx_cycle_fields(vx_cycle *cy, vx_field **env, vx_field **self_field) {
+    if (!cy) return fail(VX_EINVAL, "NULL cycle");
+    if (env) *env = &cy->env_f;
+    if (self_field) *self_field = &cy->self_f;
+    return VX_OK;
+}
+
+extern "C" int vx_cycle_grids(vx_cycle *cy, vx_grid **env, vx_grid **self_grid, vx_grid **mask) {
+    if (!cy) return fail(VX_EINVAL, "NULL cycle");
+    if (env) *env = cy->env;
+    if (self_grid) *self_grid = cy->self;
+    if (mask) *mask = cy->mask;
+    return VX_OK;
+}

@@ -1,0 +1,696 @@
+// Exact 3D EDT with nearest-site index on sm_100a: three separable passes.
+//
+// Reference algorithm: voxarm edt.py (pkg/src/voxarm/edt.py)
+//   pass 1  _sweep_lines       edt.py:168-224  -> k_pass1_*      (K3)
+//   pass 2  _slice_transform   edt.py:227-317  -> k_column<2>    (K4)
+//   pass 3  _column_transform  edt.py:320-420  -> k_column<3>    (K5)
+//
+// The output is bit-identical to the reference `site` array.  The
+// reference's passes select, for every voxel, the lexicographically smallest
+// nearest occupied voxel (ties: lower k in pass 1 edt.py:221; pop-on->= in the
+// stacks edt.py:267-268; strict < in the query walk edt.py:311).  These
+// kernels keep the same pass order and the same integer comparisons:
+//   * pass 1: per line nearest occupied k, ties to the lower k;
+//   * passes 2/3: the stack of edt.py is the strict lower convex hull of the
+//     points (row, w + row^2).  That hull is unique, so building it as 32-row
+//     band hulls merged pairwise by bridge walks (all with the >= dominance
+//     test of edt.py:267) yields the same stack; each query then takes the
+//     FIRST hull vertex minimising (y - y_p)^2 + w_p, which is what the
+//     strict-< walk of edt.py:300-317 returns.
+//
+// Layout (C order, k fastest, flat index (i*ny + j)*nz + k as edt.py:417):
+//   occ  u8  N   -> s1  i32 N (nearest k or -1)
+//   s1   i32 N   -> s2  u32 N (y << zb | z, all-ones = none)   [u64 if wide]
+//   s2   u32 N   -> site i32 N (flat index, -1 = none)
+// Pass 1 is one warp per k-line with 16-byte vector I/O and warp scans.
+// Passes 2/3: a CTA owns 32 consecutive k columns (one warp = 32 columns, so
+// every global load/store is a 128-byte coalesced row segment) and B bands
+// along the column (one warp per band).  Band stacks live in shared memory,
+// laid out [row][32 columns] so each lane owns one bank.
+#include "vx_internal.cuh"
+
+#include <algorithm>
+#include <type_traits>
+#include <cstdlib>
+
+namespace vx {
+namespace {
+
+constexpr int BIG = 0x7fffffff;
+
+// bit e (e = 0..3) set iff byte e of w is non-zero
+__device__ __forceinline__ uint32_t nibble4(uint32_t w) {
+    const uint32_t t = __vcmpne4(w, 0u);
+    return (((t & 0x01010101u) * 0x01020408u) >> 24) & 0xfu;
+}
+
+__device__ __forceinline__ int pick(int k, int l, int r) {
+    // edt.py:217-224: l if k-l <= r-k (ties -> lower k)
+    if (l < 0) return r == BIG ? -1 : r;
+    if (r == BIG) return l;
+    return (k - l <= r - k) ? l : r;
+}
+
+// ---------------------------------------------------------------------------
+// Pass 1, vector path: nz % 4 == 0, nz <= 128 * CMAX.  One warp per line;
+// lane owns 4 consecutive voxels of each 128-voxel chunk.
+// ---------------------------------------------------------------------------
+template <int CMAX>
+__global__ void __launch_bounds__(256) k_pass1_v4(const uint8_t *__restrict__ occ,
+                                                  int32_t *__restrict__ s1,
+                                                  long long nlines, int nz) {
+    const int lane = threadIdx.x & 31;
+    const long long line = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (line >= nlines) return;  // warp-uniform
+    const uint32_t *src = reinterpret_cast<const uint32_t *>(occ + line * nz);
+    int4 *dst = reinterpret_cast<int4 *>(s1 + line * nz);
+    const int nq = nz >> 2;
+    uint32_t nib[CMAX];
+#pragma unroll
+    for (int c = 0; c < CMAX; ++c) {
+        const int q = c * 32 + lane;
+        nib[c] = nibble4(q < nq ? __ldg(src + q) : 0u);
+    }
+    // forward: exclusive prefix max of the last occupied k
+    int exl[CMAX];
+    int carry = -1;
+#pragma unroll
+    for (int c = 0; c < CMAX; ++c) {
+        const int base = (c * 32 + lane) * 4;
+        int v = nib[c] ? base + 31 - __clz(nib[c]) : -1;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int o = __shfl_up_sync(VX_FULL_MASK, v, d);
+            if (lane >= d) v = max(v, o);
+        }
+        int ex = __shfl_up_sync(VX_FULL_MASK, v, 1);
+        if (lane == 0) ex = -1;
+        exl[c] = max(ex, carry);
+        carry = max(carry, __shfl_sync(VX_FULL_MASK, v, 31));
+    }
+    // backward: exclusive suffix min of the first occupied k, then combine
+    int carr = BIG;
+#pragma unroll
+    for (int c = CMAX - 1; c >= 0; --c) {
+        const int q = c * 32 + lane;
+        const int base = q * 4;
+        const uint32_t nb = nib[c];
+        int v = nb ? base + __ffs(nb) - 1 : BIG;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int o = __shfl_down_sync(VX_FULL_MASK, v, d);
+            if (lane + d < 32) v = min(v, o);
+        }
+        int ex = __shfl_down_sync(VX_FULL_MASK, v, 1);
+        if (lane == 31) ex = BIG;
+        const int exr = min(ex, carr);
+        carr = min(carr, __shfl_sync(VX_FULL_MASK, v, 0));
+        int lv[4];
+        int run = exl[c];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            if ((nb >> e) & 1u) run = base + e;
+            lv[e] = run;
+        }
+        int o[4];
+        run = exr;
+#pragma unroll
+        for (int e = 3; e >= 0; --e) {
+            if ((nb >> e) & 1u) run = base + e;
+            o[e] = pick(base + e, lv[e], run);
+        }
+        if (q < nq) dst[q] = make_int4(o[0], o[1], o[2], o[3]);
+    }
+}
+
+// Pass 1, generic path (any nz): 32-voxel chunks with ballots; the forward
+// sweep parks `l` in the output, the backward sweep combines.
+__global__ void __launch_bounds__(256) k_pass1_generic(const uint8_t *__restrict__ occ,
+                                                       int32_t *__restrict__ s1,
+                                                       long long nlines, int nz) {
+    const int lane = threadIdx.x & 31;
+    const long long line = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (line >= nlines) return;
+    const uint8_t *src = occ + line * nz;
+    int32_t *dst = s1 + line * nz;
+    int carry = -1;
+    for (int base = 0; base < nz; base += 32) {
+        const int k = base + lane;
+        const bool o = k < nz && src[k] != 0;
+        const uint32_t m = __ballot_sync(VX_FULL_MASK, o);
+        const uint32_t below = m & ((2u << lane) - 1u);
+        const int l = below ? base + 31 - __clz(below) : carry;
+        if (k < nz) dst[k] = l;
+        if (m) carry = base + 31 - __clz(m);
+    }
+    int carr = BIG;
+    for (int base = ((nz - 1) / 32) * 32; base >= 0; base -= 32) {
+        const int k = base + lane;
+        const bool o = k < nz && src[k] != 0;
+        const uint32_t m = __ballot_sync(VX_FULL_MASK, o);
+        const uint32_t above = m & (0xffffffffu << lane);
+        const int r = above ? base + __ffs(above) - 1 : carr;
+        if (k < nz) dst[k] = pick(k, dst[k], r);
+        if (m) carr = base + __ffs(m) - 1;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Passes 2 and 3: lower-envelope (strict lower hull) per column.
+// ---------------------------------------------------------------------------
+struct ColParams {
+    int nx, ny, nz;
+    int L;             // column length (ny for pass 2, nx for pass 3)
+    int B, W;          // bands per column, rows per band
+    int nkt;           // k tiles of 32
+    long long ntiles;  // total CTA tiles
+    int zb, yzb;       // packing shifts (narrow)
+    uint32_t zmask, ymask;
+    long long plane;   // ny * nz            (global; output flat index)
+    int nyl, j0;       // pass 3: rows of j held in this buffer and their offset
+    long long splane;  // nyl * nz           (pass-3 addressing stride along x)
+    long long nvox;    // nx * nyl * nz      (pass-3 scene stride)
+};
+
+template <int PASS, bool S2W, bool EW, bool FW>
+struct Col {
+    using S2T = typename std::conditional<S2W, unsigned long long, uint32_t>::type;
+    // pass 2: the stack entry is the s2 code itself; pass 3: (x, sy, sz)
+    using EntT = typename std::conditional<PASS == 2 ? S2W : EW, unsigned long long, uint32_t>::type;
+    using FT = typename std::conditional<FW, long long, int>::type;
+    using InT = typename std::conditional<PASS == 2, int32_t, S2T>::type;
+    using OutT = typename std::conditional<PASS == 2, S2T, int32_t>::type;
+
+    static __device__ __forceinline__ bool valid(InT v) {
+        if constexpr (PASS == 2) return v >= 0;
+        else return v != (S2T)~(S2T)0;
+    }
+    static __device__ __forceinline__ InT invalid() {
+        if constexpr (PASS == 2) return -1;
+        else return (S2T)~(S2T)0;
+    }
+    // pass-2 entry == the s2 code of the site (row y, line site z)
+    static __device__ __forceinline__ EntT make(const ColParams &P, InT v, int row) {
+        if constexpr (PASS == 2) {
+            if constexpr (S2W) return ((EntT)row << 32) | (EntT)(uint32_t)v;
+            else return ((EntT)row << P.zb) | (EntT)v;
+        } else {
+            uint32_t sy, sz;
+            if constexpr (S2W) { sy = (uint32_t)(v >> 32); sz = (uint32_t)v; }
+            else { sy = (uint32_t)v >> P.zb; sz = (uint32_t)v & P.zmask; }
+            if constexpr (EW) return ((EntT)row << 42) | ((EntT)sy << 21) | (EntT)sz;
+            else return ((EntT)row << P.yzb) | (EntT)v;
+        }
+    }
+    static __device__ __forceinline__ int row(const ColParams &P, EntT e) {
+        if constexpr (PASS == 2) {
+            if constexpr (S2W) return (int)(e >> 32);
+            else return (int)(e >> P.zb);
+        } else {
+            if constexpr (EW) return (int)(e >> 42);
+            else return (int)(e >> P.yzb);
+        }
+    }
+    // F = w + row^2 (edt.py:261-262, 362-364 fold the row term in at test time)
+    static __device__ __forceinline__ FT F(const ColParams &P, EntT e, int j, int k) {
+        if constexpr (PASS == 2) {
+            int y, z;
+            if constexpr (S2W) { y = (int)(e >> 32); z = (int)(uint32_t)e; }
+            else { y = (int)(e >> P.zb); z = (int)((uint32_t)e & P.zmask); }
+            const FT dz = (FT)(k - z);
+            return dz * dz + (FT)y * (FT)y;
+        } else {
+            int x, sy, sz;
+            if constexpr (EW) {
+                x = (int)(e >> 42); sy = (int)((e >> 21) & 0x1fffffull); sz = (int)(e & 0x1fffffull);
+            } else {
+                x = (int)(e >> P.yzb); sy = (int)(((uint32_t)e >> P.zb) & P.ymask);
+                sz = (int)((uint32_t)e & P.zmask);
+            }
+            const FT dy = (FT)(j - sy), dz = (FT)(k - sz);
+            return dy * dy + dz * dz + (FT)x * (FT)x;
+        }
+    }
+    static __device__ __forceinline__ OutT output(const ColParams &P, EntT e) {
+        if constexpr (PASS == 2) {
+            return (OutT)e;  // the entry is the s2 code
+        } else {
+            long long x, sy, sz;
+            if constexpr (EW) {
+                x = (long long)(e >> 42); sy = (long long)((e >> 21) & 0x1fffffull);
+                sz = (long long)(e & 0x1fffffull);
+            } else {
+                x = (long long)(e >> P.yzb); sy = (long long)(((uint32_t)e >> P.zb) & P.ymask);
+                sz = (long long)((uint32_t)e & P.zmask);
+            }
+            return (int32_t)(x * P.plane + sy * P.nz + sz);  // edt.py:417
+        }
+    }
+    static __device__ __forceinline__ OutT none() {
+        if constexpr (PASS == 2) return (OutT)~(OutT)0;
+        else return -1;
+    }
+};
+
+// b on or above segment a-c  ==> pop b   (edt.py:267-268, written with F=w+y^2)
+template <typename FT>
+__device__ __forceinline__ bool dominated(int ya, FT Fa, int yb, FT Fb, int yc, FT Fc) {
+    return (Fb - Fa) * (FT)(yc - yb) >= (Fc - Fb) * (FT)(yb - ya);
+}
+
+// succ strictly closer than cur at query row y (edt.py:311 strict <)
+template <typename FT>
+__device__ __forceinline__ bool better(int ys, FT Fs, int yp, FT Fp, int y) {
+    return Fs - Fp < (FT)2 * (FT)y * (FT)(ys - yp);
+}
+
+template <int PASS, bool S2W, bool EW, bool FW>
+__device__ __forceinline__ void column_tile(const typename Col<PASS, S2W, EW, FW>::InT *__restrict__ in,
+                                            typename Col<PASS, S2W, EW, FW>::OutT *__restrict__ out,
+                                            typename Col<PASS, S2W, EW, FW>::EntT *stk, int *meta,
+                                            const ColParams &P, long long tile) {
+    using C = Col<PASS, S2W, EW, FW>;
+    using EntT = typename C::EntT;
+    using FT = typename C::FT;
+    using InT = typename C::InT;
+
+    const int kk = threadIdx.x;
+    const int b = threadIdx.y;
+    const int kt = (int)(tile % P.nkt);
+    const long long outer = tile / P.nkt;
+    const int k = kt * 32 + kk;
+    const bool colok = k < P.nz;
+    long long base, stride;
+    int jq = 0;
+    if constexpr (PASS == 2) {  // outer = i (slices of every scene stack along i)
+        base = outer * P.plane + k;
+        stride = P.nz;
+    } else {                    // outer = scene * nyl + local j
+        const long long scene = outer / P.nyl;
+        const int jl = (int)(outer - scene * P.nyl);
+        jq = P.j0 + jl;          // global j: weights use global coordinates
+        base = scene * P.nvox + (long long)jl * P.nz + k;
+        stride = P.splane;
+    }
+    int *bs = meta;
+    int *be = bs + P.B * 32;
+    int *nbl = be + P.B * 32;
+    int *ncnt = nbl + P.B * 32;
+    const int lo = min(P.L, b * P.W);
+    const int hi = min(P.L, lo + P.W);
+
+    // ---- phase A: band-local hull (edt.py:253-276 for one band) ----------
+    int n = 0;
+    if (colok) {
+        int ya = 0, yb = 0;
+        FT Fa = 0, Fb = 0;
+        for (int y0 = lo; y0 < hi; y0 += 8) {
+            InT v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int y = y0 + u;
+                v[u] = (y < hi) ? __ldg(in + base + (long long)y * stride) : C::invalid();
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                if (!C::valid(v[u])) continue;
+                const int yc = y0 + u;
+                const EntT ec = C::make(P, v[u], yc);
+                const FT Fc = C::F(P, ec, jq, k);
+                while (n >= 2 && dominated<FT>(ya, Fa, yb, Fb, yc, Fc)) {
+                    --n;
+                    yb = ya;
+                    Fb = Fa;
+                    if (n >= 2) {
+                        const EntT t = stk[(size_t)(lo + n - 2) * 32 + kk];
+                        ya = C::row(P, t);
+                        Fa = C::F(P, t, jq, k);
+                    }
+                }
+                stk[(size_t)(lo + n) * 32 + kk] = ec;
+                ya = yb; Fa = Fb;
+                yb = yc; Fb = Fc;
+                ++n;
+            }
+        }
+    }
+    bs[b * 32 + kk] = lo;
+    be[b * 32 + kk] = lo + n;
+    __syncthreads();
+
+    // ---- phase B: pairwise bridge merges (same hull as edt.py:277-294) ---
+    for (int r = 1; r < P.B; r <<= 1) {
+        if (colok && (b & (2 * r - 1)) == r) {
+            const int gl = b - r, gm = b, ge = min(P.B, b + r);
+            int bl = gm - 1;
+            while (bl >= gl && bs[bl * 32 + kk] == be[bl * 32 + kk]) --bl;
+            int br = gm;
+            while (br < ge && bs[br * 32 + kk] == be[br * 32 + kk]) ++br;
+            if (bl >= gl && br < ge) {
+                int pl1 = be[bl * 32 + kk] - 1;
+                EntT e = stk[(size_t)pl1 * 32 + kk];
+                int yl1 = C::row(P, e);
+                FT Fl1 = C::F(P, e, jq, k);
+                int pr0 = bs[br * 32 + kk];
+                e = stk[(size_t)pr0 * 32 + kk];
+                int yr0 = C::row(P, e);
+                FT Fr0 = C::F(P, e, jq, k);
+                while (true) {
+                    while (true) {  // pop the left tail while dominated
+                        int bl2 = bl, pl2 = pl1 - 1;
+                        if (pl2 < bs[bl * 32 + kk]) {
+                            bl2 = bl - 1;
+                            while (bl2 >= gl && bs[bl2 * 32 + kk] == be[bl2 * 32 + kk]) --bl2;
+                            if (bl2 < gl) break;
+                            pl2 = be[bl2 * 32 + kk] - 1;
+                        }
+                        e = stk[(size_t)pl2 * 32 + kk];
+                        const int yl2 = C::row(P, e);
+                        const FT Fl2 = C::F(P, e, jq, k);
+                        if (!dominated<FT>(yl2, Fl2, yl1, Fl1, yr0, Fr0)) break;
+                        be[bl * 32 + kk] = pl1;
+                        bl = bl2; pl1 = pl2; yl1 = yl2; Fl1 = Fl2;
+                    }
+                    bool popped = false;
+                    while (true) {  // pop the right head while dominated
+                        int br2 = br, pr1 = pr0 + 1;
+                        if (pr1 >= be[br * 32 + kk]) {
+                            br2 = br + 1;
+                            while (br2 < ge && bs[br2 * 32 + kk] == be[br2 * 32 + kk]) ++br2;
+                            if (br2 >= ge) break;
+                            pr1 = bs[br2 * 32 + kk];
+                        }
+                        e = stk[(size_t)pr1 * 32 + kk];
+                        const int yr1 = C::row(P, e);
+                        const FT Fr1 = C::F(P, e, jq, k);
+                        if (!dominated<FT>(yl1, Fl1, yr0, Fr0, yr1, Fr1)) break;
+                        bs[br * 32 + kk] = pr0 + 1;
+                        br = br2; pr0 = pr1; yr0 = yr1; Fr0 = Fr1;
+                        popped = true;
+                    }
+                    if (!popped) break;
+                }
+            }
+        }
+        __syncthreads();
+    }
+
+    // ---- phase C: list of non-empty bands per column ---------------------
+    if (b == 0) {
+        int c = 0;
+        for (int q = 0; q < P.B; ++q)
+            if (bs[q * 32 + kk] < be[q * 32 + kk]) nbl[(c++) * 32 + kk] = q;
+        ncnt[kk] = c;
+    }
+    __syncthreads();
+
+    // ---- phase D: queries for this band's rows (edt.py:300-317) ----------
+    if (colok && lo < hi) {
+        const int cnt = ncnt[kk];
+        if (cnt == 0) {  // no candidate in the whole column (edt.py:295-299)
+            for (int y = lo; y < hi; ++y) out[base + (long long)y * stride] = C::none();
+        } else {
+            const int y0 = lo;
+            // first hull vertex minimising at y0: binary search over bands ...
+            int mlo = 0, mhi = cnt - 1;
+            while (mlo < mhi) {
+                const int mid = (mlo + mhi) >> 1;
+                const int bm = nbl[mid * 32 + kk], bn = nbl[(mid + 1) * 32 + kk];
+                const EntT a = stk[(size_t)(be[bm * 32 + kk] - 1) * 32 + kk];
+                const EntT s = stk[(size_t)bs[bn * 32 + kk] * 32 + kk];
+                if (better<FT>(C::row(P, s), C::F(P, s, jq, k), C::row(P, a), C::F(P, a, jq, k), y0))
+                    mlo = mid + 1;
+                else
+                    mhi = mid;
+            }
+            int m = mlo;
+            int bm = nbl[m * 32 + kk];
+            // ... then inside the band
+            int ilo = bs[bm * 32 + kk], ihi = be[bm * 32 + kk] - 1;
+            while (ilo < ihi) {
+                const int mid = (ilo + ihi) >> 1;
+                const EntT a = stk[(size_t)mid * 32 + kk];
+                const EntT s = stk[(size_t)(mid + 1) * 32 + kk];
+                if (better<FT>(C::row(P, s), C::F(P, s, jq, k), C::row(P, a), C::F(P, a, jq, k), y0))
+                    ilo = mid + 1;
+                else
+                    ihi = mid;
+            }
+            int pos = ilo;
+            int epos = be[bm * 32 + kk];
+            EntT cur = stk[(size_t)pos * 32 + kk];
+            int yc = C::row(P, cur);
+            FT Fc = C::F(P, cur, jq, k);
+            // successor
+            int spos = -1, sm = m;
+            if (pos + 1 < epos) spos = pos + 1;
+            else if (m + 1 < cnt) { sm = m + 1; spos = bs[nbl[sm * 32 + kk] * 32 + kk]; }
+            EntT sent = 0;
+            int ys = 0;
+            FT Fs = 0;
+            if (spos >= 0) {
+                sent = stk[(size_t)spos * 32 + kk];
+                ys = C::row(P, sent);
+                Fs = C::F(P, sent, jq, k);
+            }
+            for (int y = lo; y < hi; ++y) {
+                while (spos >= 0 && better<FT>(ys, Fs, yc, Fc, y)) {
+                    cur = sent; yc = ys; Fc = Fs; pos = spos;
+                    if (sm != m) { m = sm; epos = be[nbl[m * 32 + kk] * 32 + kk]; }
+                    if (pos + 1 < epos) spos = pos + 1;
+                    else if (m + 1 < cnt) { sm = m + 1; spos = bs[nbl[sm * 32 + kk] * 32 + kk]; }
+                    else spos = -1;
+                    if (spos >= 0) {
+                        sent = stk[(size_t)spos * 32 + kk];
+                        ys = C::row(P, sent);
+                        Fs = C::F(P, sent, jq, k);
+                    }
+                }
+                out[base + (long long)y * stride] = C::output(P, cur);
+            }
+        }
+    }
+}
+
+template <int PASS, bool S2W, bool EW, bool FW>
+__global__ void __launch_bounds__(1024) k_column_smem(const typename Col<PASS, S2W, EW, FW>::InT *__restrict__ in,
+                                                      typename Col<PASS, S2W, EW, FW>::OutT *__restrict__ out,
+                                                      const ColParams P) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    using EntT = typename Col<PASS, S2W, EW, FW>::EntT;
+    EntT *stk = reinterpret_cast<EntT *>(smem);
+    int *meta = reinterpret_cast<int *>(smem + (size_t)P.L * 32 * sizeof(EntT));
+    column_tile<PASS, S2W, EW, FW>(in, out, stk, meta, P, blockIdx.x);
+}
+
+// Columns too long for shared memory: per-CTA stack slab in global scratch,
+// persistent over tiles.
+template <int PASS, bool S2W, bool EW, bool FW>
+__global__ void __launch_bounds__(1024) k_column_gstack(const typename Col<PASS, S2W, EW, FW>::InT *__restrict__ in,
+                                                        typename Col<PASS, S2W, EW, FW>::OutT *__restrict__ out,
+                                                        typename Col<PASS, S2W, EW, FW>::EntT *gstack,
+                                                        const ColParams P) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    using EntT = typename Col<PASS, S2W, EW, FW>::EntT;
+    EntT *stk = gstack + (size_t)blockIdx.x * P.L * 32;
+    int *meta = reinterpret_cast<int *>(smem);
+    for (long long t = blockIdx.x; t < P.ntiles; t += gridDim.x) {
+        column_tile<PASS, S2W, EW, FW>(in, out, stk, meta, P, t);
+        __syncthreads();
+    }
+}
+
+int bits_of(long long v) {  // bits to hold values 0..v
+    int b = 0;
+    while (v > 0) { ++b; v >>= 1; }
+    return b;
+}
+
+int pow2ceil(int v) {
+    int p = 1;
+    while (p < v) p <<= 1;
+    return p;
+}
+
+constexpr size_t kSmemLimit = 227 * 1024;
+
+// pass 2: `outer` counts slices (nscenes * local nx); pass 3: `outer` counts
+// (scene, local j) with nyl rows of j starting at global row j0.
+ColParams col_params(const EdtPlan &p, int pass, long long nouter, int nyl, int j0) {
+    ColParams P;
+    P.nx = p.nx; P.ny = p.ny; P.nz = p.nz;
+    P.L = pass == 2 ? p.ny : p.nx;
+    P.B = pass == 2 ? p.B2 : p.B3;
+    P.W = pass == 2 ? p.W2 : p.W3;
+    P.nkt = (p.nz + 31) / 32;
+    P.ntiles = (long long)P.nkt * nouter;
+    P.nyl = nyl;
+    P.j0 = j0;
+    P.splane = (long long)nyl * p.nz;
+    P.zb = p.zb;
+    P.yzb = p.yb + p.zb;
+    P.zmask = p.zb >= 32 ? 0xffffffffu : ((1u << p.zb) - 1u);
+    P.ymask = p.yb >= 32 ? 0xffffffffu : ((1u << p.yb) - 1u);
+    P.plane = (long long)p.ny * p.nz;
+    P.nvox = P.splane * p.nx;
+    return P;
+}
+
+template <int PASS, bool S2W, bool EW, bool FW>
+cudaError_t launch_col(const void *in, void *out, void *gstack, const EdtPlan &p, long long nouter,
+                       int nyl, int j0, cudaStream_t st) {
+    using C = Col<PASS, S2W, EW, FW>;
+    const ColParams P = col_params(p, PASS, nouter, nyl, j0);
+    if (P.ntiles == 0) return cudaSuccess;
+    const dim3 block(32, P.B);
+    const bool gs = PASS == 2 ? p.gstack2 : p.gstack3;
+    const size_t smem = PASS == 2 ? p.smem2 : p.smem3;
+    if (!gs) {
+        auto kern = k_column_smem<PASS, S2W, EW, FW>;
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        kern<<<(unsigned)P.ntiles, block, smem, st>>>(
+            reinterpret_cast<const typename C::InT *>(in), reinterpret_cast<typename C::OutT *>(out), P);
+    } else {
+        auto kern = k_column_gstack<PASS, S2W, EW, FW>;
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        const long long g = std::min<long long>(P.ntiles, p.gstack_ctas);
+        kern<<<(unsigned)g, block, smem, st>>>(reinterpret_cast<const typename C::InT *>(in),
+                                              reinterpret_cast<typename C::OutT *>(out),
+                                              reinterpret_cast<typename C::EntT *>(gstack), P);
+    }
+    return cudaGetLastError();
+}
+
+template <int PASS>
+cudaError_t dispatch_col(const void *in, void *out, void *gstack, const EdtPlan &p, long long nouter,
+                         int nyl, int j0, cudaStream_t st) {
+    // narrow: u32 s2, u32 entries, int weights (the 512^3 path)
+    if (!p.s2_wide && !p.e3_wide && !p.fwide)
+        return launch_col<PASS, false, false, false>(in, out, gstack, p, nouter, nyl, j0, st);
+    if (!p.s2_wide && !p.e3_wide && p.fwide)
+        return launch_col<PASS, false, false, true>(in, out, gstack, p, nouter, nyl, j0, st);
+    if (!p.s2_wide && p.e3_wide)
+        return launch_col<PASS, false, true, true>(in, out, gstack, p, nouter, nyl, j0, st);
+    return launch_col<PASS, true, true, true>(in, out, gstack, p, nouter, nyl, j0, st);
+}
+
+}  // namespace
+
+int num_sms() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
+bool make_plan(int nx, int ny, int nz, EdtPlan *p, int force_global_stack) {
+    if (nx <= 0 || ny <= 0 || nz <= 0) return false;
+    EdtPlan q{};
+    q.nx = nx; q.ny = ny; q.nz = nz;
+    q.xb = bits_of(nx - 1);
+    q.yb = bits_of(ny - 1);
+    q.zb = bits_of(nz - 1);
+    // test hooks: VX_FORCE_WIDE=1|2|3 selects the wider code paths on small
+    // grids (1: int64 weights, 2: +u64 pass-3 entries, 3: +u64 s2 codes);
+    // VX_FORCE_GSTACK=1 puts the column stacks in global memory
+    const char *fw = getenv("VX_FORCE_WIDE");
+    const int force_wide = fw ? atoi(fw) : 0;
+    const char *fg = getenv("VX_FORCE_GSTACK");
+    if (fg && atoi(fg)) force_global_stack = 1;
+    q.s2_wide = q.yb + q.zb > 31 || force_wide >= 3;   // keep all-ones free as the sentinel
+    q.e3_wide = q.s2_wide || (q.xb + q.yb + q.zb > 32) || force_wide >= 2;
+    // weights: F = w + row^2 <= (nx-1)^2+(ny-1)^2+(nz-1)^2; products F * L
+    const double fmax = (double)(nx - 1) * (nx - 1) + (double)(ny - 1) * (ny - 1) +
+                        (double)(nz - 1) * (nz - 1);
+    const double lmax = (double)std::max(nx, ny);
+    q.fwide = q.e3_wide || force_wide >= 1 || (2.0 * fmax * lmax >= 2147483647.0) ||
+              (2.0 * lmax * lmax >= 2147483647.0);
+    auto bands = [](int L, int &B, int &W) {
+        B = std::min(32, pow2ceil((L + 31) / 32));
+        W = (L + B - 1) / B;
+    };
+    bands(ny, q.B2, q.W2);
+    bands(nx, q.B3, q.W3);
+    const size_t e2 = (q.s2_wide ? 8 : 4);  // pass-2 entry == s2 code width
+    const size_t e3 = (q.e3_wide ? 8 : 4);
+    const size_t meta2 = (size_t)(3 * q.B2 * 32 + 32) * 4;
+    const size_t meta3 = (size_t)(3 * q.B3 * 32 + 32) * 4;
+    const size_t st2 = (size_t)ny * 32 * e2, st3 = (size_t)nx * 32 * e3;
+    q.gstack2 = force_global_stack || st2 + meta2 > kSmemLimit;
+    q.gstack3 = force_global_stack || st3 + meta3 > kSmemLimit;
+    q.smem2 = q.gstack2 ? meta2 : st2 + meta2;
+    q.smem3 = q.gstack3 ? meta3 : st3 + meta3;
+    q.gstack_ctas = 2 * num_sms();
+    size_t gs = 0;
+    if (q.gstack2) gs = std::max(gs, (size_t)q.gstack_ctas * st2);
+    if (q.gstack3) gs = std::max(gs, (size_t)q.gstack_ctas * st3);
+    const size_t n = (size_t)nx * ny * nz;
+    q.s1_bytes = (n * 4 + 255) & ~(size_t)255;
+    q.s2_bytes = (n * (q.s2_wide ? 8 : 4) + 255) & ~(size_t)255;
+    q.gstack_bytes = gs;
+    *p = q;
+    return true;
+}
+
+
+cudaError_t launch_pass1(const uint8_t *occ, int32_t *s1, long long nslices, int ny, int nz,
+                         cudaStream_t st) {
+    const long long nlines = nslices * ny;
+    if (nlines == 0) return cudaSuccess;
+    const unsigned grid = (unsigned)((nlines + 7) / 8);
+    const bool vec = (nz % 4 == 0) && ((uintptr_t)occ % 16 == 0) && ((uintptr_t)s1 % 16 == 0);
+    if (vec && nz <= 128) k_pass1_v4<1><<<grid, 256, 0, st>>>(occ, s1, nlines, nz);
+    else if (vec && nz <= 256) k_pass1_v4<2><<<grid, 256, 0, st>>>(occ, s1, nlines, nz);
+    else if (vec && nz <= 512) k_pass1_v4<4><<<grid, 256, 0, st>>>(occ, s1, nlines, nz);
+    else if (vec && nz <= 1024) k_pass1_v4<8><<<grid, 256, 0, st>>>(occ, s1, nlines, nz);
+    else if (vec && nz <= 2048) k_pass1_v4<16><<<grid, 256, 0, st>>>(occ, s1, nlines, nz);
+    else k_pass1_generic<<<grid, 256, 0, st>>>(occ, s1, nlines, nz);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pass2(const int32_t *s1, void *s2, void *gstack, const EdtPlan &p,
+                         long long nslices, cudaStream_t st) {
+    return dispatch_col<2>(s1, s2, gstack, p, nslices, p.ny, 0, st);
+}
+
+cudaError_t launch_pass3(const void *s2, int32_t *site, void *gstack, const EdtPlan &p,
+                         int nscenes, int j0, int nyl, cudaStream_t st) {
+    return dispatch_col<3>(s2, site, gstack, p, (long long)nscenes * nyl, nyl, j0, st);
+}
+
+size_t scratch_bytes_for(const EdtPlan &p, int nscenes) {
+    const size_t n = (size_t)p.nx * p.ny * p.nz * nscenes;
+    const size_t s1b = (n * 4 + 255) & ~(size_t)255;
+    const size_t s2b = (n * (p.s2_wide ? 8 : 4) + 255) & ~(size_t)255;
+    return s1b + s2b + p.gstack_bytes;
+}
+
+cudaError_t edt_device_batched(const uint8_t *occ, int32_t *site, void *scratch,
+                               const EdtPlan &p, int nscenes, cudaStream_t st) {
+    // scratch = [s1 i32 N*nscenes][s2 N*nscenes][global stacks]
+    unsigned char *base = static_cast<unsigned char *>(scratch);
+    const size_t n = (size_t)p.nx * p.ny * p.nz * nscenes;
+    int32_t *s1 = reinterpret_cast<int32_t *>(base);
+    const size_t s1b = (n * 4 + 255) & ~(size_t)255;
+    void *s2 = base + s1b;
+    const size_t s2b = (n * (p.s2_wide ? 8 : 4) + 255) & ~(size_t)255;
+    void *gs = base + s1b + s2b;
+    cudaError_t e = launch_pass1(occ, s1, (long long)p.nx * nscenes, p.ny, p.nz, st);
+    if (e != cudaSuccess) return e;
+    e = launch_pass2(s1, s2, gs, p, (long long)p.nx * nscenes, st);
+    if (e != cudaSuccess) return e;
+    return launch_pass3(s2, site, gs, p, nscenes, 0, p.ny, st);
+}
+
+cudaError_t edt_device(const uint8_t *occ, int32_t *site, void *scratch, const EdtPlan &p,
+                       cudaStream_t st) {
+    return edt_device_batched(occ, site, scratch, p, 1, st);
+}
+
+}  // namespace vx

@@ -1,0 +1,88 @@
+// Internal declarations shared by the sm_100a kernels and the C-ABI layer.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stddef.h>
+
+#define VX_FULL_MASK 0xffffffffu
+
+namespace vx {
+
+// Launch configuration / layout decisions for one EDT problem.  Computed on
+// the host from the grid shape; documented in DESIGN.md ("EDT kernels").
+struct EdtPlan {
+    int nx, ny, nz;
+    int zb, yb, xb;        // bits(n-1) per axis: packing widths
+    bool s2_wide;          // pass-2 output as u64 (y<<32 | z) instead of u32 (y<<zb | z)
+    bool e3_wide;          // pass-3 stack entries as u64
+    bool fwide;            // int64 weights/products (extents beyond ~700)
+    int B2, W2;            // pass 2: bands per column, rows per band
+    int B3, W3;            // pass 3
+    bool gstack2, gstack3; // stack in global scratch (column longer than smem allows)
+    size_t smem2, smem3;   // dynamic smem bytes per CTA
+    size_t s1_bytes, s2_bytes, gstack_bytes;  // scratch layout
+    int gstack_ctas;       // persistent CTAs when a global stack is used
+};
+
+bool make_plan(int nx, int ny, int nz, EdtPlan *p, int force_global_stack);
+
+// Pass launchers (stream-ordered, no host sync).  Return cudaError_t.
+// nslices: number of (ny, nz) slices stacked along i (scenes * local nx).
+cudaError_t launch_pass1(const uint8_t *occ, int32_t *s1, long long nslices, int ny, int nz,
+                         cudaStream_t st);
+cudaError_t launch_pass2(const int32_t *s1, void *s2, void *gstack, const EdtPlan &p,
+                         long long nslices, cudaStream_t st);
+// pass 3 over nscenes buffers of shape (nx, nyl, nz) holding global rows
+// j0 .. j0+nyl-1 (slab mode); site codes are global flat indices.
+cudaError_t launch_pass3(const void *s2, int32_t *site, void *gstack, const EdtPlan &p,
+                         int nscenes, int j0, int nyl, cudaStream_t st);
+size_t scratch_bytes_for(const EdtPlan &p, int nscenes);
+// Full EDT: occ (device) -> site (device); scratch >= scratch_bytes_for(p, n).
+cudaError_t edt_device(const uint8_t *occ, int32_t *site, void *scratch, const EdtPlan &p,
+                       cudaStream_t st);
+// Batched EDT over `nscenes` equally-shaped scenes laid out back to back.
+cudaError_t edt_device_batched(const uint8_t *occ, int32_t *site, void *scratch,
+                               const EdtPlan &p, int nscenes, cudaStream_t st);
+
+// ---- map side -------------------------------------------------------------
+struct GridGeom {
+    int nx, ny, nz;
+    double vs;
+    double ox, oy, oz;
+};
+
+struct DevCounters {                // device-resident per-grid bookkeeping
+    unsigned long long inserted, skipped, oob, stamped_oob;
+    int touched;                    // entries in the touched (reset) list
+    int pending;                    // new first-touch voxels of the current insert
+    int overflow;                   // touched list overflowed -> dense reset
+    int dirty;                      // occupancy changed since last EDT (memo)
+};
+
+cudaError_t launch_reset(float *cells, uint8_t *occ, int32_t *touched, DevCounters *ctr,
+                         int64_t n, int capacity, bool dense, cudaStream_t st);
+cudaError_t launch_dense_clip(float *cells, const uint32_t *counts, int64_t n,
+                              const DevCounters *ctr, cudaStream_t st);
+cudaError_t launch_scatter(const double *pts, int64_t npts, const int64_t *npts_dev,
+                           GridGeom g, const float *mask_cells, float thr, uint32_t *counts,
+                           int32_t *touched, DevCounters *ctr, int capacity,
+                           cudaStream_t st);
+cudaError_t launch_finalize(float *cells, uint8_t *occ, uint32_t *counts, int32_t *touched,
+                            DevCounters *ctr, int64_t n, int capacity, int64_t max_new,
+                            float hit, float occ_thr, cudaStream_t st);
+cudaError_t launch_stamp(const int32_t *ijk, const int64_t *offsets, int nsets,
+                         const double *set_origin, const double *set_vs, const double *T,
+                         GridGeom g, float *cells, uint8_t *occ, float value, float occ_thr,
+                         int32_t *touched, DevCounters *ctr, unsigned long long *oob_per_set,
+                         int capacity, int64_t total, cudaStream_t st);
+cudaError_t launch_occupancy(const float *cells, uint8_t *out, int64_t n, float thr,
+                             cudaStream_t st);
+
+// ---- query ----------------------------------------------------------------
+cudaError_t launch_site_world(const int32_t *site, GridGeom g, const double *centers,
+                              int s, int32_t *out_lin, double *out_world, double *out_dist,
+                              cudaStream_t st);
+
+int num_sms();
+
+}  // namespace vx

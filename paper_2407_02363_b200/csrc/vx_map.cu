@@ -1,0 +1,285 @@
+// Map-side kernels: device-resident log-odds grid (voxarm grids.py).
+//
+//   K0 k_reset     VoxelGrid.clear             grids.py:146-147 (sparse: only
+//                  voxels touched since the last clear; dense on overflow)
+//   K1 k_scatter   insert_point_cloud          grids.py:149-188 (k_neighbors=0)
+//      k_finalize  the bincount/clip epilogue  grids.py:185-187
+//   K2 k_stamp     insert_voxel_set            grids.py:190-203 (many link
+//                  voxel sets, one launch; per-set FK transform)
+//      k_occupancy occupancy_mask              grids.py:207-208
+//
+// Float semantics follow numpy exactly: float64 discretisation with IEEE
+// division and floor (grids.py:137); hits counted as integers and applied as
+// clip(cell + f32(count) * f32(hit)) in float32 (grids.py:185-187, NEP 50
+// weak-scalar promotion) -- never per-point float atomics; the float32
+// threshold compare (numpy casts the python-float logit to float32).  The
+// rigid transform of voxel-set centres is evaluated as numpy's OpenBLAS dgemm
+// does on this image: fma(c2, r2, fma(c1, r1, c0*r0)) + t.
+#include "vx_internal.cuh"
+
+namespace vx {
+namespace {
+
+constexpr float kLMin = -2.0f;  // grids.py:18
+constexpr float kLMax = 3.5f;   // grids.py:19
+
+__device__ __forceinline__ float clip_logodds(float c) {
+    // np.clip semantics: NaN propagates
+    if (c < kLMin) return kLMin;
+    if (c > kLMax) return kLMax;
+    return c;
+}
+
+// floor((p - origin) / vs) per axis; -1 when outside [0, dims)  (grids.py:134-139)
+__device__ __forceinline__ long long discretize(double px, double py, double pz, const GridGeom &g) {
+    const double fx = floor(__ddiv_rn(__dsub_rn(px, g.ox), g.vs));
+    const double fy = floor(__ddiv_rn(__dsub_rn(py, g.oy), g.vs));
+    const double fz = floor(__ddiv_rn(__dsub_rn(pz, g.oz), g.vs));
+    if (!(fx >= 0.0) || !(fx < (double)g.nx)) return -1;
+    if (!(fy >= 0.0) || !(fy < (double)g.ny)) return -1;
+    if (!(fz >= 0.0) || !(fz < (double)g.nz)) return -1;
+    return ((long long)fx * g.ny + (long long)fy) * g.nz + (long long)fz;
+}
+
+// warp-aggregated counter add (one atomic per warp)
+__device__ __forceinline__ void warp_count(unsigned long long *dst, bool pred) {
+    const unsigned m = __ballot_sync(VX_FULL_MASK, pred);
+    if ((threadIdx.x & 31) == 0 && m) atomicAdd(dst, (unsigned long long)__popc(m));
+}
+
+__global__ void k_reset(float *__restrict__ cells, uint8_t *__restrict__ occ,
+                        const int32_t *__restrict__ touched, const DevCounters *__restrict__ ctr,
+                        long long n, int dense_req) {
+    const bool dense = dense_req || ctr->overflow;
+    const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long nth = (long long)gridDim.x * blockDim.x;
+    if (dense) {
+        const long long n4 = n >> 2;  // cells are 16-byte aligned (cudaMalloc)
+        float4 *c4 = reinterpret_cast<float4 *>(cells);
+        uint32_t *o4 = reinterpret_cast<uint32_t *>(occ);
+        for (long long v = tid; v < n4; v += nth) {
+            c4[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+            o4[v] = 0u;
+        }
+        for (long long v = (n4 << 2) + tid; v < n; v += nth) {
+            cells[v] = 0.f;
+            occ[v] = 0;
+        }
+    } else {
+        const int cnt = ctr->touched;
+        for (long long t = tid; t < cnt; t += nth) {
+            const int v = touched[t];
+            cells[v] = 0.f;
+            occ[v] = 0;
+        }
+    }
+}
+
+__global__ void k_reset_commit(DevCounters *ctr) {
+    ctr->touched = 0;
+    ctr->pending = 0;
+    ctr->overflow = 0;
+    ctr->dirty = 1;
+}
+
+// clip untouched voxels (only needed after host writes put cells out of
+// range): grids.py:187 clips every voxel whenever any point was inserted
+__global__ void k_dense_clip(float *__restrict__ cells, const uint32_t *__restrict__ counts,
+                             long long n, const DevCounters *__restrict__ ctr) {
+    if (ctr->inserted == 0) return;
+    const long long nth = (long long)gridDim.x * blockDim.x;
+    for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += nth)
+        if (counts[v] == 0) cells[v] = clip_logodds(__fadd_rn(cells[v], 0.0f));
+}
+
+__global__ void k_scatter(const double *__restrict__ pts, long long npts,
+                          const long long *__restrict__ npts_dev, GridGeom g,
+                          const float *__restrict__ mask_cells, float thr,
+                          uint32_t *__restrict__ counts, int32_t *__restrict__ touched,
+                          DevCounters *__restrict__ ctr, int capacity) {
+    const long long n = npts_dev ? *npts_dev : npts;
+    const int base = ctr->touched;
+    const long long nth = (long long)gridDim.x * blockDim.x;
+    const long long start = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    // uniform trip count so the warp-aggregated counters see full warps
+    const long long trips = (n + nth - 1) / nth;
+    for (long long it = 0; it < trips; ++it) {
+        const long long p = start + it * nth;
+        bool oob = false, skip = false, ins = false;
+        if (p < n) {
+            const double x = pts[3 * p], y = pts[3 * p + 1], z = pts[3 * p + 2];
+            const long long lin = discretize(x, y, z, g);
+            if (lin < 0) {
+                oob = true;                                          // grids.py:171
+            } else if (mask_cells && mask_cells[lin] > thr) {
+                skip = true;                                         // grids.py:178-182
+            } else {
+                ins = true;
+                if (atomicAdd(&counts[lin], 1u) == 0u) {            // first touch
+                    const int slot = atomicAdd(&ctr->pending, 1);
+                    if (base + slot < capacity) touched[base + slot] = (int32_t)lin;
+                    else ctr->overflow = 1;
+                }
+            }
+        }
+        warp_count(&ctr->oob, oob);
+        warp_count(&ctr->skipped, skip);
+        warp_count(&ctr->inserted, ins);
+    }
+}
+
+__device__ __forceinline__ void apply_hits(float *cells, uint8_t *occ, uint32_t *counts,
+                                           long long v, float hit, float occ_thr) {
+    const uint32_t c = counts[v];
+    counts[v] = 0u;
+    // np.clip(flat + hits * hit, L_MIN, L_MAX): f32 multiply, f32 add (no fma)
+    const float h = __fmul_rn((float)c, hit);
+    const float cell = clip_logodds(__fadd_rn(cells[v], h));
+    cells[v] = cell;
+    occ[v] = cell > occ_thr ? 1 : 0;
+}
+
+__global__ void k_finalize(float *__restrict__ cells, uint8_t *__restrict__ occ,
+                           uint32_t *__restrict__ counts, const int32_t *__restrict__ touched,
+                           const DevCounters *__restrict__ ctr, long long n, float hit,
+                           float occ_thr) {
+    const long long nth = (long long)gridDim.x * blockDim.x;
+    const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (ctr->overflow) {  // the touched list is incomplete: scan every voxel
+        for (long long v = tid; v < n; v += nth)
+            if (counts[v]) apply_hits(cells, occ, counts, v, hit, occ_thr);
+    } else {
+        const int base = ctr->touched, cnt = ctr->pending;
+        for (long long t = tid; t < cnt; t += nth)
+            apply_hits(cells, occ, counts, touched[base + t], hit, occ_thr);
+    }
+}
+
+__global__ void k_finalize_commit(DevCounters *ctr, int capacity) {
+    const long long t = (long long)ctr->touched + ctr->pending;
+    ctr->touched = t > capacity ? capacity : (int)t;
+    ctr->pending = 0;
+    if (ctr->inserted) ctr->dirty = 1;
+}
+
+__global__ void k_stamp(const int32_t *__restrict__ ijk, const long long *__restrict__ offsets,
+                        int nsets, const double *__restrict__ set_origin,
+                        const double *__restrict__ set_vs, const double *__restrict__ T,
+                        GridGeom g, float *__restrict__ cells, uint8_t *__restrict__ occ,
+                        float value, float occ_thr, int32_t *__restrict__ touched,
+                        DevCounters *__restrict__ ctr, unsigned long long *__restrict__ oob_per_set,
+                        int capacity, long long total) {
+    const long long nth = (long long)gridDim.x * blockDim.x;
+    for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < total; q += nth) {
+        int s = 0;
+        while (s + 1 < nsets && q >= offsets[s + 1]) ++s;
+        const double vs = set_vs[s];
+        // VoxelSet.centers(): origin + (idx + 0.5) * vs   (grids.py:87-88)
+        double c[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+            c[a] = __dadd_rn(set_origin[3 * s + a],
+                             __dmul_rn(__dadd_rn((double)ijk[3 * q + a], 0.5), vs));
+        double p[3];
+        if (T) {
+            const double *M = T + 16 * s;  // row-major 4x4; c @ R.T + t  (grids.py:198)
+#pragma unroll
+            for (int a = 0; a < 3; ++a)
+                p[a] = __dadd_rn(__fma_rn(c[2], M[4 * a + 2],
+                                          __fma_rn(c[1], M[4 * a + 1], __dmul_rn(c[0], M[4 * a]))),
+                                 M[4 * a + 3]);
+        } else {
+            p[0] = c[0]; p[1] = c[1]; p[2] = c[2];
+        }
+        const long long lin = discretize(p[0], p[1], p[2], g);
+        if (lin < 0) {
+            atomicAdd(&oob_per_set[s], 1ull);
+            continue;
+        }
+        cells[lin] = value;                                           // grids.py:202
+        occ[lin] = value > occ_thr ? 1 : 0;
+        const int slot = atomicAdd(&ctr->touched, 1);
+        if (slot < capacity) touched[slot] = (int32_t)lin;
+        else ctr->overflow = 1;
+    }
+}
+
+__global__ void k_stamp_commit(DevCounters *ctr, int capacity) {
+    if (ctr->touched > capacity) ctr->touched = capacity;
+    ctr->dirty = 1;
+}
+
+__global__ void k_occupancy(const float *__restrict__ cells, uint8_t *__restrict__ out, long long n,
+                            float thr) {
+    const long long nth = (long long)gridDim.x * blockDim.x;
+    for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += nth)
+        out[v] = cells[v] > thr ? 1 : 0;                              // grids.py:207-208
+}
+
+unsigned grid_for(long long work, int block) {
+    long long g = (work + block - 1) / block;
+    const long long cap = (long long)num_sms() * 8;
+    if (g > cap) g = cap;
+    if (g < 1) g = 1;
+    return (unsigned)g;
+}
+
+}  // namespace
+
+cudaError_t launch_reset(float *cells, uint8_t *occ, int32_t *touched, DevCounters *ctr, int64_t n,
+                         int capacity, bool dense, cudaStream_t st) {
+    (void)capacity;
+    // the sparse count is only known on the device: size for the dense case
+    // when asked, otherwise for a persistent grid-stride sweep
+    const unsigned g = dense ? grid_for(n / 4 + 1, 256) : (unsigned)(num_sms() * 4);
+    k_reset<<<g, 256, 0, st>>>(cells, occ, touched, ctr, n, dense ? 1 : 0);
+    k_reset_commit<<<1, 1, 0, st>>>(ctr);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dense_clip(float *cells, const uint32_t *counts, int64_t n,
+                              const DevCounters *ctr, cudaStream_t st) {
+    k_dense_clip<<<grid_for(n, 256), 256, 0, st>>>(cells, counts, n, ctr);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_scatter(const double *pts, int64_t npts, const int64_t *npts_dev, GridGeom g,
+                           const float *mask_cells, float thr, uint32_t *counts, int32_t *touched,
+                           DevCounters *ctr, int capacity, cudaStream_t st) {
+    if (npts <= 0 && !npts_dev) return cudaSuccess;
+    k_scatter<<<grid_for(npts, 256), 256, 0, st>>>(pts, npts, (const long long *)npts_dev, g,
+                                                   mask_cells, thr, counts, touched, ctr, capacity);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_finalize(float *cells, uint8_t *occ, uint32_t *counts, int32_t *touched,
+                            DevCounters *ctr, int64_t n, int capacity, int64_t max_new, float hit,
+                            float occ_thr, cudaStream_t st) {
+    // a dense (overflow) sweep needs the full grid; otherwise max_new bounds work
+    k_finalize<<<grid_for(n < max_new ? n : max_new, 256), 256, 0, st>>>(cells, occ, counts, touched,
+                                                                         ctr, n, hit, occ_thr);
+    k_finalize_commit<<<1, 1, 0, st>>>(ctr, capacity);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_stamp(const int32_t *ijk, const int64_t *offsets, int nsets,
+                         const double *set_origin, const double *set_vs, const double *T,
+                         GridGeom g, float *cells, uint8_t *occ, float value, float occ_thr,
+                         int32_t *touched, DevCounters *ctr, unsigned long long *oob_per_set,
+                         int capacity, int64_t total, cudaStream_t st) {
+    if (total > 0)
+        k_stamp<<<grid_for(total, 256), 256, 0, st>>>(ijk, (const long long *)offsets, nsets,
+                                                      set_origin, set_vs, T, g, cells, occ, value,
+                                                      occ_thr, touched, ctr, oob_per_set, capacity,
+                                                      total);
+    k_stamp_commit<<<1, 1, 0, st>>>(ctr, capacity);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_occupancy(const float *cells, uint8_t *out, int64_t n, float thr,
+                             cudaStream_t st) {
+    k_occupancy<<<grid_for(n, 256), 256, 0, st>>>(cells, out, n, thr);
+    return cudaGetLastError();
+}
+
+}  // namespace vx

@@ -1,0 +1,297 @@
+"""GPU map-side parity: device VoxelGrid (K0 reset, K1 scatter, K2 stamp) and
+the K6 sphere gather vs the reference (golden vectors from voxarm itself and
+the reference's own pkg/tests/test_grids.py known answers)."""
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2407_02363_b200 import (L_MAX, L_MIN, FilterConfig, PointCloud, VoxelGrid, VoxelSet,
+                                   logit, new_grid, pba_edt, synth)
+from paper_2407_02363_b200.engine import site_world
+from tests.golden_util import desk7, digest, golden
+
+pytestmark = pytest.mark.gpu
+NOFILT = FilterConfig(k_neighbors=0)
+
+
+def test_insert_cases_vs_reference():
+    for rec in golden()["insert"]:
+        case = synth.insert_case(rec["case"])
+        g = VoxelGrid(case["dims"], case["voxel_size"], case["origin"])
+        mask = None
+        if case["mask_ijk"] is not None:
+            mask = VoxelGrid(case["dims"], case["voxel_size"], case["origin"])
+            mask.insert_voxel_set(VoxelSet(case["origin"], case["voxel_size"], case["mask_ijk"]))
+        cfg = FilterConfig(k_neighbors=0, hit_logodds=case["hit"], occupancy_threshold=case["thr"])
+        stats = []
+        for pts in case["clouds"]:
+            st = g.insert_point_cloud(PointCloud(pts, case["pose"]), cfg, mask)
+            stats.append([st.inserted, st.robot_skipped, st.out_of_bounds])
+        assert stats == rec["stats"], rec["case"]
+        assert digest(g.cells) == rec["cells"], rec["case"]
+        assert digest(g.occupancy_mask(case["thr"])) == rec["occ"], rec["case"]
+
+
+def test_stamp_cases_vs_reference():
+    for rec in golden()["stamp"]:
+        case = synth.stamp_case(rec["case"])
+        g = VoxelGrid(case["dims"], case["voxel_size"], case["origin"])
+        oob = g.insert_voxel_set(VoxelSet(case["set_origin"], case["set_voxel_size"], case["ijk"]),
+                                 case["T"])
+        assert oob == rec["oob"]
+        assert digest(g.cells) == rec["cells"], rec["case"]
+        if rec["occupied"] is not None:
+            assert g.occupied_voxels().tolist() == rec["occupied"]
+
+
+def test_site_world_cases_vs_reference():
+    for rec in golden()["site_world"]:
+        case = synth.site_world_case(rec["case"])
+        f = pba_edt(case["occ"], voxel_size=case["voxel_size"])
+        lin, world, dist = site_world(f, case["origin"], case["voxel_size"], case["centers"])
+        for q, (w, d) in enumerate(zip(rec["world"], rec["dist"])):
+            if w is None:
+                assert lin[q] == -1 and np.isinf(dist[q])
+            else:
+                assert world[q].tolist() == w            # bit-exact world point
+                assert dist[q] == pytest.approx(d, rel=1e-6)   # north_star tolerance
+
+
+def test_c1_camera_tick_vs_reference():
+    """engine.py:234-280 at C1 through the shim (VoxelGrid + pba_edt + gather)."""
+    gold = golden()["c1"]
+    d = desk7()
+    spec = synth.C1
+    dims, vs, origin = spec["dims"], spec["voxel_size"], spec["origin"]
+    frames = d["frames"][0]
+    links = [VoxelSet(org, vs, ijk) for ijk, org in d["links"]]
+    env, selfg, mask = (VoxelGrid(dims, vs, origin) for _ in range(3))
+    for li in d["o_links"]:
+        selfg.insert_voxel_set(links[li], frames[li])
+    mask.insert_voxel_sets(links, list(frames))
+    assert digest(selfg.cells) == gold["self_cells"]
+    assert digest(mask.cells) == gold["mask_cells"]
+    centers = np.vstack([synth.sphere_centers(frames, d["sphere_link"], d["sphere_center"]),
+                         synth.extra_query_points(dims, vs, origin)])
+    for f in ("0", "5", "17"):
+        env.clear()
+        st = env.insert_point_cloud(PointCloud(synth.c1_cloud(int(f) / 30.0)), NOFILT, robot_mask=mask)
+        assert [st.inserted, st.robot_skipped, st.out_of_bounds] == gold[f]["stats"]
+        assert digest(env.cells) == gold[f]["env_cells"]
+        occ = env.occupancy_mask()
+        assert digest(occ) == gold[f]["env_occ"]
+        fe = env.distance_field()
+        assert digest(fe.site) == gold[f]["env_site"]
+        assert digest(pba_edt(occ, voxel_size=vs).site) == gold[f]["env_site"]
+        lin, world, _ = site_world(fe, origin, vs, centers)
+        for q, w in enumerate(gold[f]["env_world"]):
+            assert (lin[q] == -1) if w is None else (world[q].tolist() == w)
+    fs = selfg.distance_field()
+    assert digest(fs.site) == gold["self_site"]
+
+
+def test_sparse_reset_matches_dense_state():
+    rng = np.random.default_rng(4)
+    g = VoxelGrid((40, 30, 20), 0.05)
+    for _ in range(5):
+        pts = rng.uniform(-0.2, 2.2, size=(4000, 3))
+        g.insert_point_cloud(PointCloud(pts), NOFILT)
+        g.insert_voxel_set(VoxelSet((0, 0, 0), 0.05, rng.integers(0, 20, size=(300, 3))))
+        g.clear()
+        assert (g.cells == 0).all()
+        assert not g.occupancy_mask().any()
+
+
+def test_touched_list_overflow_falls_back_dense():
+    # many repeated inserts into a tiny grid overflow the touched list
+    g = VoxelGrid((4, 4, 4), 0.25)
+    ref = np.zeros((4, 4, 4), np.float32)
+    rng = np.random.default_rng(5)
+    for _ in range(40):
+        pts = rng.uniform(0, 1, size=(50, 3))
+        g.insert_point_cloud(PointCloud(pts), FilterConfig(k_neighbors=0, hit_logodds=0.05))
+        O.insert_points(ref, 0.25, (0, 0, 0), pts, hit_logodds=0.05)
+    assert np.array_equal(g.cells, ref)
+    g.clear()
+    assert (g.cells == 0).all()
+
+
+def test_host_writes_out_of_range_are_clipped_like_numpy():
+    g = VoxelGrid((6, 6, 6), 0.1)
+    ref = np.zeros((6, 6, 6), np.float32)
+    g.cells.fill(10.0)
+    ref.fill(10.0)
+    g.cells[0, 0, 0] = -7.0
+    ref[0, 0, 0] = -7.0
+    pts = np.array([[0.05, 0.05, 0.05], [0.35, 0.35, 0.35]])
+    g.insert_point_cloud(PointCloud(pts), NOFILT)
+    O.insert_points(ref, 0.1, (0, 0, 0), pts)
+    assert np.array_equal(g.cells, ref)
+
+
+# -- pkg/tests/test_grids.py known answers ------------------------------------------
+
+def test_new_grid_fresh():                                    # 20-23
+    g = new_grid((4, 4, 4), 0.1, (0, 0, 0))
+    assert g.cells.size == 64 and g.occupied_voxels().shape == (0, 3)
+
+
+@pytest.mark.parametrize("dims", [(0, 4, 4), (4, -1, 4), (4, 4, 0)])
+def test_new_grid_rejects_degenerate_dims(dims):               # 31-34
+    with pytest.raises(ValueError):
+        new_grid(dims, 0.1)
+
+
+def test_world_to_voxel_floor_convention():                   # 42-47
+    g = new_grid((16, 16, 16), 0.1)
+    assert g.world_to_voxel((0.25, 0.0, 0.95)) == (2, 0, 9)
+    assert g.world_to_voxel((-0.01, 0.0, 0.0)) is None
+    assert g.world_to_voxel((0.2, 0.0, 0.0)) == (2, 0, 0)
+    # the device kernel agrees: a point exactly on a boundary goes up
+    g.insert_point_cloud(PointCloud([[0.2, 0.0, 0.0]]), NOFILT)
+    assert g.occupied_voxels().tolist() == [[2, 0, 0]]
+
+
+def test_insert_single_point_occupies_with_defaults():       # 84-89
+    g = new_grid((8, 8, 8), 0.1)
+    st = g.insert_point_cloud(PointCloud(points=[[0.55, 0.55, 0.55]]), NOFILT)
+    assert st.inserted == 1 and g.occupied_voxels().tolist() == [[5, 5, 5]]
+
+
+def test_insert_needed_count_matches_logodds_arithmetic():   # 92-103
+    cfg = FilterConfig(k_neighbors=0, hit_logodds=0.3, occupancy_threshold=0.7)
+    need = int(np.ceil(logit(0.7) / 0.3 + 1e-12))
+    g = new_grid((4, 4, 4), 1.0)
+    cloud = PointCloud(points=[[0.5, 0.5, 0.5]])
+    for _ in range(need):
+        assert g.occupied_voxels(0.7).shape[0] == 0
+        g.insert_point_cloud(cloud, cfg)
+    if g.occupied_voxels(0.7).shape[0] == 0:
+        g.insert_point_cloud(cloud, cfg)
+    assert g.occupied_voxels(0.7).tolist() == [[0, 0, 0]]
+
+
+def test_insert_respects_robot_mask():                       # 106-113
+    g = new_grid((8, 8, 8), 0.1)
+    mask = new_grid((8, 8, 8), 0.1)
+    mask.insert_voxel_set(VoxelSet((0, 0, 0), 0.1, [[5, 5, 5]]))
+    st = g.insert_point_cloud(PointCloud(points=[[0.55, 0.55, 0.55]]), NOFILT, mask)
+    assert st.robot_skipped == 1 and st.inserted == 0
+    assert g.occupied_voxels().shape[0] == 0 and (g.cells == 0).all()
+
+
+def test_insert_mask_geometry_mismatch_rejected():           # 116-120
+    g = new_grid((8, 8, 8), 0.1)
+    mask = new_grid((8, 8, 9), 0.1)
+    with pytest.raises(ValueError):
+        g.insert_point_cloud(PointCloud(points=[[0.5] * 3]), NOFILT, mask)
+
+
+def test_insert_empty_cloud_noop():                          # 123-127
+    g = new_grid((4, 4, 4), 0.1)
+    st = g.insert_point_cloud(PointCloud(points=np.empty((0, 3))), NOFILT)
+    assert st == type(st)() and (g.cells == 0).all()
+
+
+def test_insert_applies_sensor_pose():                       # 130-136
+    g = new_grid((8, 8, 8), 0.1)
+    pose = np.eye(4)
+    pose[:3, 3] = (0.4, 0.0, 0.0)
+    g.insert_point_cloud(PointCloud(points=[[0.15, 0.15, 0.15]], sensor_pose=pose), NOFILT)
+    assert g.occupied_voxels().tolist() == [[5, 1, 1]]
+
+
+def test_insert_counts_out_of_bounds():                      # 139-143
+    g = new_grid((4, 4, 4), 0.1)
+    st = g.insert_point_cloud(PointCloud(points=[[-1, 0, 0], [0.05, 0.05, 0.05], [9, 9, 9]]), NOFILT)
+    assert st.out_of_bounds == 2 and st.inserted == 1
+
+
+def test_insert_monotone_and_clamped():                      # 146-155
+    rng = np.random.default_rng(11)
+    g = new_grid((6, 6, 6), 0.2)
+    for _ in range(30):
+        before = g.cells.copy()
+        pts = rng.uniform(-0.2, 1.4, size=(rng.integers(1, 40), 3))
+        g.insert_point_cloud(PointCloud(points=pts), NOFILT)
+        assert (g.cells >= before).all()
+        assert (g.cells <= L_MAX).all() and (g.cells >= L_MIN).all()
+    assert g.cells.max() == np.float32(L_MAX)
+
+
+def test_insert_duplicate_points_accumulate():               # 158-162
+    g = new_grid((4, 4, 4), 1.0)
+    g.insert_point_cloud(PointCloud(points=[[0.5] * 3, [0.6, 0.5, 0.5]]),
+                         FilterConfig(k_neighbors=0, hit_logodds=0.85))
+    assert g.cells[0, 0, 0] == np.float32(2 * 0.85)
+
+
+def test_voxel_set_identity_and_shift():                     # 165-175
+    g = new_grid((8, 8, 8), 0.1)
+    vs = VoxelSet((0, 0, 0), 0.1, [[2, 3, 4]])
+    assert g.insert_voxel_set(vs) == 0
+    assert g.occupied_voxels().tolist() == [[2, 3, 4]]
+    g.clear()
+    shift = np.eye(4)
+    shift[:3, 3] = (0.1, 0.0, 0.0)
+    g.insert_voxel_set(vs, shift)
+    assert g.occupied_voxels().tolist() == [[3, 3, 4]]
+
+
+def test_voxel_set_rotated_bar_rediscretizes():              # 177-188
+    g = new_grid((16, 16, 16), 0.1, (-0.8, -0.8, -0.8))
+    bar = VoxelSet((-0.05, -0.05, -0.05), 0.1, [[0, 0, 0], [1, 0, 0], [2, 0, 0]])
+    rot = np.eye(4)
+    rot[:3, :3] = [[0, -1, 0], [1, 0, 0], [0, 0, 1]]
+    g.insert_voxel_set(bar, rot)
+    occ = g.occupied_voxels()
+    assert 2 <= occ.shape[0] <= 4
+    assert len(set(occ[:, 0])) == 1 and len(set(occ[:, 2])) == 1
+    ys = sorted(occ[:, 1])
+    assert ys == list(range(ys[0], ys[0] + len(ys)))
+
+
+def test_voxel_set_out_of_bounds_counted():                  # 191-195
+    g = new_grid((4, 4, 4), 0.1)
+    assert g.insert_voxel_set(VoxelSet((0, 0, 0), 0.1, [[0, 0, 0], [9, 0, 0]])) == 1
+    assert g.occupied_voxels().shape[0] == 1
+
+
+def test_clear_idempotent_and_fresh():                       # 198-209
+    g = new_grid((6, 6, 6), 0.1)
+    g.insert_point_cloud(PointCloud(points=[[0.35, 0.35, 0.35]]), NOFILT)
+    g.clear()
+    assert g.occupied_voxels().shape[0] == 0
+    snap = g.cells.copy()
+    g.clear()
+    assert np.array_equal(g.cells, snap)
+    g2 = new_grid((6, 6, 6), 0.1)
+    g.insert_point_cloud(PointCloud(points=[[0.35, 0.35, 0.35]]), NOFILT)
+    g2.insert_point_cloud(PointCloud(points=[[0.35, 0.35, 0.35]]), NOFILT)
+    assert np.array_equal(g.cells, g2.cells)
+
+
+def test_occupied_voxels_lexicographic_and_deterministic():  # 212-223
+    rng = np.random.default_rng(5)
+    g = new_grid((10, 10, 10), 0.1)
+    g.insert_point_cloud(PointCloud(points=rng.uniform(0, 1.0, size=(120, 3))), NOFILT)
+    occ = g.occupied_voxels()
+    assert occ.shape[0] > 0
+    as_tuples = list(map(tuple, occ))
+    assert as_tuples == sorted(as_tuples)
+    g2 = new_grid((10, 10, 10), 0.1)
+    g2.cells[:] = g.cells
+    assert np.array_equal(g2.occupied_voxels(), occ)
+
+
+def test_full_grid_occupied_count():                         # 226-229
+    g = new_grid((3, 3, 3), 0.1)
+    g.cells.fill(L_MAX)
+    assert g.occupied_voxels().shape[0] == 27
+
+
+def test_outlier_filter_not_silently_skipped():
+    g = new_grid((4, 4, 4), 0.1)
+    with pytest.raises(NotImplementedError):
+        g.insert_point_cloud(PointCloud(points=np.zeros((20, 3))), FilterConfig(k_neighbors=8))
