@@ -1,0 +1,415 @@
+"""bench.py -- the driver's benchmark contract for the B200 distance-map pipeline.
+
+One step = one camera tick of voxarm's SimEngine.step (engine.py:233-280) at
+512^3 (BASELINE.json metric "EDT Gvoxel/s & map+EDT+query ms/cycle at 512^3",
+config C3): sparse reset of the env / mask maps, robot-mask stamp of the
+desk7 links at the step's FK frames, scatter of a 300k-point depth-camera
+cloud (config C2's generator, moving sphere) with robot-mask exclusion, exact
+EDT with nearest-site index of the env map, self-map memo (the self-obstacle
+link is the static torso, so its EDT is skipped exactly as the engine's digest
+memo skips it, engine.py:259-268), and the 30-sphere x 2-map gather.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...     (one independent
+      scene per rank: data-parallel weak scaling, no data-path collective)
+
+value      whole-job cycle throughput, Gvoxel/s = N * 512^3 / t_cycle with
+           inputs already resident in HBM (device-timed, CUDA events on the
+           library stream, max over ranks)
+e2e        the same through the public API (MapCycle.step with the cloud,
+           frames and centres copied from pinned host memory and the sphere
+           results + stats read back every step)
+roofline   the dominant kernel (EDT pass 2 or 3): algorithmic bytes 8 B/voxel
+           / its mean CUDA-event duration inside the timed region
+cpu_baseline  the oracle port of the reference path (oracle/, OpenMP on all
+           host threads) on a bounded sample of the same workload
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "EDT Gvoxel/s & map+EDT+query ms/cycle at 512^3; % HBM roofline; 1/2/4/8 GPU"
+DIMS = (512, 512, 512)
+VS = 0.02
+ORIGIN = (-5.12, -5.12, -0.24)
+POINTS = 300_000
+EDT_BYTES_PER_VOXEL = 21          # pass1 1+4, pass2 4+4, pass3 4+4
+PASS_BYTES = {"edt_pass1": 5, "edt_pass2": 8, "edt_pass3": 8}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def desk7():
+    from tests.golden_util import desk7 as _d
+    return _d()
+
+
+def scene_inputs(step: int, rank: int, d):
+    """Per-step synthetic inputs: cloud at t, FK frames, 30 sphere centres."""
+    from paper_2407_02363_b200 import synth
+    t = (step + 7 * rank) / 30.0
+    pts = synth.depth_camera_cloud(t, max_points=POINTS)
+    frames = d["frames"][step % d["frames"].shape[0]]
+    centers = np.vstack([synth.sphere_centers(frames, d["sphere_link"], d["sphere_center"]),
+                         synth.extra_query_points(DIMS, VS, ORIGIN, 9)])
+    return pts, frames, centers
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+        return False
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[5:9]) if v == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_init():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl" if os.environ.get("VX_BENCH_GLOO") is None else "gloo")
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        if dist.get_backend() == "nccl":
+            dist.barrier(device_ids=[torch.cuda.current_device()])
+        else:
+            dist.barrier()
+
+
+def allmax(world, v: float) -> float:
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([v], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ----------------------------------------------------------------------------
+# CPU path: the oracle port of the reference (test infrastructure, timed only)
+# ----------------------------------------------------------------------------
+def cpu_cycle(pts, frames, centers, d, threads: int):
+    """engine.py:234-280 through the oracle restatement (clear x3, stamp,
+    insert k=0, occupancy, EDT, site world) -> seconds per stage."""
+    from oracle import oracle as O
+    t = {}
+    t0 = time.perf_counter()
+    env = np.zeros(DIMS, np.float32)
+    selfc = np.zeros(DIMS, np.float32)
+    mask = np.zeros(DIMS, np.float32)
+    t["clear"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    for li in d["o_links"]:
+        ijk, org = d["links"][li]
+        O.stamp_voxels(selfc, VS, ORIGIN, ijk, org, VS, frames[li])
+    for li, (ijk, org) in enumerate(d["links"]):
+        O.stamp_voxels(mask, VS, ORIGIN, ijk, org, VS, frames[li])
+    O.insert_points(env, VS, ORIGIN, pts, mask)
+    t["insert"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    occ = env > np.float32(0.0)
+    w = threads
+    site = O.pba_edt_site(occ, w, w, 2 * w, workers=threads)
+    t["edt"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    O.site_world(site, VS, ORIGIN, centers)
+    t["query"] = time.perf_counter() - t0
+    return t
+
+
+def run_reference(args, world, rank):
+    """--impl reference: the reference's CPU algorithm (oracle port, all host
+    threads) on this arm's workload; rank 0 only."""
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    O.build()
+    threads = O.max_threads()
+    d = desk7()
+    n = float(np.prod(DIMS))
+    pts, frames, centers = scene_inputs(0, 0, d)
+    for _ in range(max(1, min(args.warmup, 1))):
+        cpu_cycle(pts, frames, centers, d, threads)
+    times, stages = [], []
+    budget = 150.0
+    t_start = time.perf_counter()
+    steps = 0
+    for s in range(args.steps):
+        pts, frames, centers = scene_inputs(s, 0, d)
+        t0 = time.perf_counter()
+        st = cpu_cycle(pts, frames, centers, d, threads)
+        times.append(time.perf_counter() - t0)
+        stages.append(st)
+        steps += 1
+        if time.perf_counter() - t_start > budget:
+            break
+    t = statistics.mean(times)
+    value = n / t / 1e9
+    edt = statistics.mean(s["edt"] for s in stages)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "Gvoxel/s",
+        "n_gpus": args.gpus, "steps": steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+        "data": "synthetic",
+        "config": {"workload": "512^3 camera tick (map update + exact EDT + 30x2 sphere query), "
+                               "CPU oracle port of voxarm edt.py/grids.py/engine.py",
+                   "grid": list(DIMS), "voxel_size": VS, "points": POINTS, "spheres": 30},
+        "edt_gvoxel_s": n / edt / 1e9,
+        "stage_ms": {k: 1e3 * statistics.mean(s[k] for s in stages) for k in stages[0]},
+        "cpu_baseline": {"value": value, "unit": "Gvoxel/s", "cores": threads, "kind": "port",
+                         "sample": f"{steps} full 512^3 camera ticks (300k pts, 8 links, 30 spheres)"},
+        "e2e": {"value": value, "unit": "Gvoxel/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline_sample(d):
+    """Bounded CPU sample (~10-30 s): two full 512^3 ticks after one warm-up."""
+    from oracle import oracle as O
+    O.build()
+    threads = O.max_threads()
+    pts, frames, centers = scene_inputs(0, 0, d)
+    cpu_cycle(pts, frames, centers, d, threads)
+    ts = []
+    for s in range(2):
+        pts, frames, centers = scene_inputs(s + 1, 0, d)
+        t0 = time.perf_counter()
+        cpu_cycle(pts, frames, centers, d, threads)
+        ts.append(time.perf_counter() - t0)
+    t = statistics.mean(ts)
+    return {"value": float(np.prod(DIMS)) / t / 1e9, "unit": "Gvoxel/s", "cores": threads,
+            "kind": "port", "ms_per_step": t * 1e3,
+            "sample": "2 full 512^3 camera ticks after 1 warm-up (oracle/ C port, OpenMP)"}
+
+
+# ----------------------------------------------------------------------------
+# GPU path
+# ----------------------------------------------------------------------------
+def run_gpu(args, world, rank, local):
+    import torch
+    torch.cuda.set_device(local)
+    os.environ["VX_DEVICE"] = str(local)
+    from paper_2407_02363_b200 import _lib
+    from paper_2407_02363_b200.engine import MapCycle
+
+    ctx = _lib.default_context(local)
+    stream = torch.cuda.ExternalStream(ctx.stream_handle(), device=f"cuda:{local}")
+    d = desk7()
+    links = d["links"]
+    cyc = MapCycle(DIMS, VS, ORIGIN, links, VS, d["o_links"], max_points=POINTS, max_spheres=32)
+    L = _lib.load()
+    nsteps_inputs = 8
+    # pinned host inputs (one per distinct step) so the e2e H2D is async
+    host = []
+    for s in range(nsteps_inputs):
+        pts, frames, centers = scene_inputs(s, rank, d)
+        hp = _lib.PinnedArray(pts.shape, np.float64)
+        hp.array[...] = pts
+        hf = _lib.PinnedArray((frames.shape[0], 16), np.float64)
+        hf.array[...] = frames.reshape(-1, 16)
+        hc = _lib.PinnedArray(centers.shape, np.float64)
+        hc.array[...] = centers
+        host.append((hp, hf, hc))
+    n = float(np.prod(DIMS))
+    # device-resident clouds for the `value` leg (inputs in HBM before timing)
+    dev_pts = [torch.from_numpy(np.array(h[0].array)).to(f"cuda:{local}") for h in host]
+    torch.cuda.synchronize()
+
+    def step(s, sync=False):
+        hp, hf, hc = host[s % nsteps_inputs]
+        dp = dev_pts[s % nsteps_inputs]
+        _lib.check(L.vx_cycle_step_device(cyc._h, ctypes.c_void_p(dp.data_ptr()), dp.shape[0],
+                                          _lib.ptr(hf.array), float(np.float32(0.85)), 0.5,
+                                          _lib.ptr(hc.array), hc.array.shape[0], 1 if sync else 0))
+
+    # --- warm-up (also builds the static self map once) ---
+    for s in range(args.warmup):
+        step(s)
+    torch.cuda.synchronize()
+
+    # --- device-timed region: inputs resident (the per-step H2D of the
+    # cloud / frames / centres is the only host traffic and is inside the
+    # step; results stay on the device) ---
+    _lib.check(L.vx_cycle_profile(cyc._h, 1))
+    launches0 = ctx.launches()
+    barrier(world)
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for s in range(args.steps):
+            step(args.warmup + s)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    barrier(world)
+    launches = ctx.launches() - launches0
+    t_dev = e0.elapsed_time(e1) / 1e3 / args.steps
+    ph = np.zeros(len(_lib.CYCLE_PHASES), np.float64)
+    nprof = ctypes.c_int()
+    _lib.check(L.vx_cycle_phase_ms(cyc._h, _lib.ptr(ph), ctypes.byref(nprof)))
+    _lib.check(L.vx_cycle_profile(cyc._h, 0))
+    phases = dict(zip(_lib.CYCLE_PHASES, (float(v) for v in ph)))
+    t_max = allmax(world, t_dev)
+
+    # --- e2e: public API, host inputs and result read-back every step ---
+    barrier(world)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    res = None
+    for s in range(args.steps):
+        hp, hf, hc = host[(args.warmup + s) % nsteps_inputs]
+        cyc.step(hp.array, hf.array, hc.array, sync=False)
+        res = cyc.wait()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    t_e2e_wall = (time.perf_counter() - t0) / args.steps
+    t_e2e = max(ev0.elapsed_time(ev1) / 1e3 / args.steps, t_e2e_wall)
+    t_e2e_max = allmax(world, t_e2e)
+    h2d = POINTS * 24 + d["frames"].shape[1] * 128 + 30 * 24
+    d2h = 2 * 30 * (4 + 24 + 8) + 64
+
+    if rank != 0:
+        return
+    peak, peak_src = peaks()
+    dom = max(("edt_pass2", "edt_pass3"), key=lambda k: phases[k])
+    dom_t = phases[dom] / 1e3
+    achieved = PASS_BYTES[dom] * n / dom_t / 1e9 if dom_t > 0 else None
+    edt_t = (phases["edt_pass1"] + phases["edt_pass2"] + phases["edt_pass3"]) / 1e3
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            traffic = json.load(fh).get(dom)
+    except Exception:
+        pass
+    cycle_bytes = EDT_BYTES_PER_VOXEL * n + 25 * POINTS + 13 * sum(
+        int(x[0].shape[0]) for x in links) + 64 * 60
+    line = {
+        "metric": METRIC, "value": world * n / t_max / 1e9, "unit": "Gvoxel/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t_max * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "config": {"workload": "512^3 camera tick: sparse reset, desk7 mask stamp (8 links, FK "
+                               "frames per step), 300k-pt depth-camera cloud scatter with robot "
+                               "mask, exact EDT + nearest-site index (env; self map static -> memo), "
+                               "30 spheres x 2 maps gather",
+                   "grid": list(DIMS), "voxel_size": VS, "points": POINTS, "spheres": 30,
+                   "parallelism": f"dp{world} (independent scene per GPU)",
+                   "l2": "inputs larger than L2: one EDT streams 2.8 GB per step"},
+        "edt_gvoxel_s": world * n / edt_t / 1e9 if edt_t > 0 else None,
+        "edt_ms": edt_t * 1e3,
+        "edt_roofline_frac": (EDT_BYTES_PER_VOXEL * n / edt_t / 1e9) / peak if edt_t > 0 else None,
+        "cycle_roofline_frac": cycle_bytes / t_max / 1e9 / peak,
+        "phase_ms": phases,
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
+                     "unit": "GB/s", "frac": (achieved / peak) if achieved else None,
+                     "traffic": traffic, "peak_source": peak_src,
+                     "bytes_per_voxel": PASS_BYTES[dom]},
+        "e2e": {"value": world * n / t_e2e_max / 1e9, "unit": "Gvoxel/s",
+                "ms_per_step": t_e2e_max * 1e3, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h,
+                "api": "paper_2407_02363_b200.engine.MapCycle.step + wait (vx_cycle_step/wait)"},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+        "last_stats": {k: res[k] for k in ("inserted", "robot_skipped", "out_of_bounds")} if res else None,
+    }
+    if not args.no_cpu_baseline and world == 1:
+        line["cpu_baseline"] = cpu_baseline_sample(d)
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    world, rank, local = dist_init()
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+    else:
+        run_gpu(args, world, rank, local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

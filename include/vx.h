@@ -165,8 +165,21 @@ int vx_cycle_destroy(vx_cycle *c);
 int vx_cycle_step(vx_cycle *c, const double *pts, int64_t npts, const double *link_T,
                   float hit_logodds, double occupancy_threshold, const double *centers,
                   int s, int sync);
+/* same tick with the cloud already in device memory (d_pts, npts points);
+ * frames and centres are host arrays (a few hundred bytes) */
+int vx_cycle_step_device(vx_cycle *c, const double *d_pts, int64_t npts, const double *link_T,
+                         float hit_logodds, double occupancy_threshold, const double *centers,
+                         int s, int sync);
 int vx_cycle_wait(vx_cycle *c, vx_cycle_result *res, int32_t *site_lin /* 2*s */,
                   double *site_world /* 2*s*3 */, double *dist /* 2*s */);
+/* Per-phase CUDA-event timing of vx_cycle_step (bench evidence).  Phases:
+ * 0 H2D, 1 self map (stamp + EDT, only when it changed), 2 mask stamp +
+ * env/mask reset, 3 scatter + finalize, 4 EDT pass 1, 5 pass 2, 6 pass 3,
+ * 7 sphere gather.  vx_cycle_profile(c, 1) resets and enables; phase_ms
+ * returns the mean over the profiled steps (up to 64). */
+#define VX_CYCLE_PHASES 8
+int vx_cycle_profile(vx_cycle *c, int enable);
+int vx_cycle_phase_ms(vx_cycle *c, double *ms, int *nsteps);
 /* fields of the last step (owned by the cycle; do not destroy) */
 int vx_cycle_fields(vx_cycle *c, vx_field **env, vx_field **self_field);
 int vx_cycle_grids(vx_cycle *c, vx_grid **env, vx_grid **self_grid, vx_grid **mask);

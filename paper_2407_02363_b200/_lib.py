@@ -34,7 +34,10 @@ EXPORTS = (
     "vx_field_site_at", "vx_field_site_world", "vx_edt_scratch_bytes", "vx_edt_device",
     "vx_edt_s2_bytes", "vx_edt_pass12_device", "vx_edt_pass3_device", "vx_cycle_create",
     "vx_cycle_destroy", "vx_cycle_step", "vx_cycle_wait", "vx_cycle_fields", "vx_cycle_grids",
+    "vx_cycle_profile", "vx_cycle_phase_ms", "vx_cycle_step_device",
 )
+CYCLE_PHASES = ("h2d", "self_map", "mask_stamp_reset", "scatter", "edt_pass1", "edt_pass2",
+                "edt_pass3", "gather")
 
 
 class InsertStatsC(ctypes.Structure):
@@ -110,6 +113,9 @@ def load():
             "vx_cycle_wait": ([P, ctypes.POINTER(CycleResultC), P, P, P], i32),
             "vx_cycle_fields": ([P, PP, PP], i32),
             "vx_cycle_grids": ([P, PP, PP, PP], i32),
+            "vx_cycle_profile": ([P, i32], i32),
+            "vx_cycle_step_device": ([P, P, i64, P, f32, f64, P, i32, i32], i32),
+            "vx_cycle_phase_ms": ([P, P, ctypes.POINTER(ctypes.c_int)], i32),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)

@@ -659,6 +659,15 @@ struct vx_cycle {
     bool self_valid = false;
     int last_s = 0;
     int self_recomputed = 0;
+    // per-phase CUDA-event timing (vx_cycle_profile)
+    static constexpr int kRing = 64;
+    bool profiling = false;
+    cudaEvent_t ev[kRing][VX_CYCLE_PHASES + 1] = {};
+    int ring_n = 0;      // steps recorded since the last reset
+    int ring_used = 0;   // event sets created
+    void mark(int phase) {
+        if (profiling && ring_n < kRing) cudaEventRecord(ev[ring_n][phase], ctx->stream);
+    }
 };
 
 extern "C" int vx_cycle_create(vx_ctx *c, int nx, int ny, int nz, double vs, const double origin[3],
@@ -762,25 +771,54 @@ extern "C" int vx_cycle_destroy(vx_cycle *cy) {
     cudaFree(cy->env_f.site);
     cudaFree(cy->self_f.site);
     cudaFree(cy->scratch);
+    for (int r = 0; r < cy->ring_used; ++r)
+        for (int q = 0; q <= VX_CYCLE_PHASES; ++q)
+            if (cy->ev[r][q]) cudaEventDestroy(cy->ev[r][q]);
     delete cy;
     return VX_OK;
 }
 
-extern "C" int vx_cycle_step(vx_cycle *cy, const double *pts, int64_t npts, const double *link_T, float hit,
-                             double thr, const double *centers, int s, int sync) {
+static cudaError_t edt_passes(vx_cycle *cy, const uint8_t *occ, int32_t *site, bool marks) {
+    unsigned char *base = static_cast<unsigned char *>(cy->scratch);
+    const EdtPlan &p = cy->plan;
+    const size_t n = (size_t)p.nx * p.ny * p.nz;
+    const size_t s1b = (n * 4 + 255) & ~(size_t)255;
+    const size_t s2b = (n * (p.s2_wide ? 8 : 4) + 255) & ~(size_t)255;
+    int32_t *s1 = reinterpret_cast<int32_t *>(base);
+    void *s2 = base + s1b, *gs = base + s1b + s2b;
+    cudaStream_t st = cy->ctx->stream;
+    cudaError_t e = launch_pass1(occ, s1, p.nx, p.ny, p.nz, st);
+    if (marks) cy->mark(5);
+    if (e == cudaSuccess) e = launch_pass2(s1, s2, gs, p, p.nx, st);
+    if (marks) cy->mark(6);
+    if (e == cudaSuccess) e = launch_pass3(s2, site, gs, p, 1, 0, p.ny, st);
+    if (marks) cy->mark(7);
+    cy->ctx->launches += 3;
+    return e;
+}
+
+static int cycle_step(vx_cycle *cy, const double *pts, const double *d_pts_in, int64_t npts,
+                      const double *link_T, float hit, double thr, const double *centers, int s, int sync) {
     if (!cy || npts < 0 || npts > cy->max_points || s < 0 || s > cy->max_spheres ||
-        (npts && !pts) || (s && !centers) || (cy->nlinks && !link_T))
+        (npts && !pts && !d_pts_in) || (s && !centers) || (cy->nlinks && !link_T))
         return fail(VX_EINVAL, "bad argument (npts %lld of max %lld, spheres %d of max %d)",
                     (long long)npts, (long long)cy->max_points, s, cy->max_spheres);
     vx_ctx *c = cy->ctx;
     cudaStream_t st = c->stream;
     int rc;
+    if (cy->profiling && cy->ring_n < vx_cycle::kRing && cy->ring_n >= cy->ring_used) {
+        for (int q = 0; q <= VX_CYCLE_PHASES; ++q) VX_CUDA(cudaEventCreate(&cy->ev[cy->ring_n][q]));
+        cy->ring_used = cy->ring_n + 1;
+    }
+    cy->mark(0);
     // H2D: FK frames of every link, the self subset, the cloud, the centres
     if (cy->nlinks) VX_CUDA(cudaMemcpyAsync(cy->T_all, link_T, 128 * cy->nlinks, cudaMemcpyHostToDevice, st));
     std::vector<double> Ts(16 * cy->nself);
     for (int q = 0; q < cy->nself; ++q) std::memcpy(&Ts[16 * q], link_T + 16 * cy->self_links[q], 128);
-    if (npts) VX_CUDA(cudaMemcpyAsync(cy->d_pts, pts, (size_t)npts * 24, cudaMemcpyHostToDevice, st));
+    const double *d_pts = d_pts_in ? d_pts_in : cy->d_pts;
+    if (npts && !d_pts_in) VX_CUDA(cudaMemcpyAsync(cy->d_pts, pts, (size_t)npts * 24, cudaMemcpyHostToDevice, st));
     if (s) VX_CUDA(cudaMemcpyAsync(cy->d_centers, centers, (size_t)s * 24, cudaMemcpyHostToDevice, st));
+    cy->mark(1);
     // self map: memo on the self-obstacle transforms (engine.py:259-268 skips
     // the EDT when the occupancy is unchanged; equal transforms => equal
     // occupancy, since the stamp is deterministic)
@@ -791,24 +829,25 @@ extern "C" int vx_cycle_step(vx_cycle *cy, const double *pts, int64_t npts, cons
         if (cy->nself && (rc = stamp_sets(cy->self, cy->nself, cy->ijk_self, cy->off_self, cy->org_self,
                                           cy->vs_self, cy->T_self, kLMax, cy->total_self)))
             return rc;
-        cudaError_t e = edt_device(cy->self->occ, cy->self_f.site, cy->scratch, cy->plan, st);
+        cudaError_t e = edt_passes(cy, cy->self->occ, cy->self_f.site, false);
         if (e != cudaSuccess) return cuda_fail(e, "edt(self)");
-        c->launches += 3;
         cy->last_self_T = Ts;
         cy->self_valid = true;
         cy->self_recomputed = 1;
     }
+    cy->mark(2);
     // mask <- all links; env <- cloud minus mask  (engine.py:236-254)
     if ((rc = grid_clear_async(cy->mask))) return rc;
     if (cy->nlinks && (rc = stamp_sets(cy->mask, cy->nlinks, cy->ijk_all, cy->off_all, cy->org_all, cy->vs_all,
                                        cy->T_all, kLMax, cy->total_all)))
         return rc;
     if ((rc = grid_clear_async(cy->env))) return rc;
-    if (npts && (rc = insert_device(cy->env, cy->d_pts, npts, nullptr, hit, thr, cy->mask))) return rc;
+    cy->mark(3);
+    if (npts && (rc = insert_device(cy->env, d_pts, npts, nullptr, hit, thr, cy->mask))) return rc;
     if (!npts) VX_CUDA(cudaMemsetAsync(cy->env->ctr, 0, 3 * sizeof(unsigned long long), st));
-    cudaError_t e = edt_device(cy->env->occ, cy->env_f.site, cy->scratch, cy->plan, st);
+    cy->mark(4);
+    cudaError_t e = edt_passes(cy, cy->env->occ, cy->env_f.site, true);
     if (e != cudaSuccess) return cuda_fail(e, "edt(env)");
-    c->launches += 3;
     // per-sphere gather on both fields (engine.py:272-280)
     const GridGeom g = cy->env->g;
     e = launch_site_world(cy->env_f.site, g, cy->d_centers, s, cy->d_lin, cy->d_world, cy->d_dist, st);
@@ -817,8 +856,44 @@ extern "C" int vx_cycle_step(vx_cycle *cy, const double *pts, int64_t npts, cons
                               cy->d_dist + s, st);
     if (e != cudaSuccess) return cuda_fail(e, "site_world");
     c->launches += s ? 2 : 0;
+    cy->mark(8);
+    if (cy->profiling && cy->ring_n < vx_cycle::kRing) cy->ring_n++;
     cy->last_s = s;
     if (sync) VX_CUDA(cudaStreamSynchronize(st));
+    return VX_OK;
+}
+
+extern "C" int vx_cycle_step(vx_cycle *cy, const double *pts, int64_t npts, const double *link_T, float hit,
+                             double thr, const double *centers, int s, int sync) {
+    return cycle_step(cy, pts, nullptr, npts, link_T, hit, thr, centers, s, sync);
+}
+
+extern "C" int vx_cycle_step_device(vx_cycle *cy, const double *d_pts, int64_t npts, const double *link_T,
+                                    float hit, double thr, const double *centers, int s, int sync) {
+    return cycle_step(cy, nullptr, d_pts, npts, link_T, hit, thr, centers, s, sync);
+}
+
+extern "C" int vx_cycle_profile(vx_cycle *cy, int enable) {
+    if (!cy) return fail(VX_EINVAL, "NULL cycle");
+    VX_CUDA(cudaStreamSynchronize(cy->ctx->stream));
+    cy->profiling = enable != 0;
+    cy->ring_n = 0;
+    return VX_OK;
+}
+
+extern "C" int vx_cycle_phase_ms(vx_cycle *cy, double *ms, int *nsteps) {
+    if (!cy || !ms) return fail(VX_EINVAL, "NULL argument");
+    VX_CUDA(cudaStreamSynchronize(cy->ctx->stream));
+    for (int q = 0; q < VX_CYCLE_PHASES; ++q) ms[q] = 0.0;
+    for (int r = 0; r < cy->ring_n; ++r)
+        for (int q = 0; q < VX_CYCLE_PHASES; ++q) {
+            float t = 0.f;
+            VX_CUDA(cudaEventElapsedTime(&t, cy->ev[r][q], cy->ev[r][q + 1]));
+            ms[q] += t;
+        }
+    if (cy->ring_n)
+        for (int q = 0; q < VX_CYCLE_PHASES; ++q) ms[q] /= cy->ring_n;
+    if (nsteps) *nsteps = cy->ring_n;
     return VX_OK;
 }
 
