@@ -29,6 +29,9 @@
 // laid out [row][32 columns] so each lane owns one bank.
 #include "vx_internal.cuh"
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <algorithm>
 #include <type_traits>
 #include <cstdlib>
@@ -37,6 +40,13 @@ namespace vx {
 namespace {
 
 constexpr int BIG = 0x7fffffff;
+// column passes: at most 16 bands (512 threads) per CTA, 3 CTAs per SM
+constexpr int kMaxBands = 16;
+constexpr int kColThreads = 32 * kMaxBands;
+#ifndef VX_COL_MIN_BLOCKS
+#define VX_COL_MIN_BLOCKS 3
+#endif
+constexpr int kColMinBlocks = VX_COL_MIN_BLOCKS;
 
 // bit e (e = 0..3) set iff byte e of w is non-zero
 __device__ __forceinline__ uint32_t nibble4(uint32_t w) {
@@ -170,6 +180,7 @@ struct ColParams {
     int nyl, j0;       // pass 3: rows of j held in this buffer and their offset
     long long splane;  // nyl * nz           (pass-3 addressing stride along x)
     long long nvox;    // nx * nyl * nz      (pass-3 scene stride)
+    int boxh, rows_alloc;  // TMA staging: rows per box, rows of smem (>= L)
 };
 
 template <int PASS, bool S2W, bool EW, bool FW>
@@ -264,7 +275,46 @@ __device__ __forceinline__ bool better(int ys, FT Fs, int yp, FT Fp, int y) {
     return Fs - Fp < (FT)2 * (FT)y * (FT)(ys - yp);
 }
 
-template <int PASS, bool S2W, bool EW, bool FW>
+// ---- TMA helpers (tile staging) ---------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)), "r"(phase) : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1,
+                                            int c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+        ::"r"(smem_u32(dst)), "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_4d(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1,
+                                            int c2, int c3) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];"
+        ::"r"(smem_u32(dst)), "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// One CTA tile: 32 consecutive k columns x the whole column length L, B bands
+// of W rows.  STAGED: the input tile was brought into the stack region of
+// shared memory by TMA and the band hulls are built in place (a band's stack
+// never grows past the rows it has consumed); otherwise rows are read with
+// coalesced 128-byte LDGs.
+template <int PASS, bool S2W, bool EW, bool FW, bool STAGED>
 __device__ __forceinline__ void column_tile(const typename Col<PASS, S2W, EW, FW>::InT *__restrict__ in,
                                             typename Col<PASS, S2W, EW, FW>::OutT *__restrict__ out,
                                             typename Col<PASS, S2W, EW, FW>::EntT *stk, int *meta,
@@ -273,6 +323,7 @@ __device__ __forceinline__ void column_tile(const typename Col<PASS, S2W, EW, FW
     using EntT = typename C::EntT;
     using FT = typename C::FT;
     using InT = typename C::InT;
+    using OutT = typename C::OutT;
 
     const int kk = threadIdx.x;
     const int b = threadIdx.y;
@@ -304,33 +355,40 @@ __device__ __forceinline__ void column_tile(const typename Col<PASS, S2W, EW, FW
     if (colok) {
         int ya = 0, yb = 0;
         FT Fa = 0, Fb = 0;
-        for (int y0 = lo; y0 < hi; y0 += 8) {
-            InT v[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const int y = y0 + u;
-                v[u] = (y < hi) ? __ldg(in + base + (long long)y * stride) : C::invalid();
-            }
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                if (!C::valid(v[u])) continue;
-                const int yc = y0 + u;
-                const EntT ec = C::make(P, v[u], yc);
-                const FT Fc = C::F(P, ec, jq, k);
-                while (n >= 2 && dominated<FT>(ya, Fa, yb, Fb, yc, Fc)) {
-                    --n;
-                    yb = ya;
-                    Fb = Fa;
-                    if (n >= 2) {
-                        const EntT t = stk[(size_t)(lo + n - 2) * 32 + kk];
-                        ya = C::row(P, t);
-                        Fa = C::F(P, t, jq, k);
-                    }
+        auto consume = [&](InT v, int yc) {
+            if (!C::valid(v)) return;
+            const EntT ec = C::make(P, v, yc);
+            const FT Fc = C::F(P, ec, jq, k);
+            while (n >= 2 && dominated<FT>(ya, Fa, yb, Fb, yc, Fc)) {
+                --n;
+                yb = ya;
+                Fb = Fa;
+                if (n >= 2) {
+                    const EntT t = stk[(size_t)(lo + n - 2) * 32 + kk];
+                    ya = C::row(P, t);
+                    Fa = C::F(P, t, jq, k);
                 }
-                stk[(size_t)(lo + n) * 32 + kk] = ec;
-                ya = yb; Fa = Fb;
-                yb = yc; Fb = Fc;
-                ++n;
+            }
+            stk[(size_t)(lo + n) * 32 + kk] = ec;
+            ya = yb; Fa = Fb;
+            yb = yc; Fb = Fc;
+            ++n;
+        };
+        if constexpr (STAGED) {
+            const InT *tin = reinterpret_cast<const InT *>(stk);
+#pragma unroll 4
+            for (int y = lo; y < hi; ++y) consume(tin[(size_t)y * 32 + kk], y);
+        } else {
+            const InT *src = in + base + (long long)lo * stride;
+            for (int y0 = lo; y0 < hi; y0 += 8) {
+                InT v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    v[u] = (y0 + u < hi) ? __ldg(src) : C::invalid();
+                    src += stride;
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) consume(v[u], y0 + u);
             }
         }
     }
@@ -407,8 +465,9 @@ __device__ __forceinline__ void column_tile(const typename Col<PASS, S2W, EW, FW
     // ---- phase D: queries for this band's rows (edt.py:300-317) ----------
     if (colok && lo < hi) {
         const int cnt = ncnt[kk];
+        OutT *dst = out + base + (long long)lo * stride;
         if (cnt == 0) {  // no candidate in the whole column (edt.py:295-299)
-            for (int y = lo; y < hi; ++y) out[base + (long long)y * stride] = C::none();
+            for (int y = lo; y < hi; ++y, dst += stride) *dst = C::none();
         } else {
             const int y0 = lo;
             // first hull vertex minimising at y0: binary search over bands ...
@@ -441,6 +500,7 @@ __device__ __forceinline__ void column_tile(const typename Col<PASS, S2W, EW, FW
             EntT cur = stk[(size_t)pos * 32 + kk];
             int yc = C::row(P, cur);
             FT Fc = C::F(P, cur, jq, k);
+            OutT ocur = C::output(P, cur);
             // successor
             int spos = -1, sm = m;
             if (pos + 1 < epos) spos = pos + 1;
@@ -453,49 +513,87 @@ __device__ __forceinline__ void column_tile(const typename Col<PASS, S2W, EW, FW
                 ys = C::row(P, sent);
                 Fs = C::F(P, sent, jq, k);
             }
-            for (int y = lo; y < hi; ++y) {
-                while (spos >= 0 && better<FT>(ys, Fs, yc, Fc, y)) {
-                    cur = sent; yc = ys; Fc = Fs; pos = spos;
-                    if (sm != m) { m = sm; epos = be[nbl[m * 32 + kk] * 32 + kk]; }
-                    if (pos + 1 < epos) spos = pos + 1;
-                    else if (m + 1 < cnt) { sm = m + 1; spos = bs[nbl[sm * 32 + kk] * 32 + kk]; }
-                    else spos = -1;
-                    if (spos >= 0) {
-                        sent = stk[(size_t)spos * 32 + kk];
-                        ys = C::row(P, sent);
-                        Fs = C::F(P, sent, jq, k);
-                    }
+            for (int y = lo; y < hi; ++y, dst += stride) {
+                if (spos >= 0 && better<FT>(ys, Fs, yc, Fc, y)) {
+                    do {
+                        cur = sent; yc = ys; Fc = Fs; pos = spos;
+                        if (sm != m) { m = sm; epos = be[nbl[m * 32 + kk] * 32 + kk]; }
+                        if (pos + 1 < epos) spos = pos + 1;
+                        else if (m + 1 < cnt) { sm = m + 1; spos = bs[nbl[sm * 32 + kk] * 32 + kk]; }
+                        else spos = -1;
+                        if (spos >= 0) {
+                            sent = stk[(size_t)spos * 32 + kk];
+                            ys = C::row(P, sent);
+                            Fs = C::F(P, sent, jq, k);
+                        }
+                    } while (spos >= 0 && better<FT>(ys, Fs, yc, Fc, y));
+                    ocur = C::output(P, cur);
                 }
-                out[base + (long long)y * stride] = C::output(P, cur);
+                *dst = ocur;
             }
         }
     }
 }
 
 template <int PASS, bool S2W, bool EW, bool FW>
-__global__ void __launch_bounds__(1024) k_column_smem(const typename Col<PASS, S2W, EW, FW>::InT *__restrict__ in,
+__global__ void __launch_bounds__(kColThreads, kColMinBlocks) k_column_smem(const typename Col<PASS, S2W, EW, FW>::InT *__restrict__ in,
                                                       typename Col<PASS, S2W, EW, FW>::OutT *__restrict__ out,
                                                       const ColParams P) {
-    extern __shared__ __align__(16) unsigned char smem[];
+    extern __shared__ __align__(128) unsigned char smem[];
     using EntT = typename Col<PASS, S2W, EW, FW>::EntT;
     EntT *stk = reinterpret_cast<EntT *>(smem);
     int *meta = reinterpret_cast<int *>(smem + (size_t)P.L * 32 * sizeof(EntT));
-    column_tile<PASS, S2W, EW, FW>(in, out, stk, meta, P, blockIdx.x);
+    column_tile<PASS, S2W, EW, FW, false>(in, out, stk, meta, P, blockIdx.x);
+}
+
+// TMA-staged variant (narrow 32-bit codes, nz % 4 == 0): one elected thread
+// issues the bulk tensor loads of the whole 32-column tile into the stack
+// region; every row of the column is in flight at once.
+template <int PASS, bool FW>
+__global__ void __launch_bounds__(kColThreads, kColMinBlocks) k_column_tma(const __grid_constant__ CUtensorMap tmap,
+                                                     typename Col<PASS, false, false, FW>::OutT *__restrict__ out,
+                                                     const ColParams P) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    using EntT = typename Col<PASS, false, false, FW>::EntT;
+    EntT *stk = reinterpret_cast<EntT *>(smem);
+    int *meta = reinterpret_cast<int *>(smem + (size_t)P.rows_alloc * 32 * sizeof(EntT));
+    uint64_t *bar = reinterpret_cast<uint64_t *>(meta + 3 * P.B * 32 + 32);
+    const long long tile = blockIdx.x;
+    if (threadIdx.x == 0 && threadIdx.y == 0) {
+        mbar_init(bar, 1);
+        const int kt = (int)(tile % P.nkt);
+        const long long outer = tile / P.nkt;
+        const int nbox = P.rows_alloc / P.boxh;
+        mbar_expect_tx(bar, (uint32_t)(P.rows_alloc * 32 * sizeof(EntT)));
+        for (int q = 0; q < nbox; ++q) {
+            void *dst = stk + (size_t)q * P.boxh * 32;
+            if constexpr (PASS == 2) {
+                tma_load_3d(dst, &tmap, bar, kt * 32, q * P.boxh, (int)outer);
+            } else {
+                const int scene = (int)(outer / P.nyl);
+                const int jl = (int)(outer - (long long)scene * P.nyl);
+                tma_load_4d(dst, &tmap, bar, kt * 32, jl, q * P.boxh, scene);
+            }
+        }
+    }
+    __syncthreads();
+    mbar_wait(bar, 0);
+    column_tile<PASS, false, false, FW, true>(nullptr, out, stk, meta, P, tile);
 }
 
 // Columns too long for shared memory: per-CTA stack slab in global scratch,
 // persistent over tiles.
 template <int PASS, bool S2W, bool EW, bool FW>
-__global__ void __launch_bounds__(1024) k_column_gstack(const typename Col<PASS, S2W, EW, FW>::InT *__restrict__ in,
+__global__ void __launch_bounds__(kColThreads, kColMinBlocks) k_column_gstack(const typename Col<PASS, S2W, EW, FW>::InT *__restrict__ in,
                                                         typename Col<PASS, S2W, EW, FW>::OutT *__restrict__ out,
                                                         typename Col<PASS, S2W, EW, FW>::EntT *gstack,
                                                         const ColParams P) {
-    extern __shared__ __align__(16) unsigned char smem[];
+    extern __shared__ __align__(128) unsigned char smem[];
     using EntT = typename Col<PASS, S2W, EW, FW>::EntT;
     EntT *stk = gstack + (size_t)blockIdx.x * P.L * 32;
     int *meta = reinterpret_cast<int *>(smem);
     for (long long t = blockIdx.x; t < P.ntiles; t += gridDim.x) {
-        column_tile<PASS, S2W, EW, FW>(in, out, stk, meta, P, t);
+        column_tile<PASS, S2W, EW, FW, false>(in, out, stk, meta, P, t);
         __syncthreads();
     }
 }
@@ -533,25 +631,85 @@ ColParams col_params(const EdtPlan &p, int pass, long long nouter, int nyl, int 
     P.ymask = p.yb >= 32 ? 0xffffffffu : ((1u << p.yb) - 1u);
     P.plane = (long long)p.ny * p.nz;
     P.nvox = P.splane * p.nx;
+    P.boxh = std::min(P.L, 256);
+    P.rows_alloc = (P.L + P.boxh - 1) / P.boxh * P.boxh;
     return P;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+// TMA view of a column pass input: 3D (k, y, slice) for pass 2, 4D
+// (k, j, x, scene) for pass 3; box = 32 columns x boxh rows.
+bool make_tmap(CUtensorMap *m, const void *in, const EdtPlan &p, int pass, long long nouter, int nyl,
+               int boxh) {
+    auto enc = tmap_encoder();
+    if (!enc) return false;
+    cuuint64_t dims[4], strides[3];
+    cuuint32_t box[4], estr[4] = {1, 1, 1, 1};
+    cuuint32_t rank;
+    if (pass == 2) {
+        rank = 3;
+        dims[0] = p.nz; dims[1] = p.ny; dims[2] = (cuuint64_t)nouter;
+        strides[0] = (cuuint64_t)p.nz * 4; strides[1] = (cuuint64_t)p.ny * p.nz * 4;
+        box[0] = 32; box[1] = boxh; box[2] = 1;
+    } else {
+        rank = 4;
+        const long long nscenes = nouter / nyl;
+        dims[0] = p.nz; dims[1] = nyl; dims[2] = p.nx; dims[3] = (cuuint64_t)nscenes;
+        strides[0] = (cuuint64_t)p.nz * 4; strides[1] = (cuuint64_t)nyl * p.nz * 4;
+        strides[2] = (cuuint64_t)p.nx * nyl * p.nz * 4;
+        box[0] = 32; box[1] = 1; box[2] = boxh; box[3] = 1;
+    }
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, rank, const_cast<void *>(in), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
 }
 
 template <int PASS, bool S2W, bool EW, bool FW>
 cudaError_t launch_col(const void *in, void *out, void *gstack, const EdtPlan &p, long long nouter,
                        int nyl, int j0, cudaStream_t st) {
     using C = Col<PASS, S2W, EW, FW>;
-    const ColParams P = col_params(p, PASS, nouter, nyl, j0);
+    ColParams P = col_params(p, PASS, nouter, nyl, j0);
     if (P.ntiles == 0) return cudaSuccess;
     const dim3 block(32, P.B);
     const bool gs = PASS == 2 ? p.gstack2 : p.gstack3;
-    const size_t smem = PASS == 2 ? p.smem2 : p.smem3;
+    const bool staged = PASS == 2 ? p.tma2 : p.tma3;
+    if constexpr (!S2W && !EW) {
+        if (staged && !gs) {
+            CUtensorMap m;
+            if (make_tmap(&m, in, p, PASS, nouter, nyl, P.boxh)) {
+                const size_t smem = PASS == 2 ? p.smem2 : p.smem3;
+                auto kern = k_column_tma<PASS, FW>;
+                cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                if (e != cudaSuccess) return e;
+                kern<<<(unsigned)P.ntiles, block, smem, st>>>(m, reinterpret_cast<typename C::OutT *>(out), P);
+                return cudaGetLastError();
+            }
+        }
+    }
+    P.rows_alloc = P.L;
     if (!gs) {
+        const size_t smem = (size_t)P.L * 32 * sizeof(typename C::EntT) + (size_t)(3 * P.B * 32 + 32) * 4;
         auto kern = k_column_smem<PASS, S2W, EW, FW>;
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         kern<<<(unsigned)P.ntiles, block, smem, st>>>(
             reinterpret_cast<const typename C::InT *>(in), reinterpret_cast<typename C::OutT *>(out), P);
     } else {
+        const size_t smem = (size_t)(3 * P.B * 32 + 32) * 4;
         auto kern = k_column_gstack<PASS, S2W, EW, FW>;
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
@@ -612,7 +770,7 @@ bool make_plan(int nx, int ny, int nz, EdtPlan *p, int force_global_stack) {
     q.fwide = q.e3_wide || force_wide >= 1 || (2.0 * fmax * lmax >= 2147483647.0) ||
               (2.0 * lmax * lmax >= 2147483647.0);
     auto bands = [](int L, int &B, int &W) {
-        B = std::min(32, pow2ceil((L + 31) / 32));
+        B = std::min(kMaxBands, pow2ceil((L + 31) / 32));
         W = (L + B - 1) / B;
     };
     bands(ny, q.B2, q.W2);
@@ -626,6 +784,20 @@ bool make_plan(int nx, int ny, int nz, EdtPlan *p, int force_global_stack) {
     q.gstack3 = force_global_stack || st3 + meta3 > kSmemLimit;
     q.smem2 = q.gstack2 ? meta2 : st2 + meta2;
     q.smem3 = q.gstack3 ? meta3 : st3 + meta3;
+    // TMA tile staging: 32-bit codes, 16-byte row strides (nz % 4 == 0), and
+    // the box-rounded tile (+ mbarrier) must fit; VX_NO_TMA=1 disables it
+    const char *nt = getenv("VX_NO_TMA");
+    const bool tma_ok = !(nt && atoi(nt)) && nz % 4 == 0;
+    auto staged_bytes = [](int L, int B) {
+        const int boxh = std::min(L, 256);
+        const size_t rows = (size_t)(L + boxh - 1) / boxh * boxh;
+        return rows * 32 * 4 + (size_t)(3 * B * 32 + 32) * 4 + 16;
+    };
+    const size_t sb2 = staged_bytes(ny, q.B2), sb3 = staged_bytes(nx, q.B3);
+    q.tma2 = tma_ok && !q.s2_wide && !q.gstack2 && sb2 <= kSmemLimit;
+    q.tma3 = tma_ok && !q.s2_wide && !q.e3_wide && !q.gstack3 && sb3 <= kSmemLimit;
+    if (q.tma2) q.smem2 = sb2;
+    if (q.tma3) q.smem3 = sb3;
     q.gstack_ctas = 2 * num_sms();
     size_t gs = 0;
     if (q.gstack2) gs = std::max(gs, (size_t)q.gstack_ctas * st2);

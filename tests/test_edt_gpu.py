@@ -60,7 +60,7 @@ def test_thin_and_degenerate_grids():
     rng = np.random.default_rng(55)   # test_edt.py:209-218 plus more
     shapes = [(1, 24, 16), (24, 1, 16), (24, 16, 1), (1, 1, 30), (30, 1, 1), (1, 30, 1),
               (2, 2, 2), (1, 1, 1), (1, 1, 4097), (4097, 1, 1), (1, 4097, 1), (3, 5, 2100),
-              (33, 65, 129), (130, 3, 7)]
+              (33, 65, 129), (130, 3, 7), (300, 7, 36), (5, 700, 20), (257, 513, 4)]
     for dims in shapes:
         for p in (0.0, 0.001, 0.25, 1.0):
             occ = rng.random(dims) < p
@@ -99,7 +99,8 @@ print("ok")
 
 @pytest.mark.parametrize("env", [{"VX_FORCE_WIDE": "1"}, {"VX_FORCE_WIDE": "2"},
                                  {"VX_FORCE_WIDE": "3"}, {"VX_FORCE_GSTACK": "1"},
-                                 {"VX_FORCE_WIDE": "3", "VX_FORCE_GSTACK": "1"}],
+                                 {"VX_FORCE_WIDE": "3", "VX_FORCE_GSTACK": "1"},
+                                 {"VX_NO_TMA": "1"}],
                          ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
 def test_wide_and_gstack_variants(env):
     """Every template variant (int64 weights, u64 entries / codes, global
