@@ -35,7 +35,6 @@
 #include <algorithm>
 #include <type_traits>
 #include <cstdlib>
-#include <climits>
 
 namespace vx {
 namespace {
@@ -276,23 +275,6 @@ __device__ __forceinline__ bool better(int ys, FT Fs, int yp, FT Fp, int y) {
     return Fs - Fp < (FT)2 * (FT)y * (FT)(ys - yp);
 }
 
-// Smallest row y with  N < y * D  (D > 0): the first row at which the
-// successor vertex is strictly closer (F_s - F_c < 2 y (y_s - y_c)).
-// Float/double estimate, then exact integer correction.
-template <typename FT>
-__device__ __forceinline__ int first_closer(FT N, int D) {
-    int y;
-    if constexpr (sizeof(FT) == 4) {
-        y = (int)floorf(__fdiv_rn((float)N, (float)D)) + 1;
-    } else {
-        const double q = floor((double)N / (double)D) + 1.0;
-        y = q > 2.0e9 ? 2000000000 : (q < -2.0e9 ? -2000000000 : (int)q);
-    }
-    while (!(N < (FT)y * (FT)D)) ++y;
-    while (N < (FT)(y - 1) * (FT)D) --y;
-    return y;
-}
-
 // ---- TMA helpers (tile staging) ---------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return (uint32_t)__cvta_generic_to_shared(p);
@@ -363,6 +345,8 @@ __device__ __forceinline__ void column_tile(const typename Col<PASS, S2W, EW, FW
     }
     int *bs = meta;
     int *be = bs + P.B * 32;
+    int *nbl = be + P.B * 32;
+    int *ncnt = nbl + P.B * 32;
     const int lo = min(P.L, b * P.W);
     const int hi = min(P.L, lo + P.W);
 
@@ -469,24 +453,28 @@ __device__ __forceinline__ void column_tile(const typename Col<PASS, S2W, EW, FW
         __syncthreads();
     }
 
+    // ---- phase C: list of non-empty bands per column ---------------------
+    if (b == 0) {
+        int c = 0;
+        for (int q = 0; q < P.B; ++q)
+            if (bs[q * 32 + kk] < be[q * 32 + kk]) nbl[(c++) * 32 + kk] = q;
+        ncnt[kk] = c;
+    }
+    __syncthreads();
+
     // ---- phase D: queries for this band's rows (edt.py:300-317) ----------
     if (colok && lo < hi) {
-        // non-empty bands of this column as a bit mask (B <= 16)
-        uint32_t mask = 0;
-        for (int q = 0; q < P.B; ++q)
-            if (bs[q * 32 + kk] < be[q * 32 + kk]) mask |= 1u << q;
-        const int cnt = __popc(mask);
+        const int cnt = ncnt[kk];
         OutT *dst = out + base + (long long)lo * stride;
         if (cnt == 0) {  // no candidate in the whole column (edt.py:295-299)
             for (int y = lo; y < hi; ++y, dst += stride) *dst = C::none();
         } else {
             const int y0 = lo;
-            // first hull vertex minimising at y0: binary search over the
-            // non-empty bands (m-th set bit of mask) ...
+            // first hull vertex minimising at y0: binary search over bands ...
             int mlo = 0, mhi = cnt - 1;
             while (mlo < mhi) {
                 const int mid = (mlo + mhi) >> 1;
-                const int bm = __fns(mask, 0, mid + 1), bn = __fns(mask, 0, mid + 2);
+                const int bm = nbl[mid * 32 + kk], bn = nbl[(mid + 1) * 32 + kk];
                 const EntT a = stk[(size_t)(be[bm * 32 + kk] - 1) * 32 + kk];
                 const EntT s = stk[(size_t)bs[bn * 32 + kk] * 32 + kk];
                 if (better<FT>(C::row(P, s), C::F(P, s, jq, k), C::row(P, a), C::F(P, a, jq, k), y0))
@@ -494,7 +482,8 @@ __device__ __forceinline__ void column_tile(const typename Col<PASS, S2W, EW, FW
                 else
                     mhi = mid;
             }
-            int bm = __fns(mask, 0, mlo + 1);
+            int m = mlo;
+            int bm = nbl[m * 32 + kk];
             // ... then inside the band
             int ilo = bs[bm * 32 + kk], ihi = be[bm * 32 + kk] - 1;
             while (ilo < ihi) {
@@ -511,39 +500,33 @@ __device__ __forceinline__ void column_tile(const typename Col<PASS, S2W, EW, FW
             EntT cur = stk[(size_t)pos * 32 + kk];
             int yc = C::row(P, cur);
             FT Fc = C::F(P, cur, jq, k);
-            // successor of the current vertex and the first row at which it
-            // is strictly closer (the strict-< walk of edt.py:311, hoisted)
-            int spos = -1, ys = 0, yth = INT_MAX;
-            FT Fs = 0;
-            EntT sent = 0;
-            auto next_succ = [&]() {
-                if (pos + 1 < epos) {
-                    spos = pos + 1;
-                } else {
-                    const uint32_t rest = mask & ~((2u << bm) - 1u);
-                    spos = rest ? bs[(__ffs(rest) - 1) * 32 + kk] : -1;
-                }
-                if (spos >= 0) {
-                    sent = stk[(size_t)spos * 32 + kk];
-                    ys = C::row(P, sent);
-                    Fs = C::F(P, sent, jq, k);
-                    yth = first_closer<FT>(Fs - Fc, 2 * (ys - yc));
-                } else {
-                    yth = INT_MAX;
-                }
-            };
-            next_succ();
             OutT ocur = C::output(P, cur);
+            // successor
+            int spos = -1, sm = m;
+            if (pos + 1 < epos) spos = pos + 1;
+            else if (m + 1 < cnt) { sm = m + 1; spos = bs[nbl[sm * 32 + kk] * 32 + kk]; }
+            EntT sent = 0;
+            int ys = 0;
+            FT Fs = 0;
+            if (spos >= 0) {
+                sent = stk[(size_t)spos * 32 + kk];
+                ys = C::row(P, sent);
+                Fs = C::F(P, sent, jq, k);
+            }
             for (int y = lo; y < hi; ++y, dst += stride) {
-                if (y >= yth) {
+                if (spos >= 0 && better<FT>(ys, Fs, yc, Fc, y)) {
                     do {
-                        if (spos >= epos) {   // the successor is in the next non-empty band
-                            bm = __ffs(mask & ~((2u << bm) - 1u)) - 1;
-                            epos = be[bm * 32 + kk];
-                        }
                         cur = sent; yc = ys; Fc = Fs; pos = spos;
-                        next_succ();
-                    } while (y >= yth);
+                        if (sm != m) { m = sm; epos = be[nbl[m * 32 + kk] * 32 + kk]; }
+                        if (pos + 1 < epos) spos = pos + 1;
+                        else if (m + 1 < cnt) { sm = m + 1; spos = bs[nbl[sm * 32 + kk] * 32 + kk]; }
+                        else spos = -1;
+                        if (spos >= 0) {
+                            sent = stk[(size_t)spos * 32 + kk];
+                            ys = C::row(P, sent);
+                            Fs = C::F(P, sent, jq, k);
+                        }
+                    } while (spos >= 0 && better<FT>(ys, Fs, yc, Fc, y));
                     ocur = C::output(P, cur);
                 }
                 *dst = ocur;
