@@ -40,11 +40,28 @@ namespace vx {
 namespace {
 
 constexpr int BIG = 0x7fffffff;
+
+#ifdef VX_PHASE_TIMING   // tools/phase_timing.cu: per-CTA phase timestamps
+__device__ unsigned long long *g_phase_buf = nullptr;
+#define VX_PT(i)                                                                       \
+    do {                                                                               \
+        if (threadIdx.x == 0 && threadIdx.y == 0 && g_phase_buf)                       \
+            g_phase_buf[(size_t)blockIdx.x * 8 + (i)] = clock64();                     \
+    } while (0)
+#else
+#define VX_PT(i) do {} while (0)
+#endif
 // column passes: at most 16 bands (512 threads) per CTA, 3 CTAs per SM
-constexpr int kMaxBands = 16;
+#ifndef VX_MAX_BANDS
+#define VX_MAX_BANDS 16
+#endif
+constexpr int kMaxBands = VX_MAX_BANDS;
 constexpr int kColThreads = 32 * kMaxBands;
+#ifndef VX_BAND_ROWS
+#define VX_BAND_ROWS 32   // target rows per band
+#endif
 #ifndef VX_COL_MIN_BLOCKS
-#define VX_COL_MIN_BLOCKS 3
+#define VX_COL_MIN_BLOCKS 2
 #endif
 constexpr int kColMinBlocks = VX_COL_MIN_BLOCKS;
 
@@ -181,6 +198,8 @@ struct ColParams {
     long long splane;  // nyl * nz           (pass-3 addressing stride along x)
     long long nvox;    // nx * nyl * nz      (pass-3 scene stride)
     int boxh, rows_alloc;  // TMA staging: rows per box, rows of smem (>= L)
+    int wb;                // pass 3 narrow entry: (x << wb) | w, w = dy^2 + dz^2
+    uint32_t wmask;
 };
 
 template <int PASS, bool S2W, bool EW, bool FW>
@@ -200,8 +219,11 @@ struct Col {
         if constexpr (PASS == 2) return -1;
         else return (S2T)~(S2T)0;
     }
-    // pass-2 entry == the s2 code of the site (row y, line site z)
-    static __device__ __forceinline__ EntT make(const ColParams &P, InT v, int row) {
+    // pass-2 entry == the s2 code of the site (row y, line site z).
+    // pass-3 narrow entry == (x << wb) | w with w = (j-sy)^2 + (k-sz)^2, so
+    // F = x^2 + w costs one multiply; the site code of a winning row is
+    // re-read from the (L2-resident) pass-3 input when it is emitted.
+    static __device__ __forceinline__ EntT make(const ColParams &P, InT v, int row, int j, int k) {
         if constexpr (PASS == 2) {
             if constexpr (S2W) return ((EntT)row << 32) | (EntT)(uint32_t)v;
             else return ((EntT)row << P.zb) | (EntT)v;
@@ -209,8 +231,12 @@ struct Col {
             uint32_t sy, sz;
             if constexpr (S2W) { sy = (uint32_t)(v >> 32); sz = (uint32_t)v; }
             else { sy = (uint32_t)v >> P.zb; sz = (uint32_t)v & P.zmask; }
-            if constexpr (EW) return ((EntT)row << 42) | ((EntT)sy << 21) | (EntT)sz;
-            else return ((EntT)row << P.yzb) | (EntT)v;
+            if constexpr (EW) {
+                return ((EntT)row << 42) | ((EntT)sy << 21) | (EntT)sz;
+            } else {
+                const int dy = j - (int)sy, dz = k - (int)sz;
+                return ((EntT)row << P.wb) | (EntT)(uint32_t)(dy * dy + dz * dz);
+            }
         }
     }
     static __device__ __forceinline__ int row(const ColParams &P, EntT e) {
@@ -219,7 +245,7 @@ struct Col {
             else return (int)(e >> P.zb);
         } else {
             if constexpr (EW) return (int)(e >> 42);
-            else return (int)(e >> P.yzb);
+            else return (int)(e >> P.wb);
         }
     }
     // F = w + row^2 (edt.py:261-262, 362-364 fold the row term in at test time)
@@ -231,18 +257,19 @@ struct Col {
             const FT dz = (FT)(k - z);
             return dz * dz + (FT)y * (FT)y;
         } else {
-            int x, sy, sz;
             if constexpr (EW) {
-                x = (int)(e >> 42); sy = (int)((e >> 21) & 0x1fffffull); sz = (int)(e & 0x1fffffull);
+                const int x = (int)(e >> 42), sy = (int)((e >> 21) & 0x1fffffull), sz = (int)(e & 0x1fffffull);
+                const FT dy = (FT)(j - sy), dz = (FT)(k - sz);
+                return dy * dy + dz * dz + (FT)x * (FT)x;
             } else {
-                x = (int)(e >> P.yzb); sy = (int)(((uint32_t)e >> P.zb) & P.ymask);
-                sz = (int)((uint32_t)e & P.zmask);
+                const int x = (int)(e >> P.wb);
+                return (FT)x * (FT)x + (FT)((uint32_t)e & P.wmask);
             }
-            const FT dy = (FT)(j - sy), dz = (FT)(k - sz);
-            return dy * dy + dz * dz + (FT)x * (FT)x;
         }
     }
-    static __device__ __forceinline__ OutT output(const ColParams &P, EntT e) {
+    // pass 3 narrow: does output() need the site code re-read from the input?
+    static constexpr bool kRereadCode = PASS == 3 && !EW;
+    static __device__ __forceinline__ OutT output(const ColParams &P, EntT e, InT code) {
         if constexpr (PASS == 2) {
             return (OutT)e;  // the entry is the s2 code
         } else {
@@ -251,8 +278,9 @@ struct Col {
                 x = (long long)(e >> 42); sy = (long long)((e >> 21) & 0x1fffffull);
                 sz = (long long)(e & 0x1fffffull);
             } else {
-                x = (long long)(e >> P.yzb); sy = (long long)(((uint32_t)e >> P.zb) & P.ymask);
-                sz = (long long)((uint32_t)e & P.zmask);
+                x = (long long)(e >> P.wb);
+                if constexpr (S2W) { sy = (long long)(code >> 32); sz = (long long)(uint32_t)code; }
+                else { sy = (long long)((uint32_t)code >> P.zb); sz = (long long)((uint32_t)code & P.zmask); }
             }
             return (int32_t)(x * P.plane + sy * P.nz + sz);  // edt.py:417
         }
@@ -350,6 +378,7 @@ __device__ __forceinline__ void column_tile(const typename Col<PASS, S2W, EW, FW
     const int lo = min(P.L, b * P.W);
     const int hi = min(P.L, lo + P.W);
 
+    VX_PT(1);
     // ---- phase A: band-local hull (edt.py:253-276 for one band) ----------
     int n = 0;
     if (colok) {
@@ -357,7 +386,7 @@ __device__ __forceinline__ void column_tile(const typename Col<PASS, S2W, EW, FW
         FT Fa = 0, Fb = 0;
         auto consume = [&](InT v, int yc) {
             if (!C::valid(v)) return;
-            const EntT ec = C::make(P, v, yc);
+            const EntT ec = C::make(P, v, yc, jq, k);
             const FT Fc = C::F(P, ec, jq, k);
             while (n >= 2 && dominated<FT>(ya, Fa, yb, Fb, yc, Fc)) {
                 --n;
@@ -395,6 +424,7 @@ __device__ __forceinline__ void column_tile(const typename Col<PASS, S2W, EW, FW
     bs[b * 32 + kk] = lo;
     be[b * 32 + kk] = lo + n;
     __syncthreads();
+    VX_PT(2);
 
     // ---- phase B: pairwise bridge merges (same hull as edt.py:277-294) ---
     for (int r = 1; r < P.B; r <<= 1) {
@@ -453,6 +483,7 @@ __device__ __forceinline__ void column_tile(const typename Col<PASS, S2W, EW, FW
         __syncthreads();
     }
 
+    VX_PT(3);
     // ---- phase C: list of non-empty bands per column ---------------------
     if (b == 0) {
         int c = 0;
@@ -462,6 +493,7 @@ __device__ __forceinline__ void column_tile(const typename Col<PASS, S2W, EW, FW
     }
     __syncthreads();
 
+    VX_PT(4);
     // ---- phase D: queries for this band's rows (edt.py:300-317) ----------
     if (colok && lo < hi) {
         const int cnt = ncnt[kk];
@@ -500,7 +532,12 @@ __device__ __forceinline__ void column_tile(const typename Col<PASS, S2W, EW, FW
             EntT cur = stk[(size_t)pos * 32 + kk];
             int yc = C::row(P, cur);
             FT Fc = C::F(P, cur, jq, k);
-            OutT ocur = C::output(P, cur);
+            const InT *src = in + base;
+            auto code_of = [&](int row) -> InT {
+                if constexpr (C::kRereadCode) return __ldg(src + (long long)row * stride);
+                else return InT(0);
+            };
+            OutT ocur = C::output(P, cur, code_of(yc));
             // successor
             int spos = -1, sm = m;
             if (pos + 1 < epos) spos = pos + 1;
@@ -508,15 +545,24 @@ __device__ __forceinline__ void column_tile(const typename Col<PASS, S2W, EW, FW
             EntT sent = 0;
             int ys = 0;
             FT Fs = 0;
+            InT scode = InT(0);   // the successor's site code, prefetched
             if (spos >= 0) {
                 sent = stk[(size_t)spos * 32 + kk];
                 ys = C::row(P, sent);
                 Fs = C::F(P, sent, jq, k);
+                scode = code_of(ys);
             }
-            for (int y = lo; y < hi; ++y, dst += stride) {
-                if (spos >= 0 && better<FT>(ys, Fs, yc, Fc, y)) {
+            // successor strictly closer at row y  <=>  Fs - Fc < y * 2 (ys - yc)
+            // (edt.py:311); the right side is stepped by t per row
+            constexpr FT kNever = sizeof(FT) == 4 ? (FT)0x7fffffff : (FT)0x7fffffffffffffffLL;
+            FT dN = spos >= 0 ? Fs - Fc : kNever;
+            FT t = spos >= 0 ? (FT)2 * (FT)(ys - yc) : (FT)0;
+            FT rhs = (FT)lo * t;
+            for (int y = lo; y < hi; ++y, dst += stride, rhs += t) {
+                if (dN < rhs) {
+                    InT ccode = scode;
                     do {
-                        cur = sent; yc = ys; Fc = Fs; pos = spos;
+                        cur = sent; yc = ys; Fc = Fs; pos = spos; ccode = scode;
                         if (sm != m) { m = sm; epos = be[nbl[m * 32 + kk] * 32 + kk]; }
                         if (pos + 1 < epos) spos = pos + 1;
                         else if (m + 1 < cnt) { sm = m + 1; spos = bs[nbl[sm * 32 + kk] * 32 + kk]; }
@@ -525,9 +571,13 @@ __device__ __forceinline__ void column_tile(const typename Col<PASS, S2W, EW, FW
                             sent = stk[(size_t)spos * 32 + kk];
                             ys = C::row(P, sent);
                             Fs = C::F(P, sent, jq, k);
+                            scode = code_of(ys);
                         }
                     } while (spos >= 0 && better<FT>(ys, Fs, yc, Fc, y));
-                    ocur = C::output(P, cur);
+                    ocur = C::output(P, cur, ccode);
+                    dN = spos >= 0 ? Fs - Fc : kNever;
+                    t = spos >= 0 ? (FT)2 * (FT)(ys - yc) : (FT)0;
+                    rhs = (FT)y * t;
                 }
                 *dst = ocur;
             }
@@ -551,6 +601,7 @@ __global__ void __launch_bounds__(kColThreads, kColMinBlocks) k_column_smem(cons
 // region; every row of the column is in flight at once.
 template <int PASS, bool FW>
 __global__ void __launch_bounds__(kColThreads, kColMinBlocks) k_column_tma(const __grid_constant__ CUtensorMap tmap,
+                                                     const typename Col<PASS, false, false, FW>::InT *__restrict__ in,
                                                      typename Col<PASS, false, false, FW>::OutT *__restrict__ out,
                                                      const ColParams P) {
     extern __shared__ __align__(128) unsigned char smem[];
@@ -559,6 +610,7 @@ __global__ void __launch_bounds__(kColThreads, kColMinBlocks) k_column_tma(const
     int *meta = reinterpret_cast<int *>(smem + (size_t)P.rows_alloc * 32 * sizeof(EntT));
     uint64_t *bar = reinterpret_cast<uint64_t *>(meta + 3 * P.B * 32 + 32);
     const long long tile = blockIdx.x;
+    VX_PT(0);
     if (threadIdx.x == 0 && threadIdx.y == 0) {
         mbar_init(bar, 1);
         const int kt = (int)(tile % P.nkt);
@@ -578,7 +630,12 @@ __global__ void __launch_bounds__(kColThreads, kColMinBlocks) k_column_tma(const
     }
     __syncthreads();
     mbar_wait(bar, 0);
-    column_tile<PASS, false, false, FW, true>(nullptr, out, stk, meta, P, tile);
+    column_tile<PASS, false, false, FW, true>(in, out, stk, meta, P, tile);
+#ifdef VX_PHASE_TIMING
+    VX_PT(5);
+    __syncthreads();
+    VX_PT(6);
+#endif
 }
 
 // Columns too long for shared memory: per-CTA stack slab in global scratch,
@@ -631,6 +688,8 @@ ColParams col_params(const EdtPlan &p, int pass, long long nouter, int nyl, int 
     P.ymask = p.yb >= 32 ? 0xffffffffu : ((1u << p.yb) - 1u);
     P.plane = (long long)p.ny * p.nz;
     P.nvox = P.splane * p.nx;
+    P.wb = p.wb;
+    P.wmask = p.wb >= 32 ? 0xffffffffu : ((1u << p.wb) - 1u);
     P.boxh = std::min(P.L, 256);
     P.rows_alloc = (P.L + P.boxh - 1) / P.boxh * P.boxh;
     return P;
@@ -695,7 +754,8 @@ cudaError_t launch_col(const void *in, void *out, void *gstack, const EdtPlan &p
                 auto kern = k_column_tma<PASS, FW>;
                 cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
                 if (e != cudaSuccess) return e;
-                kern<<<(unsigned)P.ntiles, block, smem, st>>>(m, reinterpret_cast<typename C::OutT *>(out), P);
+                kern<<<(unsigned)P.ntiles, block, smem, st>>>(m, reinterpret_cast<const typename C::InT *>(in),
+                                                              reinterpret_cast<typename C::OutT *>(out), P);
                 return cudaGetLastError();
             }
         }
@@ -762,7 +822,8 @@ bool make_plan(int nx, int ny, int nz, EdtPlan *p, int force_global_stack) {
     const char *fg = getenv("VX_FORCE_GSTACK");
     if (fg && atoi(fg)) force_global_stack = 1;
     q.s2_wide = q.yb + q.zb > 31 || force_wide >= 3;   // keep all-ones free as the sentinel
-    q.e3_wide = q.s2_wide || (q.xb + q.yb + q.zb > 32) || force_wide >= 2;
+    q.wb = bits_of((long long)(ny - 1) * (ny - 1) + (long long)(nz - 1) * (nz - 1));
+    q.e3_wide = q.s2_wide || (q.xb + q.wb > 32) || force_wide >= 2;
     // weights: F = w + row^2 <= (nx-1)^2+(ny-1)^2+(nz-1)^2; products F * L
     const double fmax = (double)(nx - 1) * (nx - 1) + (double)(ny - 1) * (ny - 1) +
                         (double)(nz - 1) * (nz - 1);
@@ -770,7 +831,7 @@ bool make_plan(int nx, int ny, int nz, EdtPlan *p, int force_global_stack) {
     q.fwide = q.e3_wide || force_wide >= 1 || (2.0 * fmax * lmax >= 2147483647.0) ||
               (2.0 * lmax * lmax >= 2147483647.0);
     auto bands = [](int L, int &B, int &W) {
-        B = std::min(kMaxBands, pow2ceil((L + 31) / 32));
+        B = std::min(kMaxBands, pow2ceil((L + VX_BAND_ROWS - 1) / VX_BAND_ROWS));
         W = (L + B - 1) / B;
     };
     bands(ny, q.B2, q.W2);

@@ -13,6 +13,7 @@ namespace vx {
 struct EdtPlan {
     int nx, ny, nz;
     int zb, yb, xb;        // bits(n-1) per axis: packing widths
+    int wb;                // bits of the largest pass-3 weight (ny-1)^2 + (nz-1)^2
     bool s2_wide;          // pass-2 output as u64 (y<<32 | z) instead of u32 (y<<zb | z)
     bool e3_wide;          // pass-3 stack entries as u64
     bool fwide;            // int64 weights/products (extents beyond ~700)
