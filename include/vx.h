@@ -137,6 +137,17 @@ int vx_edt_device(vx_ctx *ctx, const uint8_t *d_occ, int nx, int ny, int nz, int
 int vx_edt_s2_bytes(int nx, int ny, int nz);
 int vx_edt_pass12_device(vx_ctx *ctx, const uint8_t *d_occ, int nx, int ny, int nz, int nxl,
                          void *d_s2, void *d_scratch, size_t scratch_bytes);
+/* slab mode with the exchange fused into pass 2's epilogue: the pass-2 code
+ * of row j of local slice i is stored straight into the pass-3 input of the
+ * rank q owning j (j_starts[q] <= j < j_starts[q+1], j_starts[0] = 0,
+ * j_starts[nranks] = ny): dst[q] + ((x_base + i) * nyl_q + j - j_starts[q])
+ * * nz + k.  dst[q] is a device pointer: a peer's buffer mapped over NVLink
+ * (x_base = this rank's first global i, buffer (nx, nyl_q, nz)), or this
+ * rank's all-to-all send block for q (x_base = 0, block (nxl, nyl_q, nz)).
+ * nranks <= 64. */
+int vx_edt_pass12_scatter(vx_ctx *ctx, const uint8_t *d_occ, int nx, int ny, int nz, int nxl,
+                          int nranks, void *const *dst, const int *j_starts, long long x_base,
+                          void *d_scratch, size_t scratch_bytes);
 /* pass 3 over a j-slab: d_s2 holds (nx, nyl, nz) codes for global rows
  * j0..j0+nyl-1; d_site receives global flat indices, shape (nx, nyl, nz). */
 int vx_edt_pass3_device(vx_ctx *ctx, const void *d_s2, int nx, int ny, int nz, int j0, int nyl,

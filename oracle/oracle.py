@@ -47,6 +47,7 @@ def lib():
         L.vxo_sweep_lines.argtypes = [P, i32, i32, i32, i32, P, i32]
         L.vxo_slice_transform.argtypes = [P, i32, i32, i32, i32, i32, P, P, i32]
         L.vxo_column_transform.argtypes = [P, P, i32, i32, i32, i32, i32, P, i32]
+        L.vxo_column_transform_slab.argtypes = [P, P, i32, i32, i32, i32, i32, i32, i32, P, i32]
         L.vxo_pba_edt.argtypes = [P, i32, i32, i32, i32, i32, i32, P, i32]
         L.vxo_pba_edt.restype = i32
         L.vxo_insert_points.argtypes = [P, P, ctypes.c_double, P, P, i64, P,
@@ -96,6 +97,18 @@ def slice_transform(s1z: np.ndarray, m2: int = 1, m3: int = 2, workers: int = 0)
     lib().vxo_slice_transform(_ptr(s1z), *s1z.shape, int(m2), int(m3), _ptr(s2y),
                               _ptr(s2z), int(workers))
     return s2y, s2z
+
+
+def column_transform_slab(s2y: np.ndarray, s2z: np.ndarray, j0: int, ny_total: int,
+                          m2: int = 1, m3: int = 2, workers: int = 0) -> np.ndarray:
+    """edt.py:320-420 on a j-slab (nx, nyl, nz) holding global rows j0.. of a
+    grid with ny_total rows (test support for the slab-decomposed path)."""
+    s2y = np.ascontiguousarray(s2y, dtype=np.int32)
+    s2z = np.ascontiguousarray(s2z, dtype=np.int32)
+    site = np.empty(s2y.shape, np.int32)
+    lib().vxo_column_transform_slab(_ptr(s2y), _ptr(s2z), *s2y.shape, int(j0), int(ny_total),
+                                    int(m2), int(m3), _ptr(site), int(workers))
+    return site
 
 
 def pba_edt_site(occupancy, m1: int = 1, m2: int = 1, m3: int = 2,

@@ -34,7 +34,7 @@ EXPORTS = (
     "vx_field_site_at", "vx_field_site_world", "vx_edt_scratch_bytes", "vx_edt_device",
     "vx_edt_s2_bytes", "vx_edt_pass12_device", "vx_edt_pass3_device", "vx_cycle_create",
     "vx_cycle_destroy", "vx_cycle_step", "vx_cycle_wait", "vx_cycle_fields", "vx_cycle_grids",
-    "vx_cycle_profile", "vx_cycle_phase_ms", "vx_cycle_step_device",
+    "vx_cycle_profile", "vx_cycle_phase_ms", "vx_cycle_step_device", "vx_edt_pass12_scatter",
 )
 CYCLE_PHASES = ("h2d", "self_map", "mask_stamp_reset", "scatter", "edt_pass1", "edt_pass2",
                 "edt_pass3", "gather")
@@ -107,6 +107,7 @@ def load():
             "vx_edt_s2_bytes": ([i32, i32, i32], i32),
             "vx_edt_pass12_device": ([P, P, i32, i32, i32, i32, P, P, sz], i32),
             "vx_edt_pass3_device": ([P, P, i32, i32, i32, i32, i32, P, P, sz], i32),
+            "vx_edt_pass12_scatter": ([P, P, i32, i32, i32, i32, i32, P, P, ctypes.c_longlong, P, sz], i32),
             "vx_cycle_create": ([P, i32, i32, i32, f64, P, i32, P, P, P, f64, P, i32, i64, i32, PP], i32),
             "vx_cycle_destroy": ([P], i32),
             "vx_cycle_step": ([P, P, i64, P, f32, f64, P, i32, i32], i32),

@@ -612,6 +612,43 @@ extern "C" int vx_edt_pass12_device(vx_ctx *c, const uint8_t *d_occ, int nx, int
     return VX_OK;
 }
 
+extern "C" int vx_edt_pass12_scatter(vx_ctx *c, const uint8_t *d_occ, int nx, int ny, int nz, int nxl,
+                                     int nranks, void *const *dst, const int *j_starts, long long x_base,
+                                     void *d_scratch, size_t scratch_bytes) {
+    if (!c || !d_occ || !dst || !j_starts || nxl < 0 || nxl > nx || nranks < 1 || nranks > kMaxRanks)
+        return fail(VX_EINVAL, "bad argument");
+    int rc = check_edt_dims(nx, ny, nz);
+    if (rc) return rc;
+    if (j_starts[0] != 0 || j_starts[nranks] != ny) return fail(VX_EINVAL, "j_starts must cover 0..ny");
+    ScatterTab tab{};
+    tab.nranks = nranks;
+    tab.x_base = x_base;
+    for (int q = 0; q < nranks; ++q) {
+        if (j_starts[q + 1] < j_starts[q]) return fail(VX_EINVAL, "j_starts must be non-decreasing");
+        tab.dst[q] = dst[q];
+        tab.j_start[q] = j_starts[q];
+    }
+    tab.j_start[nranks] = ny;
+    EdtPlan p;
+    make_plan(nx, ny, nz, &p, 0);
+    if (p.s2_wide) return fail(VX_EINVAL, "slab exchange needs 32-bit pass-2 codes");
+    const size_t s1b = ((size_t)nxl * ny * nz * 4 + 255) & ~(size_t)255;
+    const size_t need = s1b + p.gstack_bytes;
+    if (!d_scratch) {
+        VX_CUDA(c->scratch.ensure(need));
+        d_scratch = c->scratch.p;
+    } else if (scratch_bytes < need) {
+        return fail(VX_EINVAL, "scratch too small");
+    }
+    int32_t *s1 = (int32_t *)d_scratch;
+    cudaError_t e = launch_pass1(d_occ, s1, nxl, ny, nz, c->stream);
+    if (e == cudaSuccess)
+        e = launch_pass2_scatter(s1, tab, (unsigned char *)d_scratch + s1b, p, nxl, c->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "pass12_scatter");
+    c->launches += 2;
+    return VX_OK;
+}
+
 extern "C" int vx_edt_pass3_device(vx_ctx *c, const void *d_s2, int nx, int ny, int nz, int j0, int nyl,
                                    int32_t *d_site, void *d_scratch, size_t scratch_bytes) {
     if (!c || !d_s2 || !d_site || j0 < 0 || nyl < 0 || j0 + nyl > ny) return fail(VX_EINVAL, "bad argument");

@@ -342,11 +342,50 @@ __device__ __forceinline__ void tma_load_4d(void *dst, const CUtensorMap *map, u
 // shared memory by TMA and the band hulls are built in place (a band's stack
 // never grows past the rows it has consumed); otherwise rows are read with
 // coalesced 128-byte LDGs.
-template <int PASS, bool S2W, bool EW, bool FW, bool STAGED>
+// Where pass-2 rows go.  Default: the s2 array.  SCAT (slab mode): row j of
+// slice i goes straight into the pass-3 input of the rank that owns j --
+// dst[q] + ((x_base + i) * nyl_q + j - j_start[q]) * nz + k -- a peer buffer
+// mapped over NVLink, or this rank's all-to-all send block.
+template <typename OutT, bool SCAT>
+struct RowOut {
+    OutT *p;
+    long long step;
+    int q, qend;
+    __device__ __forceinline__ void begin(OutT *out, long long base, long long stride, int lo,
+                                          const ScatterTab *sc, long long slice, int k, int nz) {
+        if constexpr (!SCAT) {
+            p = out + base + (long long)lo * stride;
+            step = stride;
+        } else {
+            step = nz;
+            q = 0;
+            while (sc->j_start[q + 1] <= lo) ++q;
+            seek(lo, sc, slice, k, nz);
+        }
+    }
+    __device__ __forceinline__ void seek(int y, const ScatterTab *sc, long long slice, int k, int nz) {
+        const int j0 = sc->j_start[q], nyl = sc->j_start[q + 1] - j0;
+        qend = sc->j_start[q + 1];
+        p = reinterpret_cast<OutT *>(sc->dst[q]) + ((sc->x_base + slice) * nyl + (y - j0)) * (long long)nz + k;
+    }
+    __device__ __forceinline__ void put(int y, OutT v, const ScatterTab *sc, long long slice, int k, int nz) {
+        if constexpr (SCAT) {
+            if (y == qend) {
+                ++q;
+                seek(y, sc, slice, k, nz);
+            }
+        }
+        *p = v;
+        p += step;
+    }
+};
+
+template <int PASS, bool S2W, bool EW, bool FW, bool STAGED, bool SCAT = false>
 __device__ __forceinline__ void column_tile(const typename Col<PASS, S2W, EW, FW>::InT *__restrict__ in,
                                             typename Col<PASS, S2W, EW, FW>::OutT *__restrict__ out,
                                             typename Col<PASS, S2W, EW, FW>::EntT *stk, int *meta,
-                                            const ColParams &P, long long tile) {
+                                            const ColParams &P, long long tile,
+                                            const ScatterTab *sc = nullptr) {
     using C = Col<PASS, S2W, EW, FW>;
     using EntT = typename C::EntT;
     using FT = typename C::FT;
@@ -497,9 +536,10 @@ __device__ __forceinline__ void column_tile(const typename Col<PASS, S2W, EW, FW
     // ---- phase D: queries for this band's rows (edt.py:300-317) ----------
     if (colok && lo < hi) {
         const int cnt = ncnt[kk];
-        OutT *dst = out + base + (long long)lo * stride;
+        RowOut<OutT, SCAT> dst;
+        dst.begin(out, base, stride, lo, sc, outer, k, P.nz);
         if (cnt == 0) {  // no candidate in the whole column (edt.py:295-299)
-            for (int y = lo; y < hi; ++y, dst += stride) *dst = C::none();
+            for (int y = lo; y < hi; ++y) dst.put(y, C::none(), sc, outer, k, P.nz);
         } else {
             const int y0 = lo;
             // first hull vertex minimising at y0: binary search over bands ...
@@ -558,7 +598,7 @@ __device__ __forceinline__ void column_tile(const typename Col<PASS, S2W, EW, FW
             FT dN = spos >= 0 ? Fs - Fc : kNever;
             FT t = spos >= 0 ? (FT)2 * (FT)(ys - yc) : (FT)0;
             FT rhs = (FT)lo * t;
-            for (int y = lo; y < hi; ++y, dst += stride, rhs += t) {
+            for (int y = lo; y < hi; ++y, rhs += t) {
                 if (dN < rhs) {
                     InT ccode = scode;
                     do {
@@ -579,31 +619,31 @@ __device__ __forceinline__ void column_tile(const typename Col<PASS, S2W, EW, FW
                     t = spos >= 0 ? (FT)2 * (FT)(ys - yc) : (FT)0;
                     rhs = (FT)y * t;
                 }
-                *dst = ocur;
+                dst.put(y, ocur, sc, outer, k, P.nz);
             }
         }
     }
 }
 
-template <int PASS, bool S2W, bool EW, bool FW>
+template <int PASS, bool S2W, bool EW, bool FW, bool SCAT>
 __global__ void __launch_bounds__(kColThreads, kColMinBlocks) k_column_smem(const typename Col<PASS, S2W, EW, FW>::InT *__restrict__ in,
                                                       typename Col<PASS, S2W, EW, FW>::OutT *__restrict__ out,
-                                                      const ColParams P) {
+                                                      const ColParams P, const __grid_constant__ ScatterTab sc) {
     extern __shared__ __align__(128) unsigned char smem[];
     using EntT = typename Col<PASS, S2W, EW, FW>::EntT;
     EntT *stk = reinterpret_cast<EntT *>(smem);
     int *meta = reinterpret_cast<int *>(smem + (size_t)P.L * 32 * sizeof(EntT));
-    column_tile<PASS, S2W, EW, FW, false>(in, out, stk, meta, P, blockIdx.x);
+    column_tile<PASS, S2W, EW, FW, false, SCAT>(in, out, stk, meta, P, blockIdx.x, &sc);
 }
 
 // TMA-staged variant (narrow 32-bit codes, nz % 4 == 0): one elected thread
 // issues the bulk tensor loads of the whole 32-column tile into the stack
 // region; every row of the column is in flight at once.
-template <int PASS, bool FW>
+template <int PASS, bool FW, bool SCAT>
 __global__ void __launch_bounds__(kColThreads, kColMinBlocks) k_column_tma(const __grid_constant__ CUtensorMap tmap,
                                                      const typename Col<PASS, false, false, FW>::InT *__restrict__ in,
                                                      typename Col<PASS, false, false, FW>::OutT *__restrict__ out,
-                                                     const ColParams P) {
+                                                     const ColParams P, const __grid_constant__ ScatterTab sc) {
     extern __shared__ __align__(128) unsigned char smem[];
     using EntT = typename Col<PASS, false, false, FW>::EntT;
     EntT *stk = reinterpret_cast<EntT *>(smem);
@@ -630,7 +670,7 @@ __global__ void __launch_bounds__(kColThreads, kColMinBlocks) k_column_tma(const
     }
     __syncthreads();
     mbar_wait(bar, 0);
-    column_tile<PASS, false, false, FW, true>(in, out, stk, meta, P, tile);
+    column_tile<PASS, false, false, FW, true, SCAT>(in, out, stk, meta, P, tile, &sc);
 #ifdef VX_PHASE_TIMING
     VX_PT(5);
     __syncthreads();
@@ -640,17 +680,17 @@ __global__ void __launch_bounds__(kColThreads, kColMinBlocks) k_column_tma(const
 
 // Columns too long for shared memory: per-CTA stack slab in global scratch,
 // persistent over tiles.
-template <int PASS, bool S2W, bool EW, bool FW>
+template <int PASS, bool S2W, bool EW, bool FW, bool SCAT>
 __global__ void __launch_bounds__(kColThreads, kColMinBlocks) k_column_gstack(const typename Col<PASS, S2W, EW, FW>::InT *__restrict__ in,
                                                         typename Col<PASS, S2W, EW, FW>::OutT *__restrict__ out,
                                                         typename Col<PASS, S2W, EW, FW>::EntT *gstack,
-                                                        const ColParams P) {
+                                                        const ColParams P, const __grid_constant__ ScatterTab sc) {
     extern __shared__ __align__(128) unsigned char smem[];
     using EntT = typename Col<PASS, S2W, EW, FW>::EntT;
     EntT *stk = gstack + (size_t)blockIdx.x * P.L * 32;
     int *meta = reinterpret_cast<int *>(smem);
     for (long long t = blockIdx.x; t < P.ntiles; t += gridDim.x) {
-        column_tile<PASS, S2W, EW, FW, false>(in, out, stk, meta, P, t);
+        column_tile<PASS, S2W, EW, FW, false, SCAT>(in, out, stk, meta, P, t, &sc);
         __syncthreads();
     }
 }
@@ -737,9 +777,9 @@ bool make_tmap(CUtensorMap *m, const void *in, const EdtPlan &p, int pass, long 
     return r == CUDA_SUCCESS;
 }
 
-template <int PASS, bool S2W, bool EW, bool FW>
+template <int PASS, bool S2W, bool EW, bool FW, bool SCAT>
 cudaError_t launch_col(const void *in, void *out, void *gstack, const EdtPlan &p, long long nouter,
-                       int nyl, int j0, cudaStream_t st) {
+                       int nyl, int j0, const ScatterTab &sc, cudaStream_t st) {
     using C = Col<PASS, S2W, EW, FW>;
     ColParams P = col_params(p, PASS, nouter, nyl, j0);
     if (P.ntiles == 0) return cudaSuccess;
@@ -751,11 +791,11 @@ cudaError_t launch_col(const void *in, void *out, void *gstack, const EdtPlan &p
             CUtensorMap m;
             if (make_tmap(&m, in, p, PASS, nouter, nyl, P.boxh)) {
                 const size_t smem = PASS == 2 ? p.smem2 : p.smem3;
-                auto kern = k_column_tma<PASS, FW>;
+                auto kern = k_column_tma<PASS, FW, SCAT>;
                 cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
                 if (e != cudaSuccess) return e;
                 kern<<<(unsigned)P.ntiles, block, smem, st>>>(m, reinterpret_cast<const typename C::InT *>(in),
-                                                              reinterpret_cast<typename C::OutT *>(out), P);
+                                                              reinterpret_cast<typename C::OutT *>(out), P, sc);
                 return cudaGetLastError();
             }
         }
@@ -763,35 +803,35 @@ cudaError_t launch_col(const void *in, void *out, void *gstack, const EdtPlan &p
     P.rows_alloc = P.L;
     if (!gs) {
         const size_t smem = (size_t)P.L * 32 * sizeof(typename C::EntT) + (size_t)(3 * P.B * 32 + 32) * 4;
-        auto kern = k_column_smem<PASS, S2W, EW, FW>;
+        auto kern = k_column_smem<PASS, S2W, EW, FW, SCAT>;
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         kern<<<(unsigned)P.ntiles, block, smem, st>>>(
-            reinterpret_cast<const typename C::InT *>(in), reinterpret_cast<typename C::OutT *>(out), P);
+            reinterpret_cast<const typename C::InT *>(in), reinterpret_cast<typename C::OutT *>(out), P, sc);
     } else {
         const size_t smem = (size_t)(3 * P.B * 32 + 32) * 4;
-        auto kern = k_column_gstack<PASS, S2W, EW, FW>;
+        auto kern = k_column_gstack<PASS, S2W, EW, FW, SCAT>;
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         const long long g = std::min<long long>(P.ntiles, p.gstack_ctas);
         kern<<<(unsigned)g, block, smem, st>>>(reinterpret_cast<const typename C::InT *>(in),
                                               reinterpret_cast<typename C::OutT *>(out),
-                                              reinterpret_cast<typename C::EntT *>(gstack), P);
+                                              reinterpret_cast<typename C::EntT *>(gstack), P, sc);
     }
     return cudaGetLastError();
 }
 
-template <int PASS>
+template <int PASS, bool SCAT>
 cudaError_t dispatch_col(const void *in, void *out, void *gstack, const EdtPlan &p, long long nouter,
-                         int nyl, int j0, cudaStream_t st) {
+                         int nyl, int j0, const ScatterTab &sc, cudaStream_t st) {
     // narrow: u32 s2, u32 entries, int weights (the 512^3 path)
     if (!p.s2_wide && !p.e3_wide && !p.fwide)
-        return launch_col<PASS, false, false, false>(in, out, gstack, p, nouter, nyl, j0, st);
+        return launch_col<PASS, false, false, false, SCAT>(in, out, gstack, p, nouter, nyl, j0, sc, st);
     if (!p.s2_wide && !p.e3_wide && p.fwide)
-        return launch_col<PASS, false, false, true>(in, out, gstack, p, nouter, nyl, j0, st);
+        return launch_col<PASS, false, false, true, SCAT>(in, out, gstack, p, nouter, nyl, j0, sc, st);
     if (!p.s2_wide && p.e3_wide)
-        return launch_col<PASS, false, true, true>(in, out, gstack, p, nouter, nyl, j0, st);
-    return launch_col<PASS, true, true, true>(in, out, gstack, p, nouter, nyl, j0, st);
+        return launch_col<PASS, false, true, true, SCAT>(in, out, gstack, p, nouter, nyl, j0, sc, st);
+    return launch_col<PASS, true, true, true, SCAT>(in, out, gstack, p, nouter, nyl, j0, sc, st);
 }
 
 }  // namespace
@@ -889,12 +929,17 @@ cudaError_t launch_pass1(const uint8_t *occ, int32_t *s1, long long nslices, int
 
 cudaError_t launch_pass2(const int32_t *s1, void *s2, void *gstack, const EdtPlan &p,
                          long long nslices, cudaStream_t st) {
-    return dispatch_col<2>(s1, s2, gstack, p, nslices, p.ny, 0, st);
+    return dispatch_col<2, false>(s1, s2, gstack, p, nslices, p.ny, 0, ScatterTab{}, st);
+}
+
+cudaError_t launch_pass2_scatter(const int32_t *s1, const ScatterTab &sc, void *gstack, const EdtPlan &p,
+                                 long long nslices, cudaStream_t st) {
+    return dispatch_col<2, true>(s1, nullptr, gstack, p, nslices, p.ny, 0, sc, st);
 }
 
 cudaError_t launch_pass3(const void *s2, int32_t *site, void *gstack, const EdtPlan &p,
                          int nscenes, int j0, int nyl, cudaStream_t st) {
-    return dispatch_col<3>(s2, site, gstack, p, (long long)nscenes * nyl, nyl, j0, st);
+    return dispatch_col<3, false>(s2, site, gstack, p, (long long)nscenes * nyl, nyl, j0, ScatterTab{}, st);
 }
 
 size_t scratch_bytes_for(const EdtPlan &p, int nscenes) {

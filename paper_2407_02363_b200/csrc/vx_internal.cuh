@@ -28,12 +28,24 @@ struct EdtPlan {
 
 bool make_plan(int nx, int ny, int nz, EdtPlan *p, int force_global_stack);
 
+// Slab-mode destination table for the fused pass-2 -> pass-3 exchange.
+constexpr int kMaxRanks = 64;
+struct ScatterTab {
+    void *dst[kMaxRanks];           // per owner rank q: its (x_extent, nyl_q, nz) buffer
+    int j_start[kMaxRanks + 1];     // rank q owns rows j_start[q] .. j_start[q+1]-1
+    long long x_base;               // x index of this launch's first slice in dst
+    int nranks;
+};
+
 // Pass launchers (stream-ordered, no host sync).  Return cudaError_t.
 // nslices: number of (ny, nz) slices stacked along i (scenes * local nx).
 cudaError_t launch_pass1(const uint8_t *occ, int32_t *s1, long long nslices, int ny, int nz,
                          cudaStream_t st);
 cudaError_t launch_pass2(const int32_t *s1, void *s2, void *gstack, const EdtPlan &p,
                          long long nslices, cudaStream_t st);
+// pass 2 with the fused exchange epilogue (slab mode)
+cudaError_t launch_pass2_scatter(const int32_t *s1, const ScatterTab &sc, void *gstack, const EdtPlan &p,
+                                 long long nslices, cudaStream_t st);
 // pass 3 over nscenes buffers of shape (nx, nyl, nz) holding global rows
 // j0 .. j0+nyl-1 (slab mode); site codes are global flat indices.
 cudaError_t launch_pass3(const void *s2, int32_t *site, void *gstack, const EdtPlan &p,

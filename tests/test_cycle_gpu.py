@@ -1,0 +1,84 @@
+"""The device-resident camera tick (MapCycle / vx_cycle_step, engine.py:233-280)
+against the reference's own C1 tick (golden vectors from voxarm) and the
+oracle: stats, env/self/mask cells, both EDT fields and the sphere gather."""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2407_02363_b200 import synth
+from paper_2407_02363_b200.engine import MapCycle
+from tests.golden_util import desk7, digest, golden
+
+pytestmark = pytest.mark.gpu
+
+
+def _c1_cycle():
+    d = desk7()
+    s = synth.C1
+    return MapCycle(s["dims"], s["voxel_size"], s["origin"], d["links"], s["voxel_size"], d["o_links"],
+                    max_points=s["points"], max_spheres=32), d
+
+
+def test_c1_cycle_vs_reference_golden():
+    gold = golden()["c1"]
+    cyc, d = _c1_cycle()
+    s = synth.C1
+    frames = d["frames"][0]
+    centers = np.vstack([synth.sphere_centers(frames, d["sphere_link"], d["sphere_center"]),
+                         synth.extra_query_points(s["dims"], s["voxel_size"], s["origin"])])
+    for f in ("0", "5", "17"):
+        cyc.step(synth.c1_cloud(int(f) / 30.0), frames, centers)
+        res = cyc.wait()
+        assert [res["inserted"], res["robot_skipped"], res["out_of_bounds"]] == gold[f]["stats"]
+        env, selfg, mask = cyc.grids()
+        assert digest(env.cells) == gold[f]["env_cells"]
+        assert digest(mask.cells) == gold["mask_cells"]
+        assert digest(selfg.cells) == gold["self_cells"]
+        fe, fs = cyc.fields()
+        assert digest(fe.site) == gold[f]["env_site"]
+        assert digest(fs.site) == gold["self_site"]
+        lin, world, dist = res["env"]
+        for q, w in enumerate(gold[f]["env_world"]):
+            assert (lin[q] == -1) if w is None else (world[q].tolist() == w)
+        lin, world, dist = res["self"]
+        for q, w in enumerate(gold["self_world"]):
+            assert (lin[q] == -1) if w is None else (world[q].tolist() == w)
+        assert res["self_recomputed"] == (f == "0")   # memo: static torso
+
+
+def test_cycle_moving_arm_vs_oracle():
+    """FK frames change every tick (mask + self recomputed when o_links move)."""
+    cyc, d = _c1_cycle()
+    s = synth.C1
+    dims, vs, origin = s["dims"], s["voxel_size"], s["origin"]
+    for step in range(4):
+        frames = d["frames"][step].copy()
+        if step >= 2:     # move the torso too: the self map must be rebuilt
+            frames[0][:3, 3] += 0.013 * step
+        centers = synth.sphere_centers(frames, d["sphere_link"], d["sphere_center"])
+        pts = synth.c1_cloud(step / 30.0)
+        cyc.step(pts, frames, centers)
+        res = cyc.wait()
+        selfc = np.zeros(dims, np.float32)
+        maskc = np.zeros(dims, np.float32)
+        for li in d["o_links"]:
+            ijk, org = d["links"][li]
+            O.stamp_voxels(selfc, vs, origin, ijk, org, vs, frames[li])
+        for li, (ijk, org) in enumerate(d["links"]):
+            O.stamp_voxels(maskc, vs, origin, ijk, org, vs, frames[li])
+        env = np.zeros(dims, np.float32)
+        st = O.insert_points(env, vs, origin, pts, maskc)
+        assert (res["inserted"], res["robot_skipped"], res["out_of_bounds"]) == st
+        site_e = O.pba_edt_site(env > 0)
+        site_s = O.pba_edt_site(selfc > 0)
+        fe, fs = cyc.fields()
+        assert np.array_equal(fe.site, site_e)
+        assert np.array_equal(fs.site, site_s)
+        for key, site in (("env", site_e), ("self", site_s)):
+            lin, world, dist = res[key]
+            rl, rw, rd = O.site_world(site, vs, origin, centers)
+            assert np.array_equal(lin, rl)
+            ok = rl >= 0
+            assert np.array_equal(world[ok], rw[ok])
+            np.testing.assert_allclose(dist[ok], rd[ok], rtol=1e-6)   # north_star tolerance
+        assert res["self_recomputed"] == (step in (0, 2, 3))
