@@ -159,15 +159,26 @@ def allmax(world, v: float) -> float:
 # ----------------------------------------------------------------------------
 # CPU path: the oracle port of the reference (test infrastructure, timed only)
 # ----------------------------------------------------------------------------
+_CPU_GRIDS = {}
+
+
 def cpu_cycle(pts, frames, centers, d, threads: int):
-    """engine.py:234-280 through the oracle restatement (clear x3, stamp,
-    insert k=0, occupancy, EDT, site world) -> seconds per stage."""
+    """engine.py:234-280 through the oracle restatement, on persistent grids
+    like the engine's: clear x3 (cells.fill(0), engine.py:236-238), stamp the
+    self-obstacle links and all links (243-248), insert the cloud with the
+    robot mask (k=0, 249-254), occupancy, EDT of env (the static self map is
+    memoised as engine.py:259-268 does), site world for the spheres (276-280).
+    Returns seconds per stage."""
     from oracle import oracle as O
+    if not _CPU_GRIDS:
+        _CPU_GRIDS.update(env=np.zeros(DIMS, np.float32), self=np.zeros(DIMS, np.float32),
+                          mask=np.zeros(DIMS, np.float32))
+    env, selfc, mask = _CPU_GRIDS["env"], _CPU_GRIDS["self"], _CPU_GRIDS["mask"]
     t = {}
     t0 = time.perf_counter()
-    env = np.zeros(DIMS, np.float32)
-    selfc = np.zeros(DIMS, np.float32)
-    mask = np.zeros(DIMS, np.float32)
+    env.fill(0.0)
+    selfc.fill(0.0)
+    mask.fill(0.0)
     t["clear"] = time.perf_counter() - t0
     t0 = time.perf_counter()
     for li in d["o_links"]:
@@ -387,9 +398,51 @@ def run_gpu(args, world, rank, local):
         "clocks": clk.summary(),
         "last_stats": {k: res[k] for k in ("inserted", "robot_skipped", "out_of_bounds")} if res else None,
     }
+    if not args.no_sweep:
+        line["edt_sweep"] = edt_sweep(ctx, stream)
     if not args.no_cpu_baseline and world == 1:
         line["cpu_baseline"] = cpu_baseline_sample(d)
     print(json.dumps(line), flush=True)
+
+
+def edt_sweep(ctx, stream):
+    """Config C3 latency sweep: device-timed EDT (K3+K4+K5, inputs resident)
+    of Bernoulli(0.02, seed 0) grids n^3 and of a single centre voxel at 512^3."""
+    import torch
+    from paper_2407_02363_b200 import _lib, synth
+    L = _lib.load()
+    out = {}
+    cases = [(n, "bernoulli_0.02") for n in (64, 96, 128, 192, 256, 384, 512)]
+    cases += [(512, "single_center"), (512, "bernoulli_1e-4")]
+    for n, kind in cases:
+        dims = (n, n, n)
+        if kind == "single_center":
+            occ = synth.structured_occupancy("single_center", dims)
+        elif kind == "bernoulli_1e-4":
+            occ = synth.bernoulli_occupancy(dims, 1e-4, 1)
+        else:
+            occ = synth.bernoulli_occupancy(dims, 0.02, 0)
+        d_occ = torch.from_numpy(occ).cuda()
+        site = torch.empty(dims, dtype=torch.int32, device="cuda")
+        sb = L.vx_edt_scratch_bytes(n, n, n, 1)
+        scratch = torch.empty(sb, dtype=torch.uint8, device="cuda")
+        args = (ctx.handle, ctypes.c_void_p(d_occ.data_ptr()), n, n, n, 1,
+                ctypes.c_void_p(site.data_ptr()), ctypes.c_void_p(scratch.data_ptr()), sb)
+        for _ in range(3):
+            _lib.check(L.vx_edt_device(*args))
+        torch.cuda.synchronize()
+        reps = 10 if n <= 256 else 5
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            _lib.check(L.vx_edt_device(*args))
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        out[f"{n}^3 {kind}"] = {"ms": ms, "gvoxel_s": n ** 3 / ms / 1e6,
+                                "hbm_frac": EDT_BYTES_PER_VOXEL * n ** 3 / ms / 1e6 / peaks()[0]}
+        del d_occ, site, scratch
+    return out
 
 
 def main():
@@ -399,6 +452,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the C3 EDT latency sweep")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     world, rank, local = dist_init()
