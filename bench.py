@@ -400,9 +400,69 @@ def run_gpu(args, world, rank, local):
     }
     if not args.no_sweep:
         line["edt_sweep"] = edt_sweep(ctx, stream)
+        line["small_configs"] = small_configs(d)
     if not args.no_cpu_baseline and world == 1:
         line["cpu_baseline"] = cpu_baseline_sample(d)
     print(json.dumps(line), flush=True)
+
+
+def small_configs(d, steps: int = 20):
+    """Configs C1 (128^3, 50k-pt sphere, 30 spheres) and C2 (256^3, 300k-pt
+    depth camera): device time per camera tick (inputs resident) and end-to-end
+    time through MapCycle.step + wait (host inputs, results read back)."""
+    import torch
+    from paper_2407_02363_b200 import _lib, synth
+    from paper_2407_02363_b200.engine import MapCycle
+    L = _lib.load()
+    out = {}
+    c1 = synth.C1
+    specs = {
+        "C1_128^3": (c1["dims"], c1["voxel_size"], c1["origin"],
+                     lambda s: synth.c1_cloud(s / 30.0)),
+        "C2_256^3": ((256, 256, 256), 0.02, (-2.56, -2.56, -0.24),
+                     lambda s: synth.depth_camera_cloud(s / 30.0)),
+    }
+    for name, (dims, vs, origin, cloud) in specs.items():
+        clouds = [cloud(s) for s in range(4)]
+        cyc = MapCycle(dims, vs, origin, d["links"], vs, d["o_links"],
+                       max_points=max(c.shape[0] for c in clouds), max_spheres=32)
+        ctx = cyc.ctx
+        stream = torch.cuda.ExternalStream(ctx.stream_handle())
+        frames = [d["frames"][s % d["frames"].shape[0]] for s in range(4)]
+        centers = [np.vstack([synth.sphere_centers(f, d["sphere_link"], d["sphere_center"]),
+                              synth.extra_query_points(dims, vs, origin, 9)]) for f in frames]
+        dev = [torch.from_numpy(c).cuda() for c in clouds]
+        T = [np.ascontiguousarray(f.reshape(-1, 16)) for f in frames]
+        for s in range(5):
+            _lib.check(L.vx_cycle_step_device(cyc._h, ctypes.c_void_p(dev[s % 4].data_ptr()),
+                                              dev[s % 4].shape[0], _lib.ptr(T[s % 4]),
+                                              float(np.float32(0.85)), 0.5, _lib.ptr(centers[s % 4]),
+                                              30, 0))
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for s in range(steps):
+            _lib.check(L.vx_cycle_step_device(cyc._h, ctypes.c_void_p(dev[s % 4].data_ptr()),
+                                              dev[s % 4].shape[0], _lib.ptr(T[s % 4]),
+                                              float(np.float32(0.85)), 0.5, _lib.ptr(centers[s % 4]),
+                                              30, 0))
+        e1.record(stream)
+        torch.cuda.synchronize()
+        dev_ms = e0.elapsed_time(e1) / steps
+        pinned = []
+        for c in clouds:
+            pa = _lib.PinnedArray(c.shape, np.float64)
+            pa.array[...] = c
+            pinned.append(pa)
+        t0 = time.perf_counter()
+        for s in range(steps):
+            cyc.step(pinned[s % 4].array, frames[s % 4], centers[s % 4], sync=False)
+            cyc.wait()
+        e2e_ms = (time.perf_counter() - t0) / steps * 1e3
+        out[name] = {"device_ms_per_tick": dev_ms, "e2e_ms_per_tick": e2e_ms,
+                     "points": int(clouds[0].shape[0]), "hz_e2e": 1e3 / e2e_ms}
+        cyc.close()
+    return out
 
 
 def edt_sweep(ctx, stream):
