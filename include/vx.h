@@ -189,6 +189,9 @@ int vx_cycle_wait(vx_cycle *c, vx_cycle_result *res, int32_t *site_lin /* 2*s */
  * 7 sphere gather.  vx_cycle_profile(c, 1) resets and enables; phase_ms
  * returns the mean over the profiled steps (up to 64). */
 #define VX_CYCLE_PHASES 8
+/* Replay the per-tick kernel sequence as one CUDA graph (default on; the
+ * profiled steps always launch directly so the phase events can be recorded). */
+int vx_cycle_use_graph(vx_cycle *c, int enable);
 int vx_cycle_profile(vx_cycle *c, int enable);
 int vx_cycle_phase_ms(vx_cycle *c, double *ms, int *nsteps);
 /* fields of the last step (owned by the cycle; do not destroy) */

@@ -696,6 +696,15 @@ struct vx_cycle {
     bool self_valid = false;
     int last_s = 0;
     int self_recomputed = 0;
+    // CUDA graph of the per-tick sequence (mask/env reset, stamp, scatter,
+    // EDT, gather); the cloud size is read from d_npts on the device
+    bool use_graph = true;
+    long long *d_npts = nullptr, *h_npts = nullptr;  // device / pinned host point count
+    cudaGraphExec_t gexec = nullptr;
+    int g_s = -1;
+    float g_hit = 0.f;
+    double g_thr = 0.0;
+    long long g_kernels = 0;
     // per-phase CUDA-event timing (vx_cycle_profile)
     static constexpr int kRing = 64;
     bool profiling = false;
@@ -778,6 +787,8 @@ extern "C" int vx_cycle_create(vx_ctx *c, int nx, int ny, int nz, double vs, con
     if (e == cudaSuccess) e = cudaMalloc(&cy->d_lin, 2 * S * 4);
     if (e == cudaSuccess) e = cudaMalloc(&cy->d_world, 2 * S * 24);
     if (e == cudaSuccess) e = cudaMalloc(&cy->d_dist, 2 * S * 8);
+    if (e == cudaSuccess) e = cudaMalloc(&cy->d_npts, sizeof(long long));
+    if (e == cudaSuccess) e = cudaHostAlloc(&cy->h_npts, sizeof(long long), cudaHostAllocPortable);
     for (vx_field *f : {&cy->env_f, &cy->self_f}) {
         f->ctx = c;
         f->nx = nx; f->ny = ny; f->nz = nz;
@@ -805,6 +816,9 @@ extern "C" int vx_cycle_destroy(vx_cycle *cy) {
     cudaFree(cy->d_lin);
     cudaFree(cy->d_world);
     cudaFree(cy->d_dist);
+    cudaFree(cy->d_npts);
+    if (cy->h_npts) cudaFreeHost(cy->h_npts);
+    if (cy->gexec) cudaGraphExecDestroy(cy->gexec);
     cudaFree(cy->env_f.site);
     cudaFree(cy->self_f.site);
     cudaFree(cy->scratch);
@@ -832,6 +846,36 @@ static cudaError_t edt_passes(vx_cycle *cy, const uint8_t *occ, int32_t *site, b
     if (marks) cy->mark(7);
     cy->ctx->launches += 3;
     return e;
+}
+
+// engine.py:236-254 and 272-280: mask <- all links; env <- cloud minus mask;
+// EDT of env; the per-sphere gather on both fields.  n_dev (graph mode): the
+// point count is read on the device and npts only sizes the launch.
+static int cycle_main_seq(vx_cycle *cy, const double *d_pts, long long npts, const long long *n_dev,
+                          float hit, double thr, int s, bool marks) {
+    vx_ctx *c = cy->ctx;
+    cudaStream_t st = c->stream;
+    int rc;
+    if ((rc = grid_clear_async(cy->mask))) return rc;
+    if (cy->nlinks && (rc = stamp_sets(cy->mask, cy->nlinks, cy->ijk_all, cy->off_all, cy->org_all, cy->vs_all,
+                                       cy->T_all, kLMax, cy->total_all)))
+        return rc;
+    if ((rc = grid_clear_async(cy->env))) return rc;
+    if (marks) cy->mark(3);
+    if ((npts || n_dev) && (rc = insert_device(cy->env, d_pts, npts, n_dev, hit, thr, cy->mask))) return rc;
+    if (!npts && !n_dev) VX_CUDA(cudaMemsetAsync(cy->env->ctr, 0, 3 * sizeof(unsigned long long), st));
+    if (marks) cy->mark(4);
+    cudaError_t e = edt_passes(cy, cy->env->occ, cy->env_f.site, marks);
+    if (e != cudaSuccess) return cuda_fail(e, "edt(env)");
+    const GridGeom g = cy->env->g;
+    e = launch_site_world(cy->env_f.site, g, cy->d_centers, s, cy->d_lin, cy->d_world, cy->d_dist, st);
+    if (e == cudaSuccess)
+        e = launch_site_world(cy->self_f.site, g, cy->d_centers, s, cy->d_lin + s, cy->d_world + 3 * s,
+                              cy->d_dist + s, st);
+    if (e != cudaSuccess) return cuda_fail(e, "site_world");
+    c->launches += s ? 2 : 0;
+    if (marks) cy->mark(8);
+    return VX_OK;
 }
 
 static int cycle_step(vx_cycle *cy, const double *pts, const double *d_pts_in, int64_t npts,
@@ -873,27 +917,39 @@ static int cycle_step(vx_cycle *cy, const double *pts, const double *d_pts_in, i
         cy->self_recomputed = 1;
     }
     cy->mark(2);
-    // mask <- all links; env <- cloud minus mask  (engine.py:236-254)
-    if ((rc = grid_clear_async(cy->mask))) return rc;
-    if (cy->nlinks && (rc = stamp_sets(cy->mask, cy->nlinks, cy->ijk_all, cy->off_all, cy->org_all, cy->vs_all,
-                                       cy->T_all, kLMax, cy->total_all)))
-        return rc;
-    if ((rc = grid_clear_async(cy->env))) return rc;
-    cy->mark(3);
-    if (npts && (rc = insert_device(cy->env, d_pts, npts, nullptr, hit, thr, cy->mask))) return rc;
-    if (!npts) VX_CUDA(cudaMemsetAsync(cy->env->ctr, 0, 3 * sizeof(unsigned long long), st));
-    cy->mark(4);
-    cudaError_t e = edt_passes(cy, cy->env->occ, cy->env_f.site, true);
-    if (e != cudaSuccess) return cuda_fail(e, "edt(env)");
-    // per-sphere gather on both fields (engine.py:272-280)
-    const GridGeom g = cy->env->g;
-    e = launch_site_world(cy->env_f.site, g, cy->d_centers, s, cy->d_lin, cy->d_world, cy->d_dist, st);
-    if (e == cudaSuccess)
-        e = launch_site_world(cy->self_f.site, g, cy->d_centers, s, cy->d_lin + s, cy->d_world + 3 * s,
-                              cy->d_dist + s, st);
-    if (e != cudaSuccess) return cuda_fail(e, "site_world");
-    c->launches += s ? 2 : 0;
-    cy->mark(8);
+    if (cy->use_graph && !cy->profiling) {
+        // cloud into the fixed buffer the graph reads; its size via d_npts
+        if (npts && d_pts_in)
+            VX_CUDA(cudaMemcpyAsync(cy->d_pts, d_pts_in, (size_t)npts * 24, cudaMemcpyDeviceToDevice, st));
+        *cy->h_npts = npts;
+        VX_CUDA(cudaMemcpyAsync(cy->d_npts, cy->h_npts, sizeof(long long), cudaMemcpyHostToDevice, st));
+        if (!cy->gexec || cy->g_s != s || cy->g_hit != hit || cy->g_thr != thr) {
+            if (cy->gexec) cudaGraphExecDestroy(cy->gexec);
+            cy->gexec = nullptr;
+            const long long l0 = c->launches;
+            VX_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed));
+            rc = cycle_main_seq(cy, cy->d_pts, cy->max_points, cy->d_npts, hit, thr, s, false);
+            cudaGraph_t graph = nullptr;
+            cudaError_t ce = cudaStreamEndCapture(st, &graph);
+            if (rc) {
+                if (graph) cudaGraphDestroy(graph);
+                return rc;
+            }
+            if (ce != cudaSuccess) return cuda_fail(ce, "cudaStreamEndCapture");
+            ce = cudaGraphInstantiate(&cy->gexec, graph, 0);
+            cudaGraphDestroy(graph);
+            if (ce != cudaSuccess) return cuda_fail(ce, "cudaGraphInstantiate");
+            cy->g_kernels = c->launches - l0;
+            c->launches = l0;
+            cy->g_s = s;
+            cy->g_hit = hit;
+            cy->g_thr = thr;
+        }
+        VX_CUDA(cudaGraphLaunch(cy->gexec, st));
+        c->launches += cy->g_kernels;
+    } else {
+        if ((rc = cycle_main_seq(cy, d_pts, npts, nullptr, hit, thr, s, true))) return rc;
+    }
     if (cy->profiling && cy->ring_n < vx_cycle::kRing) cy->ring_n++;
     cy->last_s = s;
     if (sync) VX_CUDA(cudaStreamSynchronize(st));
@@ -908,6 +964,13 @@ extern "C" int vx_cycle_step(vx_cycle *cy, const double *pts, int64_t npts, cons
 extern "C" int vx_cycle_step_device(vx_cycle *cy, const double *d_pts, int64_t npts, const double *link_T,
                                     float hit, double thr, const double *centers, int s, int sync) {
     return cycle_step(cy, nullptr, d_pts, npts, link_T, hit, thr, centers, s, sync);
+}
+
+extern "C" int vx_cycle_use_graph(vx_cycle *cy, int enable) {
+    if (!cy) return fail(VX_EINVAL, "NULL cycle");
+    VX_CUDA(cudaStreamSynchronize(cy->ctx->stream));
+    cy->use_graph = enable != 0;
+    return VX_OK;
 }
 
 extern "C" int vx_cycle_profile(vx_cycle *cy, int enable) {

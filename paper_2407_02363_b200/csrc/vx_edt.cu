@@ -735,6 +735,15 @@ ColParams col_params(const EdtPlan &p, int pass, long long nouter, int nyl, int 
     return P;
 }
 
+// raise the dynamic shared-memory ceiling once per kernel instantiation (the
+// per-launch size is the launch parameter); keeps the launch path cheap
+template <typename K>
+cudaError_t allow_smem(K kern) {
+    static cudaError_t done = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   (int)kSmemLimit);
+    return done;
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
     static bool tried = false;
@@ -792,7 +801,7 @@ cudaError_t launch_col(const void *in, void *out, void *gstack, const EdtPlan &p
             if (make_tmap(&m, in, p, PASS, nouter, nyl, P.boxh)) {
                 const size_t smem = PASS == 2 ? p.smem2 : p.smem3;
                 auto kern = k_column_tma<PASS, FW, SCAT>;
-                cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                cudaError_t e = allow_smem(kern);
                 if (e != cudaSuccess) return e;
                 kern<<<(unsigned)P.ntiles, block, smem, st>>>(m, reinterpret_cast<const typename C::InT *>(in),
                                                               reinterpret_cast<typename C::OutT *>(out), P, sc);
@@ -804,14 +813,14 @@ cudaError_t launch_col(const void *in, void *out, void *gstack, const EdtPlan &p
     if (!gs) {
         const size_t smem = (size_t)P.L * 32 * sizeof(typename C::EntT) + (size_t)(3 * P.B * 32 + 32) * 4;
         auto kern = k_column_smem<PASS, S2W, EW, FW, SCAT>;
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaError_t e = allow_smem(kern);
         if (e != cudaSuccess) return e;
         kern<<<(unsigned)P.ntiles, block, smem, st>>>(
             reinterpret_cast<const typename C::InT *>(in), reinterpret_cast<typename C::OutT *>(out), P, sc);
     } else {
         const size_t smem = (size_t)(3 * P.B * 32 + 32) * 4;
         auto kern = k_column_gstack<PASS, S2W, EW, FW, SCAT>;
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaError_t e = allow_smem(kern);
         if (e != cudaSuccess) return e;
         const long long g = std::min<long long>(P.ntiles, p.gstack_ctas);
         kern<<<(unsigned)g, block, smem, st>>>(reinterpret_cast<const typename C::InT *>(in),

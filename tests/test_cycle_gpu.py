@@ -82,3 +82,27 @@ def test_cycle_moving_arm_vs_oracle():
             assert np.array_equal(world[ok], rw[ok])
             np.testing.assert_allclose(dist[ok], rd[ok], rtol=1e-6)   # north_star tolerance
         assert res["self_recomputed"] == (step in (0, 2, 3))
+
+
+def test_graph_and_direct_launch_agree():
+    """The CUDA-graph replay of the tick equals direct launches, across cloud
+    sizes (the point count is read on the device inside the graph)."""
+    from paper_2407_02363_b200 import _lib
+    d = desk7()
+    s = synth.C1
+    outs = []
+    for graph in (1, 0):
+        cyc, _ = _c1_cycle()
+        _lib.check(_lib.load().vx_cycle_use_graph(cyc._h, graph))
+        res = []
+        for step, npts in enumerate([50_000, 1234, 0, 50_000]):
+            frames = d["frames"][step]
+            centers = synth.sphere_centers(frames, d["sphere_link"], d["sphere_center"])
+            cyc.step(synth.c1_cloud(step / 30.0)[:npts], frames, centers)
+            r = cyc.wait()
+            fe, _ = cyc.fields()
+            res.append((r["inserted"], r["robot_skipped"], r["out_of_bounds"], digest(fe.site),
+                        r["env"][0].tolist(), r["self"][2].tolist()))
+        outs.append(res)
+        cyc.close()
+    assert outs[0] == outs[1]
