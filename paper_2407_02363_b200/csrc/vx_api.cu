@@ -838,11 +838,19 @@ static cudaError_t edt_passes(vx_cycle *cy, const uint8_t *occ, int32_t *site, b
     int32_t *s1 = reinterpret_cast<int32_t *>(base);
     void *s2 = base + s1b, *gs = base + s1b + s2b;
     cudaStream_t st = cy->ctx->stream;
-    cudaError_t e = launch_pass1(occ, s1, p.nx, p.ny, p.nz, st);
+    const bool sparse = sparse_ok(p, 1);
+    SparseRows sp{};
+    cudaError_t e = cudaSuccess;
+    if (sparse) {
+        sp = sparse_rows_at(base + s1b + s2b + p.gstack_bytes, p);
+        e = launch_slice_list(occ, p, sp, st);
+        cy->ctx->launches += 2;
+    }
+    if (e == cudaSuccess) e = launch_pass1(occ, s1, p.nx, p.ny, p.nz, st, sparse ? sp.sflag : nullptr);
     if (marks) cy->mark(5);
-    if (e == cudaSuccess) e = launch_pass2(s1, s2, gs, p, p.nx, st);
+    if (e == cudaSuccess) e = launch_pass2(s1, s2, gs, p, p.nx, st, sparse ? &sp : nullptr);
     if (marks) cy->mark(6);
-    if (e == cudaSuccess) e = launch_pass3(s2, site, gs, p, 1, 0, p.ny, st);
+    if (e == cudaSuccess) e = launch_pass3(s2, site, gs, p, 1, 0, p.ny, st, sparse ? &sp : nullptr);
     if (marks) cy->mark(7);
     cy->ctx->launches += 3;
     return e;

@@ -85,10 +85,12 @@ __device__ __forceinline__ int pick(int k, int l, int r) {
 template <int CMAX>
 __global__ void __launch_bounds__(256) k_pass1_v4(const uint8_t *__restrict__ occ,
                                                   int32_t *__restrict__ s1,
-                                                  long long nlines, int nz) {
+                                                  long long nlines, int nz,
+                                                  const uint8_t *__restrict__ sflag, int ny) {
     const int lane = threadIdx.x & 31;
     const long long line = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (line >= nlines) return;  // warp-uniform
+    if (sflag && !sflag[line / ny]) return;  // empty slice: nothing downstream reads it
     const uint32_t *src = reinterpret_cast<const uint32_t *>(occ + line * nz);
     int4 *dst = reinterpret_cast<int4 *>(s1 + line * nz);
     const int nq = nz >> 2;
@@ -154,10 +156,12 @@ __global__ void __launch_bounds__(256) k_pass1_v4(const uint8_t *__restrict__ oc
 // sweep parks `l` in the output, the backward sweep combines.
 __global__ void __launch_bounds__(256) k_pass1_generic(const uint8_t *__restrict__ occ,
                                                        int32_t *__restrict__ s1,
-                                                       long long nlines, int nz) {
+                                                       long long nlines, int nz,
+                                                       const uint8_t *__restrict__ sflag, int ny) {
     const int lane = threadIdx.x & 31;
     const long long line = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (line >= nlines) return;
+    if (sflag && !sflag[line / ny]) return;
     const uint8_t *src = occ + line * nz;
     int32_t *dst = s1 + line * nz;
     int carry = -1;
@@ -200,6 +204,11 @@ struct ColParams {
     int boxh, rows_alloc;  // TMA staging: rows per box, rows of smem (>= L)
     int wb;                // pass 3 narrow entry: (x << wb) | w, w = dy^2 + dz^2
     uint32_t wmask;
+    // occupied-slice list (single-scene EDT): pass 2 skips empty slices,
+    // pass 3 stages and scans only the rows of occupied slices
+    const uint8_t *sflag;  // per slice: any occupied voxel (nullptr = dense)
+    const int *xs;         // occupied slice indices, ascending
+    const int *hdr;        // hdr[0] = number of occupied slices (device-side)
 };
 
 template <int PASS, bool S2W, bool EW, bool FW>
@@ -380,7 +389,7 @@ struct RowOut {
     }
 };
 
-template <int PASS, bool S2W, bool EW, bool FW, bool STAGED, bool SCAT = false>
+template <int PASS, bool S2W, bool EW, bool FW, bool STAGED, bool SCAT = false, bool CMP = false>
 __device__ __forceinline__ void column_tile(const typename Col<PASS, S2W, EW, FW>::InT *__restrict__ in,
                                             typename Col<PASS, S2W, EW, FW>::OutT *__restrict__ out,
                                             typename Col<PASS, S2W, EW, FW>::EntT *stk, int *meta,
@@ -419,6 +428,15 @@ __device__ __forceinline__ void column_tile(const typename Col<PASS, S2W, EW, FW
 
     VX_PT(1);
     // ---- phase A: band-local hull (edt.py:253-276 for one band) ----------
+    // slots [alo, ahi) of the staged tile; CMP: the tile holds only the rows
+    // of occupied slices (slot t = row xs[t]), split evenly over the bands
+    int alo = lo, ahi = hi;
+    if constexpr (CMP) {
+        const int m = __ldg(P.hdr);
+        const int wc = (m + P.B - 1) / P.B;
+        alo = min(m, b * wc);
+        ahi = min(m, alo + wc);
+    }
     int n = 0;
     if (colok) {
         int ya = 0, yb = 0;
@@ -432,20 +450,24 @@ __device__ __forceinline__ void column_tile(const typename Col<PASS, S2W, EW, FW
                 yb = ya;
                 Fb = Fa;
                 if (n >= 2) {
-                    const EntT t = stk[(size_t)(lo + n - 2) * 32 + kk];
+                    const EntT t = stk[(size_t)(alo + n - 2) * 32 + kk];
                     ya = C::row(P, t);
                     Fa = C::F(P, t, jq, k);
                 }
             }
-            stk[(size_t)(lo + n) * 32 + kk] = ec;
+            stk[(size_t)(alo + n) * 32 + kk] = ec;
             ya = yb; Fa = Fb;
             yb = yc; Fb = Fc;
             ++n;
         };
         if constexpr (STAGED) {
             const InT *tin = reinterpret_cast<const InT *>(stk);
+            if constexpr (CMP) {
+                for (int t = alo; t < ahi; ++t) consume(tin[(size_t)t * 32 + kk], __ldg(P.xs + t));
+            } else {
 #pragma unroll 4
-            for (int y = lo; y < hi; ++y) consume(tin[(size_t)y * 32 + kk], y);
+                for (int y = lo; y < hi; ++y) consume(tin[(size_t)y * 32 + kk], y);
+            }
         } else {
             const InT *src = in + base + (long long)lo * stride;
             for (int y0 = lo; y0 < hi; y0 += 8) {
@@ -460,8 +482,8 @@ __device__ __forceinline__ void column_tile(const typename Col<PASS, S2W, EW, FW
             }
         }
     }
-    bs[b * 32 + kk] = lo;
-    be[b * 32 + kk] = lo + n;
+    bs[b * 32 + kk] = alo;
+    be[b * 32 + kk] = alo + n;
     __syncthreads();
     VX_PT(2);
 
@@ -639,7 +661,7 @@ __global__ void __launch_bounds__(kColThreads, kColMinBlocks) k_column_smem(cons
 // TMA-staged variant (narrow 32-bit codes, nz % 4 == 0): one elected thread
 // issues the bulk tensor loads of the whole 32-column tile into the stack
 // region; every row of the column is in flight at once.
-template <int PASS, bool FW, bool SCAT>
+template <int PASS, bool FW, bool SCAT, bool CMP>
 __global__ void __launch_bounds__(kColThreads, kColMinBlocks) k_column_tma(const __grid_constant__ CUtensorMap tmap,
                                                      const typename Col<PASS, false, false, FW>::InT *__restrict__ in,
                                                      typename Col<PASS, false, false, FW>::OutT *__restrict__ out,
@@ -650,27 +672,47 @@ __global__ void __launch_bounds__(kColThreads, kColMinBlocks) k_column_tma(const
     int *meta = reinterpret_cast<int *>(smem + (size_t)P.rows_alloc * 32 * sizeof(EntT));
     uint64_t *bar = reinterpret_cast<uint64_t *>(meta + 3 * P.B * 32 + 32);
     const long long tile = blockIdx.x;
+    const int kt = (int)(tile % P.nkt);
+    const long long outer = tile / P.nkt;
+    if constexpr (PASS == 2) {
+        if (P.sflag && !P.sflag[outer]) return;   // empty slice: pass 3 never reads it
+    }
     VX_PT(0);
-    if (threadIdx.x == 0 && threadIdx.y == 0) {
-        mbar_init(bar, 1);
-        const int kt = (int)(tile % P.nkt);
-        const long long outer = tile / P.nkt;
-        const int nbox = P.rows_alloc / P.boxh;
-        mbar_expect_tx(bar, (uint32_t)(P.rows_alloc * 32 * sizeof(EntT)));
-        for (int q = 0; q < nbox; ++q) {
-            void *dst = stk + (size_t)q * P.boxh * 32;
-            if constexpr (PASS == 2) {
-                tma_load_3d(dst, &tmap, bar, kt * 32, q * P.boxh, (int)outer);
-            } else {
-                const int scene = (int)(outer / P.nyl);
-                const int jl = (int)(outer - (long long)scene * P.nyl);
-                tma_load_4d(dst, &tmap, bar, kt * 32, jl, q * P.boxh, scene);
+    if constexpr (CMP) {
+        // rows of occupied slices only: one 32-column x 1-row box per row,
+        // issued by the lanes of warp 0 into consecutive slots
+        if (threadIdx.y == 0) {
+            const int m = __ldg(P.hdr);
+            const int scene = (int)(outer / P.nyl);
+            const int jl = (int)(outer - (long long)scene * P.nyl);
+            if (threadIdx.x == 0) {
+                mbar_init(bar, 1);
+                mbar_expect_tx(bar, (uint32_t)m * 32u * (uint32_t)sizeof(EntT));
+            }
+            __syncwarp();
+            for (int t = threadIdx.x; t < m; t += 32)
+                tma_load_4d(stk + (size_t)t * 32, &tmap, bar, kt * 32, jl, __ldg(P.xs + t), scene);
+        }
+    } else {
+        if (threadIdx.x == 0 && threadIdx.y == 0) {
+            mbar_init(bar, 1);
+            const int nbox = P.rows_alloc / P.boxh;
+            mbar_expect_tx(bar, (uint32_t)(P.rows_alloc * 32 * sizeof(EntT)));
+            for (int q = 0; q < nbox; ++q) {
+                void *dst = stk + (size_t)q * P.boxh * 32;
+                if constexpr (PASS == 2) {
+                    tma_load_3d(dst, &tmap, bar, kt * 32, q * P.boxh, (int)outer);
+                } else {
+                    const int scene = (int)(outer / P.nyl);
+                    const int jl = (int)(outer - (long long)scene * P.nyl);
+                    tma_load_4d(dst, &tmap, bar, kt * 32, jl, q * P.boxh, scene);
+                }
             }
         }
     }
     __syncthreads();
     mbar_wait(bar, 0);
-    column_tile<PASS, false, false, FW, true, SCAT>(in, out, stk, meta, P, tile, &sc);
+    column_tile<PASS, false, false, FW, true, SCAT, CMP>(in, out, stk, meta, P, tile, &sc);
 #ifdef VX_PHASE_TIMING
     VX_PT(5);
     __syncthreads();
@@ -730,6 +772,9 @@ ColParams col_params(const EdtPlan &p, int pass, long long nouter, int nyl, int 
     P.nvox = P.splane * p.nx;
     P.wb = p.wb;
     P.wmask = p.wb >= 32 ? 0xffffffffu : ((1u << p.wb) - 1u);
+    P.sflag = nullptr;
+    P.xs = nullptr;
+    P.hdr = nullptr;
     P.boxh = std::min(P.L, 256);
     P.rows_alloc = (P.L + P.boxh - 1) / P.boxh * P.boxh;
     return P;
@@ -788,9 +833,13 @@ bool make_tmap(CUtensorMap *m, const void *in, const EdtPlan &p, int pass, long 
 
 template <int PASS, bool S2W, bool EW, bool FW, bool SCAT>
 cudaError_t launch_col(const void *in, void *out, void *gstack, const EdtPlan &p, long long nouter,
-                       int nyl, int j0, const ScatterTab &sc, cudaStream_t st) {
+                       int nyl, int j0, const ScatterTab &sc, cudaStream_t st, const SparseRows *sp) {
     using C = Col<PASS, S2W, EW, FW>;
     ColParams P = col_params(p, PASS, nouter, nyl, j0);
+    if (sp) {   // the caller only passes one when both column passes are TMA-staged
+        if (PASS == 2) P.sflag = sp->sflag;
+        else { P.xs = sp->xs; P.hdr = sp->hdr; }
+    }
     if (P.ntiles == 0) return cudaSuccess;
     const dim3 block(32, P.B);
     const bool gs = PASS == 2 ? p.gstack2 : p.gstack3;
@@ -798,9 +847,10 @@ cudaError_t launch_col(const void *in, void *out, void *gstack, const EdtPlan &p
     if constexpr (!S2W && !EW) {
         if (staged && !gs) {
             CUtensorMap m;
-            if (make_tmap(&m, in, p, PASS, nouter, nyl, P.boxh)) {
+            const bool cmp = PASS == 3 && P.xs != nullptr;
+            if (make_tmap(&m, in, p, PASS, nouter, nyl, cmp ? 1 : P.boxh)) {
                 const size_t smem = PASS == 2 ? p.smem2 : p.smem3;
-                auto kern = k_column_tma<PASS, FW, SCAT>;
+                auto kern = cmp ? k_column_tma<PASS, FW, SCAT, true> : k_column_tma<PASS, FW, SCAT, false>;
                 cudaError_t e = allow_smem(kern);
                 if (e != cudaSuccess) return e;
                 kern<<<(unsigned)P.ntiles, block, smem, st>>>(m, reinterpret_cast<const typename C::InT *>(in),
@@ -809,6 +859,7 @@ cudaError_t launch_col(const void *in, void *out, void *gstack, const EdtPlan &p
             }
         }
     }
+    if (P.xs) return cudaErrorNotSupported;   // compact rows need the TMA-staged kernel
     P.rows_alloc = P.L;
     if (!gs) {
         const size_t smem = (size_t)P.L * 32 * sizeof(typename C::EntT) + (size_t)(3 * P.B * 32 + 32) * 4;
@@ -832,15 +883,16 @@ cudaError_t launch_col(const void *in, void *out, void *gstack, const EdtPlan &p
 
 template <int PASS, bool SCAT>
 cudaError_t dispatch_col(const void *in, void *out, void *gstack, const EdtPlan &p, long long nouter,
-                         int nyl, int j0, const ScatterTab &sc, cudaStream_t st) {
+                         int nyl, int j0, const ScatterTab &sc, cudaStream_t st,
+                         const SparseRows *sp = nullptr) {
     // narrow: u32 s2, u32 entries, int weights (the 512^3 path)
     if (!p.s2_wide && !p.e3_wide && !p.fwide)
-        return launch_col<PASS, false, false, false, SCAT>(in, out, gstack, p, nouter, nyl, j0, sc, st);
+        return launch_col<PASS, false, false, false, SCAT>(in, out, gstack, p, nouter, nyl, j0, sc, st, sp);
     if (!p.s2_wide && !p.e3_wide && p.fwide)
-        return launch_col<PASS, false, false, true, SCAT>(in, out, gstack, p, nouter, nyl, j0, sc, st);
+        return launch_col<PASS, false, false, true, SCAT>(in, out, gstack, p, nouter, nyl, j0, sc, st, sp);
     if (!p.s2_wide && p.e3_wide)
-        return launch_col<PASS, false, true, true, SCAT>(in, out, gstack, p, nouter, nyl, j0, sc, st);
-    return launch_col<PASS, true, true, true, SCAT>(in, out, gstack, p, nouter, nyl, j0, sc, st);
+        return launch_col<PASS, false, true, true, SCAT>(in, out, gstack, p, nouter, nyl, j0, sc, st, sp);
+    return launch_col<PASS, true, true, true, SCAT>(in, out, gstack, p, nouter, nyl, j0, sc, st, sp);
 }
 
 }  // namespace
@@ -922,23 +974,23 @@ bool make_plan(int nx, int ny, int nz, EdtPlan *p, int force_global_stack) {
 
 
 cudaError_t launch_pass1(const uint8_t *occ, int32_t *s1, long long nslices, int ny, int nz,
-                         cudaStream_t st) {
+                         cudaStream_t st, const uint8_t *sflag) {
     const long long nlines = nslices * ny;
     if (nlines == 0) return cudaSuccess;
     const unsigned grid = (unsigned)((nlines + 7) / 8);
     const bool vec = (nz % 4 == 0) && ((uintptr_t)occ % 16 == 0) && ((uintptr_t)s1 % 16 == 0);
-    if (vec && nz <= 128) k_pass1_v4<1><<<grid, 256, 0, st>>>(occ, s1, nlines, nz);
-    else if (vec && nz <= 256) k_pass1_v4<2><<<grid, 256, 0, st>>>(occ, s1, nlines, nz);
-    else if (vec && nz <= 512) k_pass1_v4<4><<<grid, 256, 0, st>>>(occ, s1, nlines, nz);
-    else if (vec && nz <= 1024) k_pass1_v4<8><<<grid, 256, 0, st>>>(occ, s1, nlines, nz);
-    else if (vec && nz <= 2048) k_pass1_v4<16><<<grid, 256, 0, st>>>(occ, s1, nlines, nz);
-    else k_pass1_generic<<<grid, 256, 0, st>>>(occ, s1, nlines, nz);
+    if (vec && nz <= 128) k_pass1_v4<1><<<grid, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny);
+    else if (vec && nz <= 256) k_pass1_v4<2><<<grid, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny);
+    else if (vec && nz <= 512) k_pass1_v4<4><<<grid, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny);
+    else if (vec && nz <= 1024) k_pass1_v4<8><<<grid, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny);
+    else if (vec && nz <= 2048) k_pass1_v4<16><<<grid, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny);
+    else k_pass1_generic<<<grid, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny);
     return cudaGetLastError();
 }
 
 cudaError_t launch_pass2(const int32_t *s1, void *s2, void *gstack, const EdtPlan &p,
-                         long long nslices, cudaStream_t st) {
-    return dispatch_col<2, false>(s1, s2, gstack, p, nslices, p.ny, 0, ScatterTab{}, st);
+                         long long nslices, cudaStream_t st, const SparseRows *sp) {
+    return dispatch_col<2, false>(s1, s2, gstack, p, nslices, p.ny, 0, ScatterTab{}, st, sp);
 }
 
 cudaError_t launch_pass2_scatter(const int32_t *s1, const ScatterTab &sc, void *gstack, const EdtPlan &p,
@@ -947,20 +999,92 @@ cudaError_t launch_pass2_scatter(const int32_t *s1, const ScatterTab &sc, void *
 }
 
 cudaError_t launch_pass3(const void *s2, int32_t *site, void *gstack, const EdtPlan &p,
-                         int nscenes, int j0, int nyl, cudaStream_t st) {
-    return dispatch_col<3, false>(s2, site, gstack, p, (long long)nscenes * nyl, nyl, j0, ScatterTab{}, st);
+                         int nscenes, int j0, int nyl, cudaStream_t st, const SparseRows *sp) {
+    return dispatch_col<3, false>(s2, site, gstack, p, (long long)nscenes * nyl, nyl, j0, ScatterTab{}, st, sp);
+}
+
+// ---- occupied-slice list ------------------------------------------------------
+// per slice: does it hold any occupied voxel?
+__global__ void __launch_bounds__(256) k_slice_flags(const uint8_t *__restrict__ occ, long long plane,
+                                                     uint8_t *__restrict__ sflag) {
+    const uint8_t *src = occ + (long long)blockIdx.x * plane;
+    bool any = false;
+    if ((plane & 15) == 0 && ((uintptr_t)occ & 15) == 0) {
+        const uint4 *v = reinterpret_cast<const uint4 *>(src);
+        for (long long q = threadIdx.x; q < (plane >> 4) && !any; q += blockDim.x) {
+            const uint4 w = __ldg(v + q);
+            any = (w.x | w.y | w.z | w.w) != 0u;
+        }
+    } else {
+        for (long long q = threadIdx.x; q < plane && !any; q += blockDim.x) any = src[q] != 0;
+    }
+    any = __syncthreads_or(any);
+    if (threadIdx.x == 0) sflag[blockIdx.x] = any ? 1 : 0;
+}
+
+// ascending list of occupied slices (one CTA, block-wide prefix sums)
+__global__ void __launch_bounds__(1024) k_slice_list(const uint8_t *__restrict__ sflag, int nslices,
+                                                     int *__restrict__ xs, int *__restrict__ hdr) {
+    __shared__ int wsum[32];
+    __shared__ int base_s;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) base_s = 0;
+    __syncthreads();
+    for (int c0 = 0; c0 < nslices; c0 += blockDim.x) {
+        const int x = c0 + threadIdx.x;
+        const int f = (x < nslices && sflag[x]) ? 1 : 0;
+        const unsigned m = __ballot_sync(VX_FULL_MASK, f);
+        const int wpre = __popc(m & ((1u << lane) - 1u));
+        if (lane == 0) wsum[warp] = __popc(m);
+        __syncthreads();
+        int wbase = 0, tot = 0;
+        for (int q = 0; q < (int)(blockDim.x >> 5); ++q) {
+            if (q < warp) wbase += wsum[q];
+            tot += wsum[q];
+        }
+        const int base = base_s;
+        if (f) xs[base + wbase + wpre] = x;
+        __syncthreads();
+        if (threadIdx.x == 0) base_s = base + tot;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) hdr[0] = base_s;
+}
+
+cudaError_t launch_slice_list(const uint8_t *occ, const EdtPlan &p, const SparseRows &sp, cudaStream_t st) {
+    k_slice_flags<<<(unsigned)p.nx, 256, 0, st>>>(occ, (long long)p.ny * p.nz, const_cast<uint8_t *>(sp.sflag));
+    k_slice_list<<<1, 1024, 0, st>>>(sp.sflag, p.nx, const_cast<int *>(sp.xs), const_cast<int *>(sp.hdr));
+    return cudaGetLastError();
+}
+
+size_t sparse_bytes(const EdtPlan &p) {
+    return ((size_t)p.nx + 255) / 256 * 256 + ((size_t)p.nx * 4 + 255) / 256 * 256 + 256;
 }
 
 size_t scratch_bytes_for(const EdtPlan &p, int nscenes) {
     const size_t n = (size_t)p.nx * p.ny * p.nz * nscenes;
     const size_t s1b = (n * 4 + 255) & ~(size_t)255;
     const size_t s2b = (n * (p.s2_wide ? 8 : 4) + 255) & ~(size_t)255;
-    return s1b + s2b + p.gstack_bytes;
+    return s1b + s2b + p.gstack_bytes + sparse_bytes(p);
+}
+
+bool sparse_ok(const EdtPlan &p, int nscenes) {
+    const char *ns = getenv("VX_NO_SPARSE");
+    return nscenes == 1 && p.tma2 && p.tma3 && !(ns && atoi(ns));
+}
+
+SparseRows sparse_rows_at(void *where, const EdtPlan &p) {
+    unsigned char *b = static_cast<unsigned char *>(where);
+    SparseRows sp;
+    sp.sflag = b;
+    sp.xs = reinterpret_cast<int *>(b + ((size_t)p.nx + 255) / 256 * 256);
+    sp.hdr = reinterpret_cast<int *>(b + ((size_t)p.nx + 255) / 256 * 256 + ((size_t)p.nx * 4 + 255) / 256 * 256);
+    return sp;
 }
 
 cudaError_t edt_device_batched(const uint8_t *occ, int32_t *site, void *scratch,
                                const EdtPlan &p, int nscenes, cudaStream_t st) {
-    // scratch = [s1 i32 N*nscenes][s2 N*nscenes][global stacks]
+    // scratch = [s1 i32 N*nscenes][s2 N*nscenes][global stacks][slice list]
     unsigned char *base = static_cast<unsigned char *>(scratch);
     const size_t n = (size_t)p.nx * p.ny * p.nz * nscenes;
     int32_t *s1 = reinterpret_cast<int32_t *>(base);
@@ -968,7 +1092,16 @@ cudaError_t edt_device_batched(const uint8_t *occ, int32_t *site, void *scratch,
     void *s2 = base + s1b;
     const size_t s2b = (n * (p.s2_wide ? 8 : 4) + 255) & ~(size_t)255;
     void *gs = base + s1b + s2b;
-    cudaError_t e = launch_pass1(occ, s1, (long long)p.nx * nscenes, p.ny, p.nz, st);
+    cudaError_t e;
+    if (sparse_ok(p, nscenes)) {
+        const SparseRows sp = sparse_rows_at(base + s1b + s2b + p.gstack_bytes, p);
+        e = launch_slice_list(occ, p, sp, st);
+        if (e == cudaSuccess) e = launch_pass1(occ, s1, p.nx, p.ny, p.nz, st, sp.sflag);
+        if (e == cudaSuccess) e = launch_pass2(s1, s2, gs, p, p.nx, st, &sp);
+        if (e == cudaSuccess) e = launch_pass3(s2, site, gs, p, 1, 0, p.ny, st, &sp);
+        return e;
+    }
+    e = launch_pass1(occ, s1, (long long)p.nx * nscenes, p.ny, p.nz, st);
     if (e != cudaSuccess) return e;
     e = launch_pass2(s1, s2, gs, p, (long long)p.nx * nscenes, st);
     if (e != cudaSuccess) return e;

@@ -37,19 +37,31 @@ struct ScatterTab {
     int nranks;
 };
 
+// Occupied-slice list of a single-scene EDT (all device-side): pass 1 and
+// pass 2 skip empty slices, pass 3 stages only occupied slices' rows.
+struct SparseRows {
+    const uint8_t *sflag;   // [nx] 1 if slice i holds an occupied voxel
+    const int *xs;          // [nx] ascending occupied slice indices
+    const int *hdr;         // hdr[0] = count
+};
+
 // Pass launchers (stream-ordered, no host sync).  Return cudaError_t.
 // nslices: number of (ny, nz) slices stacked along i (scenes * local nx).
 cudaError_t launch_pass1(const uint8_t *occ, int32_t *s1, long long nslices, int ny, int nz,
-                         cudaStream_t st);
+                         cudaStream_t st, const uint8_t *sflag = nullptr);
 cudaError_t launch_pass2(const int32_t *s1, void *s2, void *gstack, const EdtPlan &p,
-                         long long nslices, cudaStream_t st);
+                         long long nslices, cudaStream_t st, const SparseRows *sp = nullptr);
 // pass 2 with the fused exchange epilogue (slab mode)
 cudaError_t launch_pass2_scatter(const int32_t *s1, const ScatterTab &sc, void *gstack, const EdtPlan &p,
                                  long long nslices, cudaStream_t st);
 // pass 3 over nscenes buffers of shape (nx, nyl, nz) holding global rows
 // j0 .. j0+nyl-1 (slab mode); site codes are global flat indices.
 cudaError_t launch_pass3(const void *s2, int32_t *site, void *gstack, const EdtPlan &p,
-                         int nscenes, int j0, int nyl, cudaStream_t st);
+                         int nscenes, int j0, int nyl, cudaStream_t st, const SparseRows *sp = nullptr);
+// occupied-slice list: flags + compacted list (2 launches)
+bool sparse_ok(const EdtPlan &p, int nscenes);
+SparseRows sparse_rows_at(void *where, const EdtPlan &p);
+cudaError_t launch_slice_list(const uint8_t *occ, const EdtPlan &p, const SparseRows &sp, cudaStream_t st);
 size_t scratch_bytes_for(const EdtPlan &p, int nscenes);
 // Full EDT: occ (device) -> site (device); scratch >= scratch_bytes_for(p, n).
 cudaError_t edt_device(const uint8_t *occ, int32_t *site, void *scratch, const EdtPlan &p,

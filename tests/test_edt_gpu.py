@@ -87,11 +87,14 @@ _SUB = r"""
 import sys, numpy as np
 sys.path.insert(0, {root!r})
 from oracle import oracle as O
-from paper_2407_02363_b200 import pba_edt
+from paper_2407_02363_b200 import pba_edt, synth
 rng = np.random.default_rng(9)
 for _ in range(40):
     dims = tuple(int(d) for d in rng.integers(1, 40, size=3))
     occ = rng.random(dims) < float(rng.choice([0.002, 0.05, 0.4]))
+    assert np.array_equal(pba_edt(occ).site, O.pba_edt_site(occ)), dims
+for dims, p in [((128, 64, 96), 1e-4), ((96, 80, 64), 0.01)]:
+    occ = synth.bernoulli_occupancy(dims, p, 4)
     assert np.array_equal(pba_edt(occ).site, O.pba_edt_site(occ)), dims
 print("ok")
 """
@@ -100,7 +103,7 @@ print("ok")
 @pytest.mark.parametrize("env", [{"VX_FORCE_WIDE": "1"}, {"VX_FORCE_WIDE": "2"},
                                  {"VX_FORCE_WIDE": "3"}, {"VX_FORCE_GSTACK": "1"},
                                  {"VX_FORCE_WIDE": "3", "VX_FORCE_GSTACK": "1"},
-                                 {"VX_NO_TMA": "1"}],
+                                 {"VX_NO_TMA": "1"}, {"VX_NO_SPARSE": "1"}],
                          ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
 def test_wide_and_gstack_variants(env):
     """Every template variant (int64 weights, u64 entries / codes, global
@@ -108,6 +111,28 @@ def test_wide_and_gstack_variants(env):
     r = subprocess.run([sys.executable, "-c", _SUB.format(root=ROOT)], env={**os.environ, **env},
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+def test_sparse_slices():
+    """Occupied-slice list path: empty slices at the ends, in the middle, in
+    runs, a single occupied slice, all occupied."""
+    rng = np.random.default_rng(21)
+    for dims in [(96, 64, 64), (200, 40, 36), (33, 128, 32)]:
+        for pattern in ("ends", "middle", "runs", "one", "all"):
+            occ = (rng.random(dims) < 0.01).astype(np.uint8)
+            nx = dims[0]
+            if pattern == "ends":
+                occ[: nx // 3] = 0
+                occ[-nx // 4:] = 0
+            elif pattern == "middle":
+                occ[nx // 3: 2 * nx // 3] = 0
+            elif pattern == "runs":
+                for i0 in range(0, nx, 7):
+                    occ[i0: i0 + 3] = 0
+            elif pattern == "one":
+                occ[:] = 0
+                occ[nx // 2, 3, 5] = 1
+            assert np.array_equal(pba_edt(occ).site, O.pba_edt_site(occ)), (dims, pattern)
 
 
 def test_density_sweep_256():
