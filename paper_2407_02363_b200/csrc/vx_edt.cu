@@ -663,6 +663,7 @@ __global__ void __launch_bounds__(kColThreads, kColMinBlocks) k_column_smem(cons
 // region; every row of the column is in flight at once.
 template <int PASS, bool FW, bool SCAT, bool CMP>
 __global__ void __launch_bounds__(kColThreads, kColMinBlocks) k_column_tma(const __grid_constant__ CUtensorMap tmap,
+                                                     const __grid_constant__ CUtensorMap tmap1,
                                                      const typename Col<PASS, false, false, FW>::InT *__restrict__ in,
                                                      typename Col<PASS, false, false, FW>::OutT *__restrict__ out,
                                                      const ColParams P, const __grid_constant__ ScatterTab sc) {
@@ -678,22 +679,27 @@ __global__ void __launch_bounds__(kColThreads, kColMinBlocks) k_column_tma(const
         if (P.sflag && !P.sflag[outer]) return;   // empty slice: pass 3 never reads it
     }
     VX_PT(0);
+    bool all_rows = true;
     if constexpr (CMP) {
-        // rows of occupied slices only: one 32-column x 1-row box per row,
-        // issued by the lanes of warp 0 into consecutive slots
-        if (threadIdx.y == 0) {
-            const int m = __ldg(P.hdr);
+        // rows of occupied slices only (slot t <- row xs[t]); when every slice
+        // is occupied the plain box loads below are used instead
+        const int m = __ldg(P.hdr);
+        all_rows = m == P.L;
+        if (!all_rows) {
             const int scene = (int)(outer / P.nyl);
             const int jl = (int)(outer - (long long)scene * P.nyl);
-            if (threadIdx.x == 0) {
+            if (threadIdx.x == 0 && threadIdx.y == 0) {
                 mbar_init(bar, 1);
                 mbar_expect_tx(bar, (uint32_t)m * 32u * (uint32_t)sizeof(EntT));
             }
-            __syncwarp();
-            for (int t = threadIdx.x; t < m; t += 32)
-                tma_load_4d(stk + (size_t)t * 32, &tmap, bar, kt * 32, jl, __ldg(P.xs + t), scene);
+            __syncthreads();
+            // one 32-column x 1-row box per occupied row, issued by all threads
+            const int tid = threadIdx.y * 32 + threadIdx.x, nth = blockDim.x * blockDim.y;
+            for (int t = tid; t < m; t += nth)
+                tma_load_4d(stk + (size_t)t * 32, &tmap1, bar, kt * 32, jl, __ldg(P.xs + t), scene);
         }
-    } else {
+    }
+    if (all_rows) {
         if (threadIdx.x == 0 && threadIdx.y == 0) {
             mbar_init(bar, 1);
             const int nbox = P.rows_alloc / P.boxh;
@@ -846,14 +852,16 @@ cudaError_t launch_col(const void *in, void *out, void *gstack, const EdtPlan &p
     const bool staged = PASS == 2 ? p.tma2 : p.tma3;
     if constexpr (!S2W && !EW) {
         if (staged && !gs) {
-            CUtensorMap m;
+            CUtensorMap m, m1;
             const bool cmp = PASS == 3 && P.xs != nullptr;
-            if (make_tmap(&m, in, p, PASS, nouter, nyl, cmp ? 1 : P.boxh)) {
+            if (make_tmap(&m, in, p, PASS, nouter, nyl, P.boxh) &&
+                (!cmp || make_tmap(&m1, in, p, PASS, nouter, nyl, 1))) {
+                if (!cmp) m1 = m;
                 const size_t smem = PASS == 2 ? p.smem2 : p.smem3;
                 auto kern = cmp ? k_column_tma<PASS, FW, SCAT, true> : k_column_tma<PASS, FW, SCAT, false>;
                 cudaError_t e = allow_smem(kern);
                 if (e != cudaSuccess) return e;
-                kern<<<(unsigned)P.ntiles, block, smem, st>>>(m, reinterpret_cast<const typename C::InT *>(in),
+                kern<<<(unsigned)P.ntiles, block, smem, st>>>(m, m1, reinterpret_cast<const typename C::InT *>(in),
                                                               reinterpret_cast<typename C::OutT *>(out), P, sc);
                 return cudaGetLastError();
             }
