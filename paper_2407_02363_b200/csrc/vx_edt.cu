@@ -57,6 +57,15 @@ __device__ unsigned long long *g_phase_buf = nullptr;
 #endif
 constexpr int kMaxBands = VX_MAX_BANDS;
 constexpr int kColThreads = 32 * kMaxBands;
+// pass-3 narrow stack entries: 1 = (x, w) (F is one IMAD; the winner's site
+// code is re-read from L2), 0 = (x, sy, sz) (F decodes; no re-read)
+#ifndef VX_P3_XW
+#define VX_P3_XW 1
+#endif
+constexpr bool kP3XW = VX_P3_XW != 0;
+#ifndef VX_CMP_GROUP_ROWS
+#define VX_CMP_GROUP_ROWS 24   // target candidates per group in compact pass 3
+#endif
 #ifndef VX_BAND_ROWS
 #define VX_BAND_ROWS 32   // target rows per band
 #endif
@@ -242,9 +251,11 @@ struct Col {
             else { sy = (uint32_t)v >> P.zb; sz = (uint32_t)v & P.zmask; }
             if constexpr (EW) {
                 return ((EntT)row << 42) | ((EntT)sy << 21) | (EntT)sz;
-            } else {
+            } else if constexpr (kP3XW) {
                 const int dy = j - (int)sy, dz = k - (int)sz;
                 return ((EntT)row << P.wb) | (EntT)(uint32_t)(dy * dy + dz * dz);
+            } else {
+                return ((EntT)row << P.yzb) | (EntT)v;
             }
         }
     }
@@ -254,7 +265,8 @@ struct Col {
             else return (int)(e >> P.zb);
         } else {
             if constexpr (EW) return (int)(e >> 42);
-            else return (int)(e >> P.wb);
+            else if constexpr (kP3XW) return (int)(e >> P.wb);
+            else return (int)(e >> P.yzb);
         }
     }
     // F = w + row^2 (edt.py:261-262, 362-364 fold the row term in at test time)
@@ -270,14 +282,19 @@ struct Col {
                 const int x = (int)(e >> 42), sy = (int)((e >> 21) & 0x1fffffull), sz = (int)(e & 0x1fffffull);
                 const FT dy = (FT)(j - sy), dz = (FT)(k - sz);
                 return dy * dy + dz * dz + (FT)x * (FT)x;
-            } else {
+            } else if constexpr (kP3XW) {
                 const int x = (int)(e >> P.wb);
                 return (FT)x * (FT)x + (FT)((uint32_t)e & P.wmask);
+            } else {
+                const int x = (int)(e >> P.yzb), sy = (int)(((uint32_t)e >> P.zb) & P.ymask);
+                const int sz = (int)((uint32_t)e & P.zmask);
+                const FT dy = (FT)(j - sy), dz = (FT)(k - sz);
+                return dy * dy + dz * dz + (FT)x * (FT)x;
             }
         }
     }
     // pass 3 narrow: does output() need the site code re-read from the input?
-    static constexpr bool kRereadCode = PASS == 3 && !EW;
+    static constexpr bool kRereadCode = PASS == 3 && !EW && kP3XW;
     static __device__ __forceinline__ OutT output(const ColParams &P, EntT e, InT code) {
         if constexpr (PASS == 2) {
             return (OutT)e;  // the entry is the s2 code
@@ -286,10 +303,13 @@ struct Col {
             if constexpr (EW) {
                 x = (long long)(e >> 42); sy = (long long)((e >> 21) & 0x1fffffull);
                 sz = (long long)(e & 0x1fffffull);
-            } else {
+            } else if constexpr (kP3XW) {
                 x = (long long)(e >> P.wb);
                 if constexpr (S2W) { sy = (long long)(code >> 32); sz = (long long)(uint32_t)code; }
                 else { sy = (long long)((uint32_t)code >> P.zb); sz = (long long)((uint32_t)code & P.zmask); }
+            } else {
+                x = (long long)(e >> P.yzb); sy = (long long)(((uint32_t)e >> P.zb) & P.ymask);
+                sz = (long long)((uint32_t)e & P.zmask);
             }
             return (int32_t)(x * P.plane + sy * P.nz + sz);  // edt.py:417
         }
@@ -431,11 +451,17 @@ __device__ __forceinline__ void column_tile(const typename Col<PASS, S2W, EW, FW
     // slots [alo, ahi) of the staged tile; CMP: the tile holds only the rows
     // of occupied slices (slot t = row xs[t]), split evenly over the bands
     int alo = lo, ahi = hi;
+    int G = P.B;   // groups that build band hulls (and then merge: log2 G rounds)
     if constexpr (CMP) {
         const int m = __ldg(P.hdr);
-        const int wc = (m + P.B - 1) / P.B;
-        alo = min(m, b * wc);
-        ahi = min(m, alo + wc);
+        if (m < P.L) {
+            // few occupied slices: longer groups, fewer merge rounds
+            G = 1;
+            while (2 * G <= P.B && 2 * G * VX_CMP_GROUP_ROWS <= m) G *= 2;
+        }
+        const int wc = (m + G - 1) / G;
+        alo = b < G ? min(m, b * wc) : m;
+        ahi = b < G ? min(m, alo + wc) : m;
     }
     int n = 0;
     if (colok) {
@@ -488,7 +514,7 @@ __device__ __forceinline__ void column_tile(const typename Col<PASS, S2W, EW, FW
     VX_PT(2);
 
     // ---- phase B: pairwise bridge merges (same hull as edt.py:277-294) ---
-    for (int r = 1; r < P.B; r <<= 1) {
+    for (int r = 1; r < G; r <<= 1) {
         if (colok && (b & (2 * r - 1)) == r) {
             const int gl = b - r, gm = b, ge = min(P.B, b + r);
             int bl = gm - 1;
@@ -932,7 +958,7 @@ bool make_plan(int nx, int ny, int nz, EdtPlan *p, int force_global_stack) {
     if (fg && atoi(fg)) force_global_stack = 1;
     q.s2_wide = q.yb + q.zb > 31 || force_wide >= 3;   // keep all-ones free as the sentinel
     q.wb = bits_of((long long)(ny - 1) * (ny - 1) + (long long)(nz - 1) * (nz - 1));
-    q.e3_wide = q.s2_wide || (q.xb + q.wb > 32) || force_wide >= 2;
+    q.e3_wide = q.s2_wide || (kP3XW ? q.xb + q.wb > 32 : q.xb + q.yb + q.zb > 32) || force_wide >= 2;
     // weights: F = w + row^2 <= (nx-1)^2+(ny-1)^2+(nz-1)^2; products F * L
     const double fmax = (double)(nx - 1) * (nx - 1) + (double)(ny - 1) * (ny - 1) +
                         (double)(nz - 1) * (nz - 1);
@@ -1019,9 +1045,18 @@ __global__ void __launch_bounds__(256) k_slice_flags(const uint8_t *__restrict__
     bool any = false;
     if ((plane & 15) == 0 && ((uintptr_t)occ & 15) == 0) {
         const uint4 *v = reinterpret_cast<const uint4 *>(src);
-        for (long long q = threadIdx.x; q < (plane >> 4) && !any; q += blockDim.x) {
-            const uint4 w = __ldg(v + q);
-            any = (w.x | w.y | w.z | w.w) != 0u;
+        const long long nv = plane >> 4;
+        for (long long q0 = threadIdx.x; q0 < nv && !any; q0 += 8 * blockDim.x) {
+            uint32_t acc = 0;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {   // 8 independent 16-byte loads in flight
+                const long long q = q0 + (long long)u * blockDim.x;
+                if (q < nv) {
+                    const uint4 w = __ldg(v + q);
+                    acc |= w.x | w.y | w.z | w.w;
+                }
+            }
+            any = acc != 0u;
         }
     } else {
         for (long long q = threadIdx.x; q < plane && !any; q += blockDim.x) any = src[q] != 0;

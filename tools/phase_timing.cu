@@ -26,6 +26,12 @@ int main(int argc, char **argv) {
     int32_t *s1 = (int32_t *)scratch;
     const size_t s1b = (n * 4 + 255) & ~(size_t)255;
     void *s2 = (char *)scratch + s1b;
+    const size_t s2b = (n * 4 + 255) & ~(size_t)255;
+    const bool sparse = vx::sparse_ok(p, 1);
+    const vx::SparseRows sp = vx::sparse_rows_at((char *)scratch + s1b + s2b + p.gstack_bytes, p);
+    const vx::SparseRows *spp = sparse ? &sp : nullptr;
+    if (sparse) { vx::launch_slice_list(occ, p, sp, 0); cudaDeviceSynchronize(); }
+    printf("sparse path: %d\n", (int)sparse);
     {   // plain kernel timings (CUDA events), instrumentation buffer detached
         unsigned long long *null_buf = nullptr;
         cudaMemcpyToSymbol(vx::g_phase_buf, &null_buf, sizeof null_buf);
@@ -34,11 +40,11 @@ int main(int argc, char **argv) {
         float t1 = 0, t2 = 0, t3 = 0;
         for (int rep = 0; rep < 6; ++rep) {
             cudaEventRecord(e[0]);
-            vx::launch_pass1(occ, s1, nx, ny, nz, 0);
+            vx::launch_pass1(occ, s1, nx, ny, nz, 0, sparse ? sp.sflag : nullptr);
             cudaEventRecord(e[1]);
-            vx::launch_pass2(s1, s2, nullptr, p, nx, 0);
+            vx::launch_pass2(s1, s2, nullptr, p, nx, 0, spp);
             cudaEventRecord(e[2]);
-            vx::launch_pass3(s2, site, nullptr, p, 1, 0, ny, 0);
+            vx::launch_pass3(s2, site, nullptr, p, 1, 0, ny, 0, spp);
             cudaEventRecord(e[3]);
             cudaEventSynchronize(e[3]);
             float a, b, c;
@@ -52,17 +58,17 @@ int main(int argc, char **argv) {
     }
     for (int pass = 2; pass <= 3; ++pass) {
         for (int rep = 0; rep < 3; ++rep) {
-            vx::launch_pass1(occ, s1, nx, ny, nz, 0);
-            vx::launch_pass2(s1, s2, nullptr, p, nx, 0);
+            vx::launch_pass1(occ, s1, nx, ny, nz, 0, sparse ? sp.sflag : nullptr);
+            vx::launch_pass2(s1, s2, nullptr, p, nx, 0, spp);
             if (pass == 3) {
                 cudaMemset(buf, 0, tiles * 64);
-                vx::launch_pass3(s2, site, nullptr, p, 1, 0, ny, 0);
+                vx::launch_pass3(s2, site, nullptr, p, 1, 0, ny, 0, spp);
             }
             cudaDeviceSynchronize();
         }
         if (pass == 2) {  // re-run pass 2 with the buffer cleared
             cudaMemset(buf, 0, tiles * 64);
-            vx::launch_pass2(s1, s2, nullptr, p, nx, 0);
+            vx::launch_pass2(s1, s2, nullptr, p, nx, 0, spp);
             cudaDeviceSynchronize();
         }
         const long long nt = (long long)((nz + 31) / 32) * (pass == 2 ? nx : ny);
