@@ -92,23 +92,8 @@ __device__ __forceinline__ int pick(int k, int l, int r) {
 // lane owns 4 consecutive voxels of each 128-voxel chunk.
 // ---------------------------------------------------------------------------
 template <int CMAX>
-__global__ void __launch_bounds__(256) k_pass1_v4(const uint8_t *__restrict__ occ,
-                                                  int32_t *__restrict__ s1,
-                                                  long long nlines, int nz,
-                                                  const uint8_t *__restrict__ sflag, int ny) {
-    const int lane = threadIdx.x & 31;
-    const long long line = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (line >= nlines) return;  // warp-uniform
-    if (sflag && !sflag[line / ny]) return;  // empty slice: nothing downstream reads it
-    const uint32_t *src = reinterpret_cast<const uint32_t *>(occ + line * nz);
-    int4 *dst = reinterpret_cast<int4 *>(s1 + line * nz);
-    const int nq = nz >> 2;
-    uint32_t nib[CMAX];
-#pragma unroll
-    for (int c = 0; c < CMAX; ++c) {
-        const int q = c * 32 + lane;
-        nib[c] = nibble4(q < nq ? __ldg(src + q) : 0u);
-    }
+__device__ __forceinline__ void pass1_line(const uint32_t (&nib)[CMAX], int4 *__restrict__ dst, int nq,
+                                           int lane) {
     // forward: exclusive prefix max of the last occupied k
     int exl[CMAX];
     int carry = -1;
@@ -161,6 +146,35 @@ __global__ void __launch_bounds__(256) k_pass1_v4(const uint8_t *__restrict__ oc
     }
 }
 
+// LPW lines per warp: all their loads are issued before any line is scanned
+// (memory-level parallelism for the streaming read).
+template <int CMAX, int LPW>
+__global__ void __launch_bounds__(256) k_pass1_v4(const uint8_t *__restrict__ occ,
+                                                  int32_t *__restrict__ s1,
+                                                  long long nlines, int nz,
+                                                  const uint8_t *__restrict__ sflag, int ny) {
+    const int lane = threadIdx.x & 31;
+    const long long line0 = ((long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * LPW;
+    const int nq = nz >> 2;
+    uint32_t nib[LPW][CMAX];
+    bool act[LPW];
+#pragma unroll
+    for (int l = 0; l < LPW; ++l) {
+        const long long line = line0 + l;
+        // warp-uniform; empty slices are skipped (nothing downstream reads them)
+        act[l] = line < nlines && (!sflag || sflag[(uint32_t)line / (uint32_t)ny]);
+        const uint32_t *src = reinterpret_cast<const uint32_t *>(occ + line * nz);
+#pragma unroll
+        for (int c = 0; c < CMAX; ++c) {
+            const int q = c * 32 + lane;
+            nib[l][c] = nibble4(act[l] && q < nq ? __ldg(src + q) : 0u);
+        }
+    }
+#pragma unroll
+    for (int l = 0; l < LPW; ++l)
+        if (act[l]) pass1_line<CMAX>(nib[l], reinterpret_cast<int4 *>(s1 + (line0 + l) * nz), nq, lane);
+}
+
 // Pass 1, generic path (any nz): 32-voxel chunks with ballots; the forward
 // sweep parks `l` in the output, the backward sweep combines.
 __global__ void __launch_bounds__(256) k_pass1_generic(const uint8_t *__restrict__ occ,
@@ -170,7 +184,7 @@ __global__ void __launch_bounds__(256) k_pass1_generic(const uint8_t *__restrict
     const int lane = threadIdx.x & 31;
     const long long line = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (line >= nlines) return;
-    if (sflag && !sflag[line / ny]) return;
+    if (sflag && !sflag[(uint32_t)line / (uint32_t)ny]) return;
     const uint8_t *src = occ + line * nz;
     int32_t *dst = s1 + line * nz;
     int carry = -1;
@@ -1012,12 +1026,13 @@ cudaError_t launch_pass1(const uint8_t *occ, int32_t *s1, long long nslices, int
     const long long nlines = nslices * ny;
     if (nlines == 0) return cudaSuccess;
     const unsigned grid = (unsigned)((nlines + 7) / 8);
+    const unsigned grid2 = (unsigned)((nlines + 15) / 16);
     const bool vec = (nz % 4 == 0) && ((uintptr_t)occ % 16 == 0) && ((uintptr_t)s1 % 16 == 0);
-    if (vec && nz <= 128) k_pass1_v4<1><<<grid, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny);
-    else if (vec && nz <= 256) k_pass1_v4<2><<<grid, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny);
-    else if (vec && nz <= 512) k_pass1_v4<4><<<grid, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny);
-    else if (vec && nz <= 1024) k_pass1_v4<8><<<grid, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny);
-    else if (vec && nz <= 2048) k_pass1_v4<16><<<grid, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny);
+    if (vec && nz <= 128) k_pass1_v4<1, 2><<<grid2, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny);
+    else if (vec && nz <= 256) k_pass1_v4<2, 2><<<grid2, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny);
+    else if (vec && nz <= 512) k_pass1_v4<4, 2><<<grid2, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny);
+    else if (vec && nz <= 1024) k_pass1_v4<8, 1><<<grid, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny);
+    else if (vec && nz <= 2048) k_pass1_v4<16, 1><<<grid, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny);
     else k_pass1_generic<<<grid, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny);
     return cudaGetLastError();
 }
