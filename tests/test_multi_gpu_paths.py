@@ -61,3 +61,20 @@ def test_slab_single_rank_api():
     slab = SlabEDT(occ.shape, exchange="nccl")
     site = slab(torch.from_numpy(occ).cuda()).cpu().numpy()
     assert np.array_equal(site, O.pba_edt_site(occ))
+
+
+@pytest.mark.parametrize("rec", __import__("tests.golden_util", fromlist=["golden"]).golden()
+                         .get("edt_digests_1024", []), ids=lambda r: f"1024-{r['p']}")
+def test_c5_1024_single_gpu_and_slab_vs_reference(rec):
+    """Config C5 (1024^3): the single-GPU EDT and the 8-rank slab pipeline
+    (emulated, both transports' addressing) against the reference digest."""
+    from tests.golden_util import digest
+    occ = synth.bernoulli_occupancy(rec["dims"], rec["p"], rec["seed"])
+    d_occ = torch.from_numpy(occ).cuda()
+    del occ
+    site = _edt_batched(d_occ.unsqueeze(0))[0]
+    assert digest(site.cpu().numpy()) == rec["site"]
+    del site
+    torch.cuda.empty_cache()
+    got = emulate_ranks(d_occ, 8, "p2p").cpu().numpy()
+    assert digest(got) == rec["site"]
