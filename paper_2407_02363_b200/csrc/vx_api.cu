@@ -642,9 +642,9 @@ extern "C" int vx_edt_pass12_scatter(vx_ctx *c, const uint8_t *d_occ, int nx, in
     }
     int32_t *s1 = (int32_t *)d_scratch;
     cudaError_t e = launch_pass1(d_occ, s1, nxl, ny, nz, c->stream);
-    if (e == cudaSuccess)
-        e = launch_pass2_scatter(s1, tab, (unsigned char *)d_scratch + s1b, p, nxl, c->stream);
-    if (e != cudaSuccess) return cuda_fail(e, "pass12_scatter");
+    if (e != cudaSuccess) return cuda_fail(e, "pass12_scatter (pass 1)");
+    e = launch_pass2_scatter(s1, tab, (unsigned char *)d_scratch + s1b, p, nxl, c->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "pass12_scatter (pass 2)");
     c->launches += 2;
     return VX_OK;
 }

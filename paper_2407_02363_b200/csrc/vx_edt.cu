@@ -34,6 +34,9 @@
 
 #include <algorithm>
 #include <type_traits>
+#include <mutex>
+#include <set>
+#include <utility>
 #include <cstdlib>
 
 namespace vx {
@@ -826,13 +829,21 @@ ColParams col_params(const EdtPlan &p, int pass, long long nouter, int nyl, int 
     return P;
 }
 
-// raise the dynamic shared-memory ceiling once per kernel instantiation (the
+// raise the dynamic shared-memory ceiling once per kernel and device (the
 // per-launch size is the launch parameter); keeps the launch path cheap
 template <typename K>
 cudaError_t allow_smem(K kern) {
-    static cudaError_t done = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   (int)kSmemLimit);
-    return done;
+    static std::mutex mu;
+    static std::set<std::pair<const void *, int>> done;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const auto key = std::make_pair(reinterpret_cast<const void *>(kern), dev);
+    std::lock_guard<std::mutex> lock(mu);
+    if (done.count(key)) return cudaSuccess;
+    const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)kSmemLimit);
+    if (e == cudaSuccess) done.insert(key);
+    return e;
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
