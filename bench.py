@@ -473,7 +473,7 @@ def edt_sweep(ctx, stream):
     L = _lib.load()
     out = {}
     cases = [(n, "bernoulli_0.02") for n in (64, 96, 128, 192, 256, 384, 512)]
-    cases += [(512, "single_center"), (512, "bernoulli_1e-4")]
+    cases += [(512, "single_center"), (512, "bernoulli_1e-4"), (1024, "bernoulli_0.02")]
     for n, kind in cases:
         dims = (n, n, n)
         if kind == "single_center":
@@ -491,7 +491,7 @@ def edt_sweep(ctx, stream):
         for _ in range(3):
             _lib.check(L.vx_edt_device(*args))
         torch.cuda.synchronize()
-        reps = 10 if n <= 256 else 5
+        reps = 10 if n <= 256 else (5 if n <= 512 else 3)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(reps):
