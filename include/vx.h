@@ -84,6 +84,16 @@ int vx_grid_clear(vx_grid *g);
 int vx_grid_insert_points(vx_grid *g, const double *xyz, int64_t n, float hit_logodds,
                           double occupancy_threshold, const vx_grid *robot_mask,
                           vx_insert_stats *stats);
+/* insert_point_cloud with the statistical outlier filter (grids.py:166-169,
+ * 224-240) when k_neighbors > 0 (k_neighbors <= 31): exact kNN on the GPU
+ * and numpy's summation order, so the survivors equal the reference's.
+ * stats->outliers_removed is filled. */
+int vx_grid_insert_points_ex(vx_grid *g, const double *xyz, int64_t n, float hit_logodds,
+                             double occupancy_threshold, const vx_grid *robot_mask,
+                             int k_neighbors, double std_multiplier, vx_insert_stats *stats);
+/* statistical_outlier_filter (grids.py:224-240) alone: keep mask (1 = kept) */
+int vx_outlier_mask(vx_ctx *ctx, const double *xyz, int64_t n, int k_neighbors,
+                    double std_multiplier, uint8_t *keep_out, int64_t *removed);
 /* Same, points already in device memory (stream-ordered, stats stay on the
  * device until vx_grid_last_stats). */
 int vx_grid_insert_points_device(vx_grid *g, const double *d_xyz, int64_t n, float hit_logodds,

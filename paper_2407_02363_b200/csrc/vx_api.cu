@@ -71,7 +71,7 @@ constexpr float kOccThr = 0.0f;  // float32(logit(0.5)): the cached occupancy th
 struct vx_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
-    DevBuf scratch, staging, staging2, temp;
+    DevBuf scratch, staging, staging2, temp, outl;
     long long launches = 0;
 };
 
@@ -135,6 +135,7 @@ extern "C" int vx_ctx_destroy(vx_ctx *c) {
     c->staging.release();
     c->staging2.release();
     c->temp.release();
+    c->outl.release();
     cudaStreamDestroy(c->stream);
     delete c;
     return VX_OK;
@@ -240,14 +241,14 @@ static bool same_geometry(const vx_grid *a, const vx_grid *b) {  // grids.py:214
 }
 
 static int insert_device(vx_grid *g, const double *d_xyz, long long n, const long long *n_dev,
-                         float hit, double thr, const vx_grid *mask) {
+                         float hit, double thr, const vx_grid *mask, const uint8_t *keep = nullptr) {
     if (mask && !same_geometry(g, mask))
         return fail(VX_EINVAL, "robot_mask geometry does not match this grid");
     cudaStream_t st = g->ctx->stream;
     VX_CUDA(cudaMemsetAsync(g->ctr, 0, 3 * sizeof(unsigned long long), st));
     const float thr32 = (float)logit(thr);  // numpy compares in float32
     cudaError_t e = launch_scatter(d_xyz, n, (const int64_t *)n_dev, g->g, mask ? mask->cells : nullptr,
-                                   thr32, g->counts, g->touched, g->ctr, g->capacity, st);
+                                   thr32, g->counts, g->touched, g->ctr, g->capacity, st, keep);
     if (e != cudaSuccess) return cuda_fail(e, "scatter");
     g->ctx->launches += 1;
     if (g->maybe_oor) {
@@ -301,6 +302,83 @@ extern "C" int vx_grid_insert_points(vx_grid *g, const double *xyz, int64_t n, f
     rc = vx_grid_last_stats(g, &s);
     if (rc) return rc;
     if (s.inserted > 0) g->maybe_oor = false;  // the dense clip ran
+    if (stats) *stats = s;
+    return VX_OK;
+}
+
+// statistical_outlier_filter (grids.py:224-240) on device points: keep mask
+// into outl scratch, removed count into *removed_host (syncs)
+static int outlier_device(vx_ctx *c, const double *d_xyz, long long n, int k, double stdm, uint8_t **keep_out,
+                          long long *removed_host) {
+    if (k > 31) return fail(VX_EINVAL, "k_neighbors > 31 is not supported on the GPU");
+    auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
+    const size_t need = al(n) + 256 + outlier_scratch_bytes(n) + 148 * 6 * 8 + 256;
+    VX_CUDA(c->outl.ensure(need));
+    unsigned char *p = (unsigned char *)c->outl.p;
+    uint8_t *keep = p;
+    unsigned long long *removed = (unsigned long long *)(p + al(n));
+    void *scr = p + al(n) + 256;
+    double lo[3], hi[3];
+    VX_CUDA(cloud_bounds(d_xyz, n, lo, hi, (unsigned char *)scr + outlier_scratch_bytes(n), c->stream));
+    VX_CUDA(cudaMemsetAsync(removed, 0, sizeof(unsigned long long), c->stream));
+    cudaError_t e = outlier_filter(d_xyz, n, k, stdm, lo, hi, keep, removed, scr, outlier_scratch_bytes(n),
+                                   c->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "outlier_filter");
+    c->launches += 9;
+    unsigned long long rem = 0;
+    VX_CUDA(cudaMemcpyAsync(&rem, removed, sizeof rem, cudaMemcpyDeviceToHost, c->stream));
+    VX_CUDA(cudaStreamSynchronize(c->stream));
+    *keep_out = keep;
+    *removed_host = (long long)rem;
+    return VX_OK;
+}
+
+extern "C" int vx_outlier_mask(vx_ctx *c, const double *xyz, int64_t n, int k_neighbors, double std_multiplier,
+                               uint8_t *keep_host, int64_t *removed) {
+    if (!c || (n > 0 && (!xyz || !keep_host))) return fail(VX_EINVAL, "NULL argument");
+    if (k_neighbors < 0) return fail(VX_EINVAL, "k_neighbors must be >= 0");
+    if (!(std_multiplier > 0.0)) return fail(VX_EINVAL, "std_multiplier must be > 0");
+    if (n <= k_neighbors || n == 0 || k_neighbors == 0) {   // grids.py:233-234: pass through
+        if (n > 0) std::memset(keep_host, 1, (size_t)n);
+        if (removed) *removed = 0;
+        return VX_OK;
+    }
+    VX_CUDA(c->staging.ensure((size_t)n * 24));
+    VX_CUDA(cudaMemcpyAsync(c->staging.p, xyz, (size_t)n * 24, cudaMemcpyHostToDevice, c->stream));
+    uint8_t *keep = nullptr;
+    long long rem = 0;
+    int rc = outlier_device(c, (const double *)c->staging.p, n, k_neighbors, std_multiplier, &keep, &rem);
+    if (rc) return rc;
+    VX_CUDA(cudaMemcpyAsync(keep_host, keep, (size_t)n, cudaMemcpyDeviceToHost, c->stream));
+    VX_CUDA(cudaStreamSynchronize(c->stream));
+    if (removed) *removed = rem;
+    return VX_OK;
+}
+
+extern "C" int vx_grid_insert_points_ex(vx_grid *g, const double *xyz, int64_t n, float hit, double thr,
+                                        const vx_grid *mask, int k_neighbors, double std_multiplier,
+                                        vx_insert_stats *stats) {
+    if (!g || (n > 0 && !xyz)) return fail(VX_EINVAL, "NULL argument");
+    if (k_neighbors < 0) return fail(VX_EINVAL, "k_neighbors must be >= 0");
+    if (!(std_multiplier > 0.0)) return fail(VX_EINVAL, "std_multiplier must be > 0");
+    if (k_neighbors == 0 || n <= k_neighbors)
+        return vx_grid_insert_points(g, xyz, n, hit, thr, mask, stats);
+    if (mask && !same_geometry(g, mask))
+        return fail(VX_EINVAL, "robot_mask geometry does not match this grid");
+    vx_ctx *c = g->ctx;
+    VX_CUDA(c->staging.ensure((size_t)n * 24));
+    VX_CUDA(cudaMemcpyAsync(c->staging.p, xyz, (size_t)n * 24, cudaMemcpyHostToDevice, c->stream));
+    uint8_t *keep = nullptr;
+    long long rem = 0;
+    int rc = outlier_device(c, (const double *)c->staging.p, n, k_neighbors, std_multiplier, &keep, &rem);
+    if (rc) return rc;
+    rc = insert_device(g, (const double *)c->staging.p, n, nullptr, hit, thr, mask, keep);
+    if (rc) return rc;
+    vx_insert_stats s;
+    rc = vx_grid_last_stats(g, &s);
+    if (rc) return rc;
+    s.outliers_removed = rem;
+    if (s.inserted > 0) g->maybe_oor = false;
     if (stats) *stats = s;
     return VX_OK;
 }

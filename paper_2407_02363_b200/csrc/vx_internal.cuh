@@ -92,7 +92,7 @@ cudaError_t launch_dense_clip(float *cells, const uint32_t *counts, int64_t n,
 cudaError_t launch_scatter(const double *pts, int64_t npts, const int64_t *npts_dev,
                            GridGeom g, const float *mask_cells, float thr, uint32_t *counts,
                            int32_t *touched, DevCounters *ctr, int capacity,
-                           cudaStream_t st);
+                           cudaStream_t st, const uint8_t *keep = nullptr);
 cudaError_t launch_finalize(float *cells, uint8_t *occ, uint32_t *counts, int32_t *touched,
                             DevCounters *ctr, int64_t n, int capacity, int64_t max_new,
                             float hit, float occ_thr, cudaStream_t st);
@@ -103,6 +103,14 @@ cudaError_t launch_stamp(const int32_t *ijk, const int64_t *offsets, int nsets,
                          int capacity, int64_t total, cudaStream_t st);
 cudaError_t launch_occupancy(const float *cells, uint8_t *out, int64_t n, float thr,
                              cudaStream_t st);
+
+// ---- statistical outlier filter (grids.py:224-240) ---------------------------
+size_t outlier_scratch_bytes(long long n);
+cudaError_t cloud_bounds(const double *pts, long long n, double lo[3], double hi[3], void *scratch,
+                         cudaStream_t st);
+cudaError_t outlier_filter(const double *pts, long long n, int k, double stdm, const double lo[3],
+                           const double hi[3], uint8_t *keep, unsigned long long *removed, void *scratch,
+                           size_t scratch_bytes, cudaStream_t st);
 
 // ---- query ----------------------------------------------------------------
 cudaError_t launch_site_world(const int32_t *site, GridGeom g, const double *centers,

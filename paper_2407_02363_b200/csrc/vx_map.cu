@@ -96,7 +96,7 @@ __global__ void k_scatter(const double *__restrict__ pts, long long npts,
                           const long long *__restrict__ npts_dev, GridGeom g,
                           const float *__restrict__ mask_cells, float thr,
                           uint32_t *__restrict__ counts, int32_t *__restrict__ touched,
-                          DevCounters *__restrict__ ctr, int capacity) {
+                          DevCounters *__restrict__ ctr, int capacity, const uint8_t *__restrict__ keep) {
     const long long n = npts_dev ? *npts_dev : npts;
     const int base = ctr->touched;
     const long long nth = (long long)gridDim.x * blockDim.x;
@@ -106,7 +106,7 @@ __global__ void k_scatter(const double *__restrict__ pts, long long npts,
     for (long long it = 0; it < trips; ++it) {
         const long long p = start + it * nth;
         bool oob = false, skip = false, ins = false;
-        if (p < n) {
+        if (p < n && (!keep || keep[p])) {   // outliers were removed before discretising (grids.py:166-170)
             const double x = pts[3 * p], y = pts[3 * p + 1], z = pts[3 * p + 2];
             const long long lin = discretize(x, y, z, g);
             if (lin < 0) {
@@ -245,10 +245,10 @@ cudaError_t launch_dense_clip(float *cells, const uint32_t *counts, int64_t n,
 
 cudaError_t launch_scatter(const double *pts, int64_t npts, const int64_t *npts_dev, GridGeom g,
                            const float *mask_cells, float thr, uint32_t *counts, int32_t *touched,
-                           DevCounters *ctr, int capacity, cudaStream_t st) {
+                           DevCounters *ctr, int capacity, cudaStream_t st, const uint8_t *keep) {
     if (npts <= 0 && !npts_dev) return cudaSuccess;
     k_scatter<<<grid_for(npts, 256), 256, 0, st>>>(pts, npts, (const long long *)npts_dev, g,
-                                                   mask_cells, thr, counts, touched, ctr, capacity);
+                                                   mask_cells, thr, counts, touched, ctr, capacity, keep);
     return cudaGetLastError();
 }
 

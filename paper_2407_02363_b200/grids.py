@@ -15,9 +15,8 @@ Reference line map:
   VoxelSet                 grids.py:73-88
   InsertStats              grids.py:91-96
   VoxelGrid                grids.py:99-217
-The statistical outlier filter (grids.py:224-240, k_neighbors > 0) is not on
-the GPU yet (SURVEY 8(f) "next"); it raises NotImplementedError rather than
-falling back to a CPU implementation.
+The statistical outlier filter (grids.py:224-240, k_neighbors > 0) runs on the
+GPU too (vx_outlier.cu): exact kNN and numpy's summation order.
 """
 
 from __future__ import annotations
@@ -208,19 +207,18 @@ class VoxelGrid:
         pts = cloud.world_points()
         if pts.shape[0] == 0:
             return stats
-        if cfg.k_neighbors > 0:
-            raise NotImplementedError(
-                "statistical outlier filter (k_neighbors > 0) is not implemented on the GPU yet; "
-                "use FilterConfig(k_neighbors=0)")
         pts = np.ascontiguousarray(pts, dtype=np.float64)
         self._push()
         mh = robot_mask.handle if robot_mask is not None else None
         st = _lib.InsertStatsC()
-        _lib.check(_lib.load().vx_grid_insert_points(
+        # k_neighbors > 0: statistical outlier filter on the GPU first (grids.py:166-169)
+        _lib.check(_lib.load().vx_grid_insert_points_ex(
             self._h, _lib.ptr(pts), pts.shape[0], float(np.float32(cfg.hit_logodds)),
-            float(cfg.occupancy_threshold), mh, ctypes.byref(st)))
+            float(cfg.occupancy_threshold), mh, int(cfg.k_neighbors), float(cfg.std_multiplier),
+            ctypes.byref(st)))
         self._touched()
         stats.inserted = int(st.inserted)
+        stats.outliers_removed = int(st.outliers_removed)
         stats.robot_skipped = int(st.robot_skipped)
         stats.out_of_bounds = int(st.out_of_bounds)
         return stats
@@ -280,3 +278,18 @@ class VoxelGrid:
 
 def new_grid(dims, voxel_size: float, origin=(0.0, 0.0, 0.0)) -> VoxelGrid:
     return VoxelGrid(dims, voxel_size, origin)
+
+
+def statistical_outlier_filter(points: np.ndarray, k_neighbors: int,
+                               std_multiplier: float) -> np.ndarray:
+    """grids.py:224-240 on the GPU: the points whose mean k-NN distance is at
+    most mean + std_multiplier * std (population); <= k points pass through."""
+    pts = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 3)
+    if pts.shape[0] <= k_neighbors or pts.shape[0] == 0:
+        return pts
+    keep = np.empty(pts.shape[0], np.uint8)
+    removed = ctypes.c_int64()
+    _lib.check(_lib.load().vx_outlier_mask(_lib.default_context().handle, _lib.ptr(pts),
+                                           pts.shape[0], int(k_neighbors), float(std_multiplier),
+                                           _lib.ptr(keep), ctypes.byref(removed)))
+    return pts[keep.view(np.bool_)]

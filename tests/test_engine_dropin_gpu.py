@@ -21,14 +21,14 @@ from paper_2407_02363_b200 import voxarm_bridge  # noqa: E402
 pytestmark = pytest.mark.gpu
 
 
-def _scenario(obstacles, duration=0.3, grid=None):
+def _scenario(obstacles, duration=0.3, grid=None, k_neighbors=0):
     from voxarm.robot import shipped_robot_path
     from voxarm.scenario import CloudConfig, GridSpec, Scenario
     from voxarm.tasks import AvoidanceConfig
     grid = grid or GridSpec(dims=(48, 48, 48), voxel_size=0.04, origin=(-0.96, -0.96, -0.24))
     return Scenario(name="gpu-parity", robot_path=shipped_robot_path(), grid=grid,
                     duration=duration, q0=[0, 0, 0.2, 0, 0.5, 0, 0.3, 0], obstacles=obstacles,
-                    cloud=CloudConfig(points_per_obstacle=800, k_neighbors=0),
+                    cloud=CloudConfig(points_per_obstacle=800, k_neighbors=k_neighbors),
                     avoidance=AvoidanceConfig(kappa=10.0, x_star_offset=0.12))
 
 
@@ -58,9 +58,10 @@ OBSTACLES = [
 ]
 
 
+@pytest.mark.parametrize("k", [0, 8], ids=["k0", "k8-default-filter"])
 @pytest.mark.parametrize("obstacles", OBSTACLES, ids=["static", "moving"])
-def test_closed_loop_identical_to_cpu_engine(obstacles):
-    sc = _scenario(obstacles)
+def test_closed_loop_identical_to_cpu_engine(obstacles, k):
+    sc = _scenario(obstacles, k_neighbors=k)
     ticks = 60
     cpu = _run(sc, gpu=False, ticks=ticks)
     gpu = _run(sc, gpu=True, ticks=ticks)

@@ -291,7 +291,3 @@ def test_full_grid_occupied_count():                         # 226-229
     assert g.occupied_voxels().shape[0] == 27
 
 
-def test_outlier_filter_not_silently_skipped():
-    g = new_grid((4, 4, 4), 0.1)
-    with pytest.raises(NotImplementedError):
-        g.insert_point_cloud(PointCloud(points=np.zeros((20, 3))), FilterConfig(k_neighbors=8))
