@@ -401,6 +401,7 @@ def run_gpu(args, world, rank, local):
     if not args.no_sweep:
         line["edt_sweep"] = edt_sweep(ctx, stream)
         line["small_configs"] = small_configs(d)
+        line["outlier_filter"] = outlier_timing()
     if not args.no_cpu_baseline and world == 1:
         line["cpu_baseline"] = cpu_baseline_sample(d)
     print(json.dumps(line), flush=True)
@@ -462,6 +463,30 @@ def small_configs(d, steps: int = 20):
         out[name] = {"device_ms_per_tick": dev_ms, "e2e_ms_per_tick": e2e_ms,
                      "points": int(clouds[0].shape[0]), "hz_e2e": 1e3 / e2e_ms}
         cyc.close()
+    return out
+
+
+def outlier_timing():
+    """insert_point_cloud with the engine's default filter (k_neighbors=8,
+    grids.py:166-169) on the 300k-point C2 cloud through the public API
+    (host points in, stats out), vs k_neighbors=0."""
+    from paper_2407_02363_b200 import FilterConfig, PointCloud, VoxelGrid
+    from paper_2407_02363_b200 import synth
+    pts = synth.depth_camera_cloud(0.1)
+    g = VoxelGrid((256, 256, 256), 0.02, (-2.56, -2.56, -0.24))
+    out = {"points": int(pts.shape[0])}
+    for k in (0, 8):
+        cfg = FilterConfig(k_neighbors=k)
+        for _ in range(2):
+            g.clear()
+            g.insert_point_cloud(PointCloud(pts), cfg)
+        t0 = time.perf_counter()
+        reps = 5
+        for _ in range(reps):
+            g.clear()
+            st = g.insert_point_cloud(PointCloud(pts), cfg)
+        out[f"k{k}_ms"] = (time.perf_counter() - t0) / reps * 1e3
+        out[f"k{k}_outliers_removed"] = st.outliers_removed
     return out
 
 
