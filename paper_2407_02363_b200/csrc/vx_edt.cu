@@ -704,8 +704,8 @@ __global__ void __launch_bounds__(kColThreads, kColMinBlocks) k_column_smem(cons
 // TMA-staged variant (narrow 32-bit codes, nz % 4 == 0): one elected thread
 // issues the bulk tensor loads of the whole 32-column tile into the stack
 // region; every row of the column is in flight at once.
-template <int PASS, bool FW, bool SCAT, bool CMP>
-__global__ void __launch_bounds__(kColThreads, kColMinBlocks) k_column_tma(const __grid_constant__ CUtensorMap tmap,
+template <int PASS, bool FW, bool SCAT, bool CMP, int MAXT>
+__global__ void __launch_bounds__(MAXT, MAXT >= 1024 ? 1 : kColMinBlocks) k_column_tma(const __grid_constant__ CUtensorMap tmap,
                                                      const __grid_constant__ CUtensorMap tmap1,
                                                      const typename Col<PASS, false, false, FW>::InT *__restrict__ in,
                                                      typename Col<PASS, false, false, FW>::OutT *__restrict__ out,
@@ -909,7 +909,12 @@ cudaError_t launch_col(const void *in, void *out, void *gstack, const EdtPlan &p
                 (!cmp || make_tmap(&m1, in, p, PASS, nouter, nyl, 1))) {
                 if (!cmp) m1 = m;
                 const size_t smem = PASS == 2 ? p.smem2 : p.smem3;
-                auto kern = cmp ? k_column_tma<PASS, FW, SCAT, true> : k_column_tma<PASS, FW, SCAT, false>;
+                // long columns (L > 512) take 32 bands = 1024 threads: their tile
+                // already fills an SM's shared memory, so one CTA per SM anyway
+                auto kern = P.B > kMaxBands
+                                ? (cmp ? k_column_tma<PASS, FW, SCAT, true, 1024> : k_column_tma<PASS, FW, SCAT, false, 1024>)
+                                : (cmp ? k_column_tma<PASS, FW, SCAT, true, kColThreads>
+                                       : k_column_tma<PASS, FW, SCAT, false, kColThreads>);
                 cudaError_t e = allow_smem(kern);
                 if (e != cudaSuccess) return e;
                 kern<<<(unsigned)P.ntiles, block, smem, st>>>(m, m1, reinterpret_cast<const typename C::InT *>(in),
@@ -918,7 +923,7 @@ cudaError_t launch_col(const void *in, void *out, void *gstack, const EdtPlan &p
             }
         }
     }
-    if (P.xs) return cudaErrorNotSupported;   // compact rows need the TMA-staged kernel
+    if (P.xs || P.B > kMaxBands) return cudaErrorNotSupported;   // TMA-staged kernel only
     P.rows_alloc = P.L;
     if (!gs) {
         const size_t smem = (size_t)P.L * 32 * sizeof(typename C::EntT) + (size_t)(3 * P.B * 32 + 32) * 4;
@@ -1017,8 +1022,19 @@ bool make_plan(int nx, int ny, int nz, EdtPlan *p, int force_global_stack) {
     const size_t sb2 = staged_bytes(ny, q.B2), sb3 = staged_bytes(nx, q.B3);
     q.tma2 = tma_ok && !q.s2_wide && !q.gstack2 && sb2 <= kSmemLimit;
     q.tma3 = tma_ok && !q.s2_wide && !q.e3_wide && !q.gstack3 && sb3 <= kSmemLimit;
+    // TMA-staged long columns: up to 32 bands (the 1024-thread kernel)
+    auto widen = [&](int L, bool tma, int &B, int &W, size_t &smem) {
+        if (!tma || L <= 512) return;
+        const int B32 = std::min(32, pow2ceil((L + VX_BAND_ROWS - 1) / VX_BAND_ROWS));
+        if (B32 <= B || staged_bytes(L, B32) > kSmemLimit) return;
+        B = B32;
+        W = (L + B - 1) / B;
+        smem = staged_bytes(L, B);
+    };
     if (q.tma2) q.smem2 = sb2;
     if (q.tma3) q.smem3 = sb3;
+    widen(ny, q.tma2, q.B2, q.W2, q.smem2);
+    widen(nx, q.tma3, q.B3, q.W3, q.smem3);
     q.gstack_ctas = 2 * num_sms();
     size_t gs = 0;
     if (q.gstack2) gs = std::max(gs, (size_t)q.gstack_ctas * st2);
