@@ -204,6 +204,23 @@ int vx_cycle_wait(vx_cycle *c, vx_cycle_result *res, int32_t *site_lin /* 2*s */
 int vx_cycle_use_graph(vx_cycle *c, int enable);
 int vx_cycle_profile(vx_cycle *c, int enable);
 int vx_cycle_phase_ms(vx_cycle *c, double *ms, int *nsteps);
+/* Avoidance rows on the device (tasks.py:88-123 _distance_rows, fused after
+ * the gather of every step with s == the configured sphere count).  Per
+ * sphere: radius, buffer (> 0), link index (< n_joints); kappa > 0;
+ * x_star_offset <= 0 means 2*buffer (tasks.py:63-73).  Re-configuring drops
+ * the captured graph; s = 0 disables. */
+int vx_cycle_set_avoidance(vx_cycle *c, int s, const double *radius, const double *buffer,
+                           const int32_t *link_index, int n_joints, double kappa,
+                           double x_star_offset);
+/* joint frames at this step's q (robot.py:545-558): n_joints world origins
+ * and axes, each n_joints*3 row-major; set before vx_cycle_step */
+int vx_cycle_set_joint_frames(vx_cycle *c, const double *origins, const double *axes);
+/* rows of the last step, env then self (2*s rows): J (2*s x n_joints),
+ * activation, xdot_ref, value (|O - C|, inf when no site), flag (0 no site /
+ * inert row, 1 built, 2 x <= 1e-12: activation 1, J zero -- the caller
+ * applies its held direction, tasks.py:111-119).  Any output may be NULL. */
+int vx_cycle_rows(vx_cycle *c, double *J, double *activation, double *xdot_ref, double *value,
+                  int32_t *flag);
 /* fields of the last step (owned by the cycle; do not destroy) */
 int vx_cycle_fields(vx_cycle *c, vx_field **env, vx_field **self_field);
 int vx_cycle_grids(vx_cycle *c, vx_grid **env, vx_grid **self_grid, vx_grid **mask);

@@ -769,6 +769,14 @@ struct vx_cycle {
     double *d_world = nullptr, *d_dist = nullptr;
     void *scratch = nullptr;
     size_t scratch_bytes = 0;
+    // K7 avoidance rows (tasks.py:88-123), enabled by vx_cycle_set_avoidance
+    int av_s = 0, av_nj = 0;
+    double av_kappa = 0.0, av_offset = -1.0;
+    double *d_av_par = nullptr;   // radius[s], buffer[s]
+    int *d_av_link = nullptr;
+    double *d_frames = nullptr, *h_frames = nullptr;   // origins[nj*3], axes[nj*3] (pinned)
+    double *d_J = nullptr, *d_act = nullptr, *d_ref = nullptr, *d_val = nullptr;
+    int *d_flag = nullptr;
     EdtPlan plan{};
     std::vector<double> last_self_T;
     bool self_valid = false;
@@ -793,6 +801,8 @@ struct vx_cycle {
         if (profiling && ring_n < kRing) cudaEventRecord(ev[ring_n][phase], ctx->stream);
     }
 };
+
+static void av_free(vx_cycle *cy);
 
 extern "C" int vx_cycle_create(vx_ctx *c, int nx, int ny, int nz, double vs, const double origin[3],
                                int nlinks, const int32_t *const *link_ijk, const int64_t *link_counts,
@@ -894,6 +904,7 @@ extern "C" int vx_cycle_destroy(vx_cycle *cy) {
     cudaFree(cy->d_lin);
     cudaFree(cy->d_world);
     cudaFree(cy->d_dist);
+    av_free(cy);
     cudaFree(cy->d_npts);
     if (cy->h_npts) cudaFreeHost(cy->h_npts);
     if (cy->gexec) cudaGraphExecDestroy(cy->gexec);
@@ -960,6 +971,14 @@ static int cycle_main_seq(vx_cycle *cy, const double *d_pts, long long npts, con
                               cy->d_dist + s, st);
     if (e != cudaSuccess) return cuda_fail(e, "site_world");
     c->launches += s ? 2 : 0;
+    if (cy->av_s && s == cy->av_s) {
+        e = launch_avoidance_rows(cy->d_world, cy->d_dist, cy->d_lin, cy->d_centers, s, cy->d_av_par,
+                                  cy->d_av_par + s, cy->d_av_link, cy->d_frames, cy->d_frames + 3 * cy->av_nj,
+                                  cy->av_nj, cy->av_kappa, cy->av_offset, cy->d_J, cy->d_act, cy->d_ref,
+                                  cy->d_val, cy->d_flag, st);
+        if (e != cudaSuccess) return cuda_fail(e, "avoidance_rows");
+        c->launches += 1;
+    }
     if (marks) cy->mark(8);
     return VX_OK;
 }
@@ -985,6 +1004,8 @@ static int cycle_step(vx_cycle *cy, const double *pts, const double *d_pts_in, i
     const double *d_pts = d_pts_in ? d_pts_in : cy->d_pts;
     if (npts && !d_pts_in) VX_CUDA(cudaMemcpyAsync(cy->d_pts, pts, (size_t)npts * 24, cudaMemcpyHostToDevice, st));
     if (s) VX_CUDA(cudaMemcpyAsync(cy->d_centers, centers, (size_t)s * 24, cudaMemcpyHostToDevice, st));
+    if (cy->av_s && s == cy->av_s)
+        VX_CUDA(cudaMemcpyAsync(cy->d_frames, cy->h_frames, (size_t)cy->av_nj * 48, cudaMemcpyHostToDevice, st));
     cy->mark(1);
     // self map: memo on the self-obstacle transforms (engine.py:259-268 skips
     // the EDT when the occupancy is unchanged; equal transforms => equal
@@ -1097,6 +1118,89 @@ extern "C" int vx_cycle_wait(vx_cycle *cy, vx_cycle_result *res, int32_t *lin, d
         res->stats = vx_insert_stats{(int64_t)h.inserted, 0, (int64_t)h.skipped, (int64_t)h.oob};
         res->self_recomputed = cy->self_recomputed;
     }
+    VX_CUDA(cudaStreamSynchronize(st));
+    return VX_OK;
+}
+
+static void av_free(vx_cycle *cy) {
+    cudaFree(cy->d_av_par);
+    cudaFree(cy->d_av_link);
+    cudaFree(cy->d_frames);
+    cudaFreeHost(cy->h_frames);
+    cudaFree(cy->d_J);
+    cudaFree(cy->d_act);
+    cudaFree(cy->d_ref);
+    cudaFree(cy->d_val);
+    cudaFree(cy->d_flag);
+    cy->d_av_par = cy->d_frames = cy->h_frames = cy->d_J = cy->d_act = cy->d_ref = cy->d_val = nullptr;
+    cy->d_av_link = cy->d_flag = nullptr;
+    cy->av_s = cy->av_nj = 0;
+}
+
+extern "C" int vx_cycle_set_avoidance(vx_cycle *cy, int s, const double *radius, const double *buffer,
+                                      const int32_t *link_index, int n_joints, double kappa,
+                                      double x_star_offset) {
+    if (!cy || s < 0 || s > cy->max_spheres || n_joints < 0 || (s && (!radius || !buffer || !link_index)))
+        return fail(VX_EINVAL, "bad argument (spheres %d of max %d, joints %d)", s,
+                    cy ? cy->max_spheres : 0, n_joints);
+    for (int q = 0; q < s; ++q) {
+        if (!(buffer[q] > 0)) return fail(VX_EINVAL, "buffer b must be > 0 (sphere %d)", q);
+        if (link_index[q] < 0 || link_index[q] >= n_joints)
+            return fail(VX_EINVAL, "link index %d out of range (sphere %d)", link_index[q], q);
+    }
+    if (!(kappa > 0)) return fail(VX_EINVAL, "kappa must be > 0");
+    cudaStream_t st = cy->ctx->stream;
+    VX_CUDA(cudaStreamSynchronize(st));
+    av_free(cy);
+    if (cy->gexec) cudaGraphExecDestroy(cy->gexec);
+    cy->gexec = nullptr;
+    if (!s) return VX_OK;
+    const int nj = n_joints > 0 ? n_joints : 1;
+    cudaError_t e = cudaMalloc(&cy->d_av_par, (size_t)2 * s * 8);
+    if (e == cudaSuccess) e = cudaMalloc(&cy->d_av_link, (size_t)s * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&cy->d_frames, (size_t)nj * 48);
+    if (e == cudaSuccess) e = cudaMallocHost(&cy->h_frames, (size_t)nj * 48);
+    if (e == cudaSuccess) e = cudaMalloc(&cy->d_J, (size_t)2 * s * nj * 8);
+    if (e == cudaSuccess) e = cudaMalloc(&cy->d_act, (size_t)2 * s * 8);
+    if (e == cudaSuccess) e = cudaMalloc(&cy->d_ref, (size_t)2 * s * 8);
+    if (e == cudaSuccess) e = cudaMalloc(&cy->d_val, (size_t)2 * s * 8);
+    if (e == cudaSuccess) e = cudaMalloc(&cy->d_flag, (size_t)2 * s * 4);
+    if (e != cudaSuccess) {
+        av_free(cy);
+        return cuda_fail(e, "cudaMalloc(avoidance)");
+    }
+    std::memset(cy->h_frames, 0, (size_t)nj * 48);
+    VX_CUDA(cudaMemcpy(cy->d_av_par, radius, (size_t)s * 8, cudaMemcpyHostToDevice));
+    VX_CUDA(cudaMemcpy(cy->d_av_par + s, buffer, (size_t)s * 8, cudaMemcpyHostToDevice));
+    VX_CUDA(cudaMemcpy(cy->d_av_link, link_index, (size_t)s * 4, cudaMemcpyHostToDevice));
+    cy->av_s = s;
+    cy->av_nj = n_joints;
+    cy->av_kappa = kappa;
+    cy->av_offset = x_star_offset > 0 ? x_star_offset : -1.0;
+    return VX_OK;
+}
+
+extern "C" int vx_cycle_set_joint_frames(vx_cycle *cy, const double *origins, const double *axes) {
+    if (!cy || !cy->av_s) return fail(VX_EINVAL, "avoidance rows not enabled (vx_cycle_set_avoidance)");
+    if (cy->av_nj && (!origins || !axes)) return fail(VX_EINVAL, "NULL joint frames");
+    // the previous step's H2D reads h_frames: wait for it before overwriting
+    VX_CUDA(cudaStreamSynchronize(cy->ctx->stream));
+    std::memcpy(cy->h_frames, origins, (size_t)cy->av_nj * 24);
+    std::memcpy(cy->h_frames + 3 * cy->av_nj, axes, (size_t)cy->av_nj * 24);
+    return VX_OK;
+}
+
+extern "C" int vx_cycle_rows(vx_cycle *cy, double *J, double *act, double *ref, double *val, int32_t *flag) {
+    if (!cy || !cy->av_s) return fail(VX_EINVAL, "avoidance rows not enabled (vx_cycle_set_avoidance)");
+    if (cy->last_s != cy->av_s)
+        return fail(VX_EINVAL, "last step had %d spheres, avoidance set for %d", cy->last_s, cy->av_s);
+    cudaStream_t st = cy->ctx->stream;
+    const size_t r = (size_t)2 * cy->av_s;
+    if (J && cy->av_nj) VX_CUDA(cudaMemcpyAsync(J, cy->d_J, r * cy->av_nj * 8, cudaMemcpyDeviceToHost, st));
+    if (act) VX_CUDA(cudaMemcpyAsync(act, cy->d_act, r * 8, cudaMemcpyDeviceToHost, st));
+    if (ref) VX_CUDA(cudaMemcpyAsync(ref, cy->d_ref, r * 8, cudaMemcpyDeviceToHost, st));
+    if (val) VX_CUDA(cudaMemcpyAsync(val, cy->d_val, r * 8, cudaMemcpyDeviceToHost, st));
+    if (flag) VX_CUDA(cudaMemcpyAsync(flag, cy->d_flag, r * 4, cudaMemcpyDeviceToHost, st));
     VX_CUDA(cudaStreamSynchronize(st));
     return VX_OK;
 }

@@ -117,6 +117,13 @@ cudaError_t launch_site_world(const int32_t *site, GridGeom g, const double *cen
                               int s, int32_t *out_lin, double *out_world, double *out_dist,
                               cudaStream_t st);
 
+// K7: obstacle / self avoidance rows from the K6 outputs of both maps
+cudaError_t launch_avoidance_rows(const double *world, const double *dist, const int32_t *lin,
+                                  const double *centers, int s, const double *radius, const double *buffer,
+                                  const int *link, const double *origins, const double *axes, int nj,
+                                  double kappa, double offset, double *J, double *act, double *ref,
+                                  double *val, int *flag, cudaStream_t st);
+
 int num_sms();
 
 }  // namespace vx

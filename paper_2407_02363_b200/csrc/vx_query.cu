@@ -67,3 +67,81 @@ cudaError_t launch_site_world(const int32_t *site, GridGeom g, const double *cen
 }
 
 }  // namespace vx
+
+// ---------------------------------------------------------------------------
+// K7: avoidance rows, the consumer of K6 fused on the
+// device: voxarm tasks.py:88-123 (_distance_rows) per sphere and map --
+//   x = |O - C|, act = activation_sigmoid(x, r, b) (tasks.py:21-32),
+//   ref = kappa * (r + offset - x), offset = cfg or 2b,
+//   J_row = (-(O - C)/x) . position_jacobian(q, link, C)   (robot.py:560-578:
+//   column j <= link is axis_j x (C - origin_j)).
+// flag: 0 no site (inert row), 1 row built, 2 x <= 1e-12 (the host applies
+// the held-direction rule of tasks.py:111-119).
+// ---------------------------------------------------------------------------
+namespace vx {
+namespace {
+
+__global__ void k_avoidance_rows(const double *__restrict__ world, const double *__restrict__ dist,
+                                 const int32_t *__restrict__ lin, const double *__restrict__ centers,
+                                 int s, const double *__restrict__ radius, const double *__restrict__ buffer,
+                                 const int *__restrict__ link, const double *__restrict__ origins,
+                                 const double *__restrict__ axes, int nj, double kappa, double offset,
+                                 double *__restrict__ J, double *__restrict__ act, double *__restrict__ ref,
+                                 double *__restrict__ val, int *__restrict__ flag) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;   // row = map * s + sphere
+    if (r >= 2 * s) return;
+    const int q = r % s;
+    double *Jr = J + (size_t)r * nj;
+    for (int j = 0; j < nj; ++j) Jr[j] = 0.0;
+    if (lin[r] < 0) {   // no site: inert row (tasks.py:100-101)
+        act[r] = 0.0;
+        ref[r] = 0.0;
+        val[r] = CUDART_INF;
+        flag[r] = 0;
+        return;
+    }
+    const double c[3] = {centers[3 * q], centers[3 * q + 1], centers[3 * q + 2]};
+    const double d[3] = {world[3 * r] - c[0], world[3 * r + 1] - c[1], world[3 * r + 2] - c[2]};
+    const double x = dist[r];
+    const double rad = radius[q], b = buffer[q];
+    val[r] = x;
+    double a;
+    if (x <= rad) a = 1.0;
+    else if (x >= rad + b) a = 0.0;
+    else a = 0.5 * (cos((x - rad) * CUDART_PI / b) + 1.0);
+    const double off = offset >= 0.0 ? offset : 2.0 * b;
+    ref[r] = kappa * (rad + off - x);
+    if (!(x > 1e-12)) {
+        act[r] = 1.0;
+        flag[r] = 2;
+        return;
+    }
+    act[r] = a;
+    flag[r] = 1;
+    const double u[3] = {-d[0] / x, -d[1] / x, -d[2] / x};
+    const int kmax = min(link[q] + 1, nj);
+    for (int j = 0; j < kmax; ++j) {
+        const double *o = origins + 3 * j, *ax = axes + 3 * j;
+        const double rx = c[0] - o[0], ry = c[1] - o[1], rz = c[2] - o[2];
+        const double cx = ax[1] * rz - ax[2] * ry;
+        const double cy = ax[2] * rx - ax[0] * rz;
+        const double cz = ax[0] * ry - ax[1] * rx;
+        Jr[j] = u[0] * cx + u[1] * cy + u[2] * cz;
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_avoidance_rows(const double *world, const double *dist, const int32_t *lin,
+                                  const double *centers, int s, const double *radius, const double *buffer,
+                                  const int *link, const double *origins, const double *axes, int nj,
+                                  double kappa, double offset, double *J, double *act, double *ref,
+                                  double *val, int *flag, cudaStream_t st) {
+    if (s <= 0) return cudaSuccess;
+    k_avoidance_rows<<<(2 * s + 63) / 64, 64, 0, st>>>(world, dist, lin, centers, s, radius, buffer, link,
+                                                      origins, axes, nj, kappa, offset, J, act, ref, val,
+                                                      flag);
+    return cudaGetLastError();
+}
+
+}  // namespace vx

@@ -118,6 +118,44 @@ class MapCycle:
                 "out_of_bounds": st.out_of_bounds, "self_recomputed": bool(res.self_recomputed),
                 "env": (lin[0], world[0], dist[0]), "self": (lin[1], world[1], dist[1])}
 
+    def set_avoidance(self, radius, buffer, link_index, n_joints: int, kappa: float,
+                      x_star_offset=None):
+        """Enable the on-device avoidance rows (tasks.py:88-123) for a fixed
+        sphere set: radius/buffer/link_index per sphere (robot.build_spheres),
+        n_joints = chain.n, AvoidanceConfig's kappa and x_star_offset (None
+        means 2*buffer).  Steps with exactly this many centres build them."""
+        r = np.ascontiguousarray(radius, dtype=np.float64).reshape(-1)
+        b = np.ascontiguousarray(buffer, dtype=np.float64).reshape(-1)
+        li = np.ascontiguousarray(link_index, dtype=np.int32).reshape(-1)
+        if not (r.size == b.size == li.size):
+            raise ValueError("radius, buffer and link_index lengths differ")
+        off = -1.0 if x_star_offset is None else float(x_star_offset)
+        _lib.check(_lib.load().vx_cycle_set_avoidance(self._h, r.size, _lib.ptr(r), _lib.ptr(b),
+                                                      _lib.ptr(li), int(n_joints), float(kappa), off))
+        self._av = (r.size, int(n_joints))
+
+    def set_joint_frames(self, origins, axes):
+        """chain.joint_frames(q) of the next step (robot.py:545-558)."""
+        o = np.ascontiguousarray(origins, dtype=np.float64).reshape(-1, 3)
+        a = np.ascontiguousarray(axes, dtype=np.float64).reshape(-1, 3)
+        _lib.check(_lib.load().vx_cycle_set_joint_frames(self._h, _lib.ptr(o), _lib.ptr(a)))
+
+    def rows(self):
+        """Avoidance rows of the last step per map ("env", "self"): dict of
+        J (s, n), activation, xdot_ref, value (s,) and flag (s,) -- 0 no site,
+        1 built, 2 zero distance (activation 1, J zero: the caller applies
+        its held direction, tasks.py:111-119)."""
+        s, n = self._av
+        J = np.zeros((2, s, n), np.float64)
+        act = np.empty((2, s), np.float64)
+        ref = np.empty((2, s), np.float64)
+        val = np.empty((2, s), np.float64)
+        flag = np.empty((2, s), np.int32)
+        _lib.check(_lib.load().vx_cycle_rows(self._h, _lib.ptr(J), _lib.ptr(act), _lib.ptr(ref),
+                                             _lib.ptr(val), _lib.ptr(flag)))
+        return {k: {"J": J[m], "activation": act[m], "xdot_ref": ref[m], "value": val[m],
+                    "flag": flag[m]} for m, k in enumerate(("env", "self"))}
+
     def fields(self):
         e, s = ctypes.c_void_p(), ctypes.c_void_p()
         _lib.check(_lib.load().vx_cycle_fields(self._h, ctypes.byref(e), ctypes.byref(s)))
