@@ -112,6 +112,12 @@ int vx_grid_read_cells(vx_grid *g, float *host_out);           /* .cells */
 int vx_grid_write_cells(vx_grid *g, const float *host_in);     /* .cells[...] = */
 /* VoxelGrid.occupancy_mask (grids.py:207-208) as uint8 0/1 */
 int vx_grid_occupancy(vx_grid *g, double threshold, uint8_t *host_out);
+/* VoxelGrid.occupied_voxels (grids.py:210-212): np.argwhere of the mask,
+ * (count,3) int64 in lexicographic order, compacted on the device.
+ * host_out == NULL returns the count only; capacity (rows) < count fails
+ * with VX_ERANGE and still sets *count. */
+int vx_grid_occupied_voxels(vx_grid *g, double threshold, int64_t *host_out, int64_t capacity,
+                            int64_t *count);
 
 /* ---- edt (edt.py) --------------------------------------------------------- */
 /* pba_edt (edt.py:466-484) of a host occupancy array (any nonzero byte is
@@ -128,6 +134,13 @@ int vx_field_dims(const vx_field *f, int dims[3]);
 /* DistanceField.site (edt.py:106-111) */
 int vx_field_read_site(vx_field *f, int32_t *host_out);
 /* DistanceField.site[i,j,k]; VX_ERANGE outside the grid (edt.py:155-156) */
+/* DistanceField.sq_distance_grid (edt.py:123-135): int64 squared voxel
+ * distance, -1 where there is no site; out is host or (out_on_device) device */
+int vx_field_sq_distance(vx_field *f, int64_t *out, int out_on_device);
+/* DistanceField.dump_squared (edt.py:137-145): the golden text, formatted on
+ * the device.  buf == NULL returns the byte count only; capacity < count
+ * fails with VX_ERANGE and still sets *nbytes.  No terminating NUL. */
+int vx_field_dump_squared(vx_field *f, char *buf, int64_t capacity, int64_t *nbytes);
 int vx_field_site_at(vx_field *f, int64_t i, int64_t j, int64_t k, int32_t *out);
 /* SimEngine._site_world (engine.py:212-221) for s centres, plus the
  * distance of tasks.py:102-104.  site_lin[q] = -1 (world NaN, dist +inf)

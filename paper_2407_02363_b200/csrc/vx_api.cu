@@ -71,7 +71,7 @@ constexpr float kOccThr = 0.0f;  // float32(logit(0.5)): the cached occupancy th
 struct vx_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
-    DevBuf scratch, staging, staging2, temp, outl;
+    DevBuf scratch, staging, staging2, temp, outl, exp, exp_out;
     long long launches = 0;
 };
 
@@ -135,6 +135,8 @@ extern "C" int vx_ctx_destroy(vx_ctx *c) {
     c->staging.release();
     c->staging2.release();
     c->temp.release();
+    c->exp.release();
+    c->exp_out.release();
     c->outl.release();
     cudaStreamDestroy(c->stream);
     delete c;
@@ -495,6 +497,35 @@ extern "C" int vx_grid_occupancy(vx_grid *g, double thr, uint8_t *out) {
     return VX_OK;
 }
 
+// grids.py:210-212: np.argwhere(occupancy_mask) -- (K,3) int64, flat-index
+// order.  host_out == NULL (or too small): *count only (VX_ERANGE if short).
+extern "C" int vx_grid_occupied_voxels(vx_grid *g, double thr, int64_t *host_out, int64_t capacity,
+                                       int64_t *count) {
+    if (!g || !count) return fail(VX_EINVAL, "NULL argument");
+    vx_ctx *c = g->ctx;
+    const uint8_t *d = nullptr;
+    int rc = grid_occ_device(g, thr, &d);
+    if (rc) return rc;
+    VX_CUDA(c->exp.ensure(occ_scratch_bytes(g->n)));
+    cudaError_t e = launch_occ_layout(d, g->n, c->exp.p, c->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "occupied_voxels");
+    c->launches += 2;
+    long long total = 0;
+    VX_CUDA(cudaMemcpyAsync(&total, occ_total_ptr(c->exp.p, g->n), 8, cudaMemcpyDeviceToHost, c->stream));
+    VX_CUDA(cudaStreamSynchronize(c->stream));
+    *count = total;
+    if (!host_out) return VX_OK;
+    if (capacity < total) return fail(VX_ERANGE, "capacity %lld < %lld occupied voxels", (long long)capacity, total);
+    if (!total) return VX_OK;
+    VX_CUDA(c->exp_out.ensure((size_t)total * 24));
+    e = launch_occ_write(d, g->n, g->g.ny, g->g.nz, c->exp.p, (long long *)c->exp_out.p, c->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "occupied_voxels");
+    c->launches += 1;
+    VX_CUDA(cudaMemcpyAsync(host_out, c->exp_out.p, (size_t)total * 24, cudaMemcpyDeviceToHost, c->stream));
+    VX_CUDA(cudaStreamSynchronize(c->stream));
+    return VX_OK;
+}
+
 // ---- EDT ----------------------------------------------------------------------
 static int check_edt_dims(int nx, int ny, int nz) {
     if (nx <= 0 || ny <= 0 || nz <= 0) return fail(VX_EINVAL, "occupancy must be a non-empty 3D array");
@@ -615,6 +646,50 @@ extern "C" int vx_field_read_site(vx_field *f, int32_t *out) {
     const size_t n = (size_t)f->nx * f->ny * f->nz;
     VX_CUDA(cudaMemcpyAsync(out, f->site, n * 4, cudaMemcpyDeviceToHost, f->ctx->stream));
     VX_CUDA(cudaStreamSynchronize(f->ctx->stream));
+    return VX_OK;
+}
+
+// edt.py:123-135: squared voxel distance, int64, -1 where there is no site
+extern "C" int vx_field_sq_distance(vx_field *f, int64_t *out, int out_on_device) {
+    if (!f || !out) return fail(VX_EINVAL, "NULL argument");
+    vx_ctx *c = f->ctx;
+    const size_t n = (size_t)f->nx * f->ny * f->nz;
+    long long *d = (long long *)out;
+    if (!out_on_device) {
+        VX_CUDA(c->exp_out.ensure(n * 8));
+        d = (long long *)c->exp_out.p;
+    }
+    cudaError_t e = launch_sq_distance(f->site, f->nx, f->ny, f->nz, d, c->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "sq_distance");
+    c->launches += 1;
+    if (!out_on_device) VX_CUDA(cudaMemcpyAsync(out, d, n * 8, cudaMemcpyDeviceToHost, c->stream));
+    VX_CUDA(cudaStreamSynchronize(c->stream));
+    return VX_OK;
+}
+
+// edt.py:137-145: the golden text of dump_squared.  buf == NULL (or too
+// small): *nbytes only (VX_ERANGE if short).  No terminating NUL.
+extern "C" int vx_field_dump_squared(vx_field *f, char *buf, int64_t capacity, int64_t *nbytes) {
+    if (!f || !nbytes) return fail(VX_EINVAL, "NULL argument");
+    if (f->ny > 65535) return fail(VX_EINVAL, "dump_squared: ny %d > 65535", f->ny);
+    vx_ctx *c = f->ctx;
+    VX_CUDA(c->exp.ensure(dump_scratch_bytes(f->ny, f->nz)));
+    cudaError_t e = launch_dump_layout(f->site, f->nx, f->ny, f->nz, c->exp.p, c->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "dump_squared");
+    c->launches += 2;
+    long long total = 0;
+    VX_CUDA(cudaMemcpyAsync(&total, dump_total_ptr(c->exp.p, f->ny, f->nz), 8, cudaMemcpyDeviceToHost,
+                            c->stream));
+    VX_CUDA(cudaStreamSynchronize(c->stream));
+    *nbytes = total;
+    if (!buf) return VX_OK;
+    if (capacity < total) return fail(VX_ERANGE, "capacity %lld < %lld bytes", (long long)capacity, total);
+    VX_CUDA(c->exp_out.ensure((size_t)total));
+    e = launch_dump_write(f->site, f->nx, f->ny, f->nz, c->exp.p, (char *)c->exp_out.p, c->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "dump_squared");
+    c->launches += 1;
+    VX_CUDA(cudaMemcpyAsync(buf, c->exp_out.p, (size_t)total, cudaMemcpyDeviceToHost, c->stream));
+    VX_CUDA(cudaStreamSynchronize(c->stream));
     return VX_OK;
 }
 

@@ -124,6 +124,19 @@ cudaError_t launch_avoidance_rows(const double *world, const double *dist, const
                                   double kappa, double offset, double *J, double *act, double *ref,
                                   double *val, int *flag, cudaStream_t st);
 
+// export formats (vx_export.cu)
+cudaError_t launch_sq_distance(const int32_t *site, int nx, int ny, int nz, long long *out, cudaStream_t st);
+size_t dump_scratch_bytes(int ny, int nz);
+cudaError_t launch_dump_layout(const int32_t *site, int nx, int ny, int nz, void *scratch, cudaStream_t st);
+const long long *dump_total_ptr(void *scratch, int ny, int nz);
+cudaError_t launch_dump_write(const int32_t *site, int nx, int ny, int nz, const void *scratch, char *out,
+                              cudaStream_t st);
+size_t occ_scratch_bytes(long long n);
+cudaError_t launch_occ_layout(const uint8_t *occ, long long n, void *scratch, cudaStream_t st);
+const long long *occ_total_ptr(void *scratch, long long n);
+cudaError_t launch_occ_write(const uint8_t *occ, long long n, int ny, int nz, const void *scratch,
+                             long long *out, cudaStream_t st);
+
 int num_sms();
 
 }  // namespace vx

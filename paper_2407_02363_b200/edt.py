@@ -133,8 +133,18 @@ class DistanceField:
             return None
         return lin // (ny * nz), (lin // nz) % ny, lin % nz
 
+    def _device_only(self) -> bool:
+        # the host copy, once materialised, may have been edited in place:
+        # from then on it is the source of truth (as _site_lin treats it)
+        return self._site is None and self._handle is not None
+
     def sq_distance_grid(self) -> np.ndarray:
-        """edt.py:123-135 (export format; int64, -1 where there is no site)."""
+        """edt.py:123-135 (export format; int64, -1 where there is no site).
+        Computed on the device (vx_field_sq_distance) for a device field."""
+        if self._device_only():
+            out = np.empty(self.dims, np.int64)
+            _lib.check(_lib.load().vx_field_sq_distance(self._handle, _lib.ptr(out), 0))
+            return out
         _, ny, nz = self.dims
         flat = self.site.reshape(-1).astype(np.int64)
         out = np.full(flat.shape, -1, dtype=np.int64)
@@ -148,7 +158,16 @@ class DistanceField:
         return out.reshape(self.dims)
 
     def dump_squared(self, stream) -> None:
-        """edt.py:137-145 (golden-file text format)."""
+        """edt.py:137-145 (golden-file text format).  A device field is
+        formatted on the device (vx_field_dump_squared) and written once."""
+        if self._device_only():
+            L = _lib.load()
+            n = ctypes.c_int64()
+            _lib.check(L.vx_field_dump_squared(self._handle, None, 0, ctypes.byref(n)))
+            buf = ctypes.create_string_buffer(max(1, n.value))
+            _lib.check(L.vx_field_dump_squared(self._handle, buf, n.value, ctypes.byref(n)))
+            stream.write(buf.raw[:n.value].decode("ascii"))
+            return
         sq = self.sq_distance_grid()
         nx, ny, nz = self.dims
         for k in range(nz):

@@ -258,7 +258,17 @@ class VoxelGrid:
         return out.view(np.bool_)
 
     def occupied_voxels(self, threshold: float = DEFAULT_OCCUPANCY_THRESHOLD) -> np.ndarray:
-        return np.argwhere(self.occupancy_mask(threshold))
+        """grids.py:210-212: np.argwhere(occupancy_mask), compacted on the
+        device in lexicographic order ((K,3) int64)."""
+        self._push()
+        L = _lib.load()
+        n = ctypes.c_int64()
+        _lib.check(L.vx_grid_occupied_voxels(self._h, float(threshold), None, 0, ctypes.byref(n)))
+        out = np.empty((n.value, 3), np.int64)
+        if n.value:
+            _lib.check(L.vx_grid_occupied_voxels(self._h, float(threshold), _lib.ptr(out), n.value,
+                                                 ctypes.byref(n)))
+        return out
 
     def same_geometry(self, other: "VoxelGrid") -> bool:
         return (self.dims == other.dims
