@@ -1014,7 +1014,8 @@ static cudaError_t edt_passes(vx_cycle *cy, const uint8_t *occ, int32_t *site, b
     if (marks) cy->mark(5);
     if (e == cudaSuccess) e = launch_pass2(s1, s2, gs, p, p.nx, st, sparse ? &sp : nullptr);
     if (marks) cy->mark(6);
-    if (e == cudaSuccess) e = launch_pass3(s2, site, gs, p, 1, 0, p.ny, st, sparse ? &sp : nullptr);
+    // sparse path: s1 is dead by pass 3 and is the spill slab of its column stacks
+    if (e == cudaSuccess) e = launch_pass3(s2, site, sparse ? (void *)s1 : gs, p, 1, 0, p.ny, st, sparse ? &sp : nullptr);
     if (marks) cy->mark(7);
     cy->ctx->launches += 3;
     return e;

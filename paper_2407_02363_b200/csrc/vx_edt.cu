@@ -51,8 +51,14 @@ __device__ unsigned long long *g_phase_buf = nullptr;
         if (threadIdx.x == 0 && threadIdx.y == 0 && g_phase_buf)                       \
             g_phase_buf[(size_t)blockIdx.x * 8 + (i)] = clock64();                     \
     } while (0)
+#define VX_PTW(slot, i)                                                                \
+    do {                                                                               \
+        if ((threadIdx.x & 31) == 0 && g_phase_buf)                                   \
+            g_phase_buf[(size_t)(slot) * 8 + (i)] = clock64();                         \
+    } while (0)
 #else
 #define VX_PT(i) do {} while (0)
+#define VX_PTW(slot, i) do {} while (0)
 #endif
 // column passes: at most 16 bands (512 threads) per CTA, 3 CTAs per SM
 #ifndef VX_MAX_BANDS
@@ -69,6 +75,13 @@ constexpr bool kP3XW = VX_P3_XW != 0;
 #ifndef VX_CMP_GROUP_ROWS
 #define VX_CMP_GROUP_ROWS 24   // target candidates per group in compact pass 3
 #endif
+#ifndef VX_STREAM_CAP
+#define VX_STREAM_CAP 48   // shared-memory stack entries per column (k_pass3_stream)
+#endif
+#ifndef VX_STREAM_MAX_ROWS
+#define VX_STREAM_MAX_ROWS 256   // occupied slices up to which pass 3 runs one warp per tile
+#endif
+constexpr int kStreamMaxRows = VX_STREAM_MAX_ROWS;
 #ifndef VX_BAND_ROWS
 #define VX_BAND_ROWS 32   // target rows per band
 #endif
@@ -235,6 +248,7 @@ struct ColParams {
     const uint8_t *sflag;  // per slice: any occupied voxel (nullptr = dense)
     const int *xs;         // occupied slice indices, ascending
     const int *hdr;        // hdr[0] = number of occupied slices (device-side)
+    int stream_max;        // pass 3: k_pass3_stream takes m <= stream_max (-1: never)
 };
 
 template <int PASS, bool S2W, bool EW, bool FW>
@@ -727,6 +741,7 @@ __global__ void __launch_bounds__(MAXT, MAXT >= 1024 ? 1 : kColMinBlocks) k_colu
         // rows of occupied slices only (slot t <- row xs[t]); when every slice
         // is occupied the plain box loads below are used instead
         const int m = __ldg(P.hdr);
+        if (m <= P.stream_max) return;   // k_pass3_stream did this pass
         all_rows = m == P.L;
         if (!all_rows) {
             const int scene = (int)(outer / P.nyl);
@@ -786,6 +801,170 @@ __global__ void __launch_bounds__(kColThreads, kColMinBlocks) k_column_gstack(co
     }
 }
 
+constexpr int kWarpCtaThreads = 1024;
+
+// ---- pass 3 with one warp per tile (few occupied slices) ----------------------
+// A warp owns a whole 32-column tile: the m candidate rows (occupied slices,
+// read on the device) stream through registers as 128-byte LDG rows, 8 in
+// flight; the 32 column hulls are built in one sequential sweep (edt.py:253-276
+// with no bands and no merges) and all L query rows are walked (edt.py:300-
+// 317).  Only the hulls live in shared memory: the first kStreamCap entries of
+// every column stack, the rest spill to a per-warp slab of global scratch
+// (rare: hulls are short when few slices are occupied).  No CTA barrier: 32
+// independent warps per SM.  Stack entry (x << yzb) | (y << zb | z): the output
+// site needs no re-read; F = x^2 + (j - y)^2 + (k - z)^2.
+// Runs when m <= P.stream_max; otherwise it exits and the banded
+// k_column_tma (launched right after it) does the pass.
+constexpr int kStreamCap = VX_STREAM_CAP;
+
+template <typename FT, bool CMP>
+__global__ void __launch_bounds__(kWarpCtaThreads, 1) k_pass3_stream(const uint32_t *__restrict__ in,
+                                                                     int32_t *__restrict__ out,
+                                                                     uint32_t *__restrict__ ovf, const ColParams P) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    int m = P.L;
+    bool all_rows = true;
+    if constexpr (CMP) {
+        m = __ldg(P.hdr);
+        if (m > P.stream_max) return;
+        all_rows = m == P.L;
+    }
+    uint32_t *sst = reinterpret_cast<uint32_t *>(smem) + (size_t)w * kStreamCap * 32 + lane;
+    const long long gw = (long long)blockIdx.x * nw + w;
+    uint32_t *gst = ovf + gw * (long long)max(P.L - kStreamCap, 0) * 32 + lane - (long long)kStreamCap * 32;
+    // shared entries stay LDS/STS (no generic-pointer select); spills bypass L1
+    auto ent = [&](int i) -> uint32_t { return i < kStreamCap ? sst[i * 32] : gst[(long long)i * 32]; };
+    auto put = [&](int i, uint32_t e) {
+        if (i < kStreamCap) sst[i * 32] = e;
+        else gst[(long long)i * 32] = e;
+    };
+    const uint32_t yzb = (uint32_t)P.yzb, zb = (uint32_t)P.zb, zmask = P.zmask, ymask = P.ymask;
+    constexpr FT kNever = sizeof(FT) == 4 ? (FT)0x7fffffff : (FT)0x7fffffffffffffffLL;
+    const long long step = (long long)gridDim.x * nw;
+    for (long long tile = gw; tile < P.ntiles; tile += step) {
+        const int kt = (int)(tile % P.nkt);
+        const long long outer = tile / P.nkt;
+        const int scene = (int)(outer / P.nyl);
+        const int jl = (int)(outer - (long long)scene * P.nyl);
+        const int jq = P.j0 + jl;
+        const int k = kt * 32 + lane;
+        if (k >= P.nz) continue;   // lanes only; no warp-wide sync below
+        const long long base = (long long)scene * P.nvox + (long long)jl * P.nz + k;
+        const uint32_t *src = in + base;
+        VX_PTW(tile, 0);
+        VX_PTW(tile, 1);
+        auto Fof = [&](uint32_t e) -> FT {
+            const int x = (int)(e >> yzb), sy = (int)((e >> zb) & ymask), sz = (int)(e & zmask);
+            const FT dy = (FT)(jq - sy), dz = (FT)(k - sz);
+            return dy * dy + dz * dz + (FT)x * (FT)x;
+        };
+        int n = 0, ya = 0, yb = 0;
+        FT Fa = 0, Fb = 0;
+        auto consume = [&](uint32_t v, int yc) {
+            if (v == 0xffffffffu) return;
+            const uint32_t ec = ((uint32_t)yc << yzb) | v;
+            const FT Fc = Fof(ec);
+            while (n >= 2 && dominated<FT>(ya, Fa, yb, Fb, yc, Fc)) {
+                --n;
+                yb = ya;
+                Fb = Fa;
+                if (n >= 2) {
+                    const uint32_t e = ent(n - 2);
+                    ya = (int)(e >> yzb);
+                    Fa = Fof(e);
+                }
+            }
+            put(n, ec);
+            ya = yb;
+            Fa = Fb;
+            yb = yc;
+            Fb = Fc;
+            ++n;
+        };
+        constexpr int U = 8;
+        for (int t0 = 0; t0 < m; t0 += U) {
+            uint32_t v[U];
+            int yr[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int t = t0 + u;
+                yr[u] = t < m ? (all_rows ? t : __ldg(P.xs + t)) : 0;
+                v[u] = t < m ? __ldg(src + (long long)yr[u] * P.splane) : 0xffffffffu;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) consume(v[u], yr[u]);
+        }
+#ifdef VX_PHASE_TIMING
+        {   // hull size (max over the warp's columns) for tools/phase_timing
+            int hmax = n;
+            const unsigned am = __activemask();
+            for (int d = 16; d; d >>= 1) hmax = max(hmax, __shfl_xor_sync(am, hmax, d));
+            if (lane == __ffs(am) - 1 && g_phase_buf) g_phase_buf[(size_t)tile * 8 + 7] = (unsigned long long)hmax;
+        }
+#endif
+        VX_PTW(tile, 2);
+        // ---- queries: first minimiser at every row, stepped walk
+        // 32-bit row offsets: nx * ny * nz < 2^31 (int32 sites)
+        int32_t *dst = out + base;
+        const uint32_t ostep = (uint32_t)P.splane;
+        uint32_t off = 0;
+        if (n == 0) {
+            for (int y = 0; y < P.L; ++y, off += ostep) dst[off] = -1;
+        } else {
+            int pos = 0;
+            uint32_t cur = ent(0);
+            int yc = (int)(cur >> yzb);
+            FT Fc = Fof(cur);
+            auto site_of = [&](uint32_t e) -> int32_t {
+                const long long x = (long long)(e >> yzb), sy = (long long)((e >> zb) & ymask);
+                return (int32_t)(x * P.plane + sy * P.nz + (long long)(e & zmask));   // edt.py:417
+            };
+            int32_t ocur = site_of(cur);
+            bool has = n > 1;
+            uint32_t sent = 0;
+            int ys = 0;
+            FT Fs = 0;
+            if (has) {
+                sent = ent(1);
+                ys = (int)(sent >> yzb);
+                Fs = Fof(sent);
+            }
+            FT dN = has ? Fs - Fc : kNever;
+            FT tt = has ? (FT)2 * (FT)(ys - yc) : (FT)0;
+            FT rhs = 0;
+#pragma unroll 4
+            for (int y = 0; y < P.L; ++y) {
+                if (dN < rhs) {   // successor strictly closer at row y (edt.py:311)
+                    do {
+                        cur = sent;
+                        yc = ys;
+                        Fc = Fs;
+                        ++pos;
+                        has = pos + 1 < n;
+                        if (has) {
+                            sent = ent(pos + 1);
+                            ys = (int)(sent >> yzb);
+                            Fs = Fof(sent);
+                        }
+                    } while (has && better<FT>(ys, Fs, yc, Fc, y));
+                    ocur = site_of(cur);
+                    dN = has ? Fs - Fc : kNever;
+                    tt = has ? (FT)2 * (FT)(ys - yc) : (FT)0;
+                    rhs = (FT)y * tt;
+                }
+                dst[off] = ocur;
+                off += ostep;
+                rhs += tt;
+            }
+        }
+        VX_PTW(tile, 3);
+        VX_PTW(tile, 4);
+        VX_PTW(tile, 5);
+        VX_PTW(tile, 6);
+    }
+}
+
 int bits_of(long long v) {  // bits to hold values 0..v
     int b = 0;
     while (v > 0) { ++b; v >>= 1; }
@@ -824,6 +1003,7 @@ ColParams col_params(const EdtPlan &p, int pass, long long nouter, int nyl, int 
     P.sflag = nullptr;
     P.xs = nullptr;
     P.hdr = nullptr;
+    P.stream_max = -1;
     P.boxh = std::min(P.L, 256);
     P.rows_alloc = (P.L + P.boxh - 1) / P.boxh * P.boxh;
     return P;
@@ -908,6 +1088,27 @@ cudaError_t launch_col(const void *in, void *out, void *gstack, const EdtPlan &p
             if (make_tmap(&m, in, p, PASS, nouter, nyl, P.boxh) &&
                 (!cmp || make_tmap(&m1, in, p, PASS, nouter, nyl, 1))) {
                 if (!cmp) m1 = m;
+                if constexpr (PASS == 3 && !SCAT) {
+                    // few occupied slices: one warp per tile (k_pass3_stream) when
+                    // m <= stream_max, decided on the device; s1 (gstack here) is
+                    // its spill slab
+                    const long long spill = std::min<long long>(P.ntiles, (long long)num_sms() * 32) *
+                                            std::max(P.L - kStreamCap, 0) * 32 * 4;
+                    if (cmp && gstack && p.xb + p.yb + p.zb <= 32 && spill <= (long long)p.s1_bytes) {
+                        const char *sm = getenv("VX_STREAM_MAX");
+                        P.stream_max = sm ? atoi(sm) : kStreamMaxRows;
+                        auto kern = k_pass3_stream<typename C::FT, true>;
+                        cudaError_t e = allow_smem(kern);
+                        if (e != cudaSuccess) return e;
+                        const int ssm = 32 * kStreamCap * 32 * 4;
+                        const unsigned grid = (unsigned)std::min<long long>((P.ntiles + 31) / 32, num_sms());
+                        kern<<<grid, kWarpCtaThreads, ssm, st>>>(reinterpret_cast<const uint32_t *>(in),
+                                                                 reinterpret_cast<int32_t *>(out),
+                                                                 reinterpret_cast<uint32_t *>(gstack), P);
+                        e = cudaGetLastError();
+                        if (e != cudaSuccess) return e;
+                    }
+                }
                 const size_t smem = PASS == 2 ? p.smem2 : p.smem3;
                 // long columns (L > 512) take 32 bands = 1024 threads: their tile
                 // already fills an SM's shared memory, so one CTA per SM anyway
@@ -1183,7 +1384,9 @@ cudaError_t edt_device_batched(const uint8_t *occ, int32_t *site, void *scratch,
         e = launch_slice_list(occ, p, sp, st);
         if (e == cudaSuccess) e = launch_pass1(occ, s1, p.nx, p.ny, p.nz, st, sp.sflag);
         if (e == cudaSuccess) e = launch_pass2(s1, s2, gs, p, p.nx, st, &sp);
-        if (e == cudaSuccess) e = launch_pass3(s2, site, gs, p, 1, 0, p.ny, st, &sp);
+        // pass 3 of the sparse path: s1 is dead by now and serves as the
+        // spill slab of the per-warp column stacks
+        if (e == cudaSuccess) e = launch_pass3(s2, site, s1, p, 1, 0, p.ny, st, &sp);
         return e;
     }
     e = launch_pass1(occ, s1, (long long)p.nx * nscenes, p.ny, p.nz, st);

@@ -44,7 +44,7 @@ int main(int argc, char **argv) {
             cudaEventRecord(e[1]);
             vx::launch_pass2(s1, s2, nullptr, p, nx, 0, spp);
             cudaEventRecord(e[2]);
-            vx::launch_pass3(s2, site, nullptr, p, 1, 0, ny, 0, spp);
+            vx::launch_pass3(s2, site, s1, p, 1, 0, ny, 0, spp);
             cudaEventRecord(e[3]);
             cudaEventSynchronize(e[3]);
             float a, b, c;
@@ -62,7 +62,7 @@ int main(int argc, char **argv) {
             vx::launch_pass2(s1, s2, nullptr, p, nx, 0, spp);
             if (pass == 3) {
                 cudaMemset(buf, 0, tiles * 64);
-                vx::launch_pass3(s2, site, nullptr, p, 1, 0, ny, 0, spp);
+                vx::launch_pass3(s2, site, s1, p, 1, 0, ny, 0, spp);
             }
             cudaDeviceSynchronize();
         }
@@ -81,6 +81,18 @@ int main(int argc, char **argv) {
             ++cnt;
             for (int q = 0; q < 6; ++q) acc[q] += (double)(t[i * 8 + q + 1] - t[i * 8 + q]);
             acc[6] += (double)(t[i * 8 + 6] - t[i * 8]);
+        }
+        if (pass == 3 && getenv("VX_HULL_HIST")) {   // hull-size histogram (k_pass3_stream slot 7)
+            long long hist[9] = {0};
+            for (long long i = 0; i < nt; ++i) {
+                const unsigned long long h = t[i * 8 + 7];
+                int b = 0;
+                while (b < 8 && (1ull << (b + 1)) <= h) ++b;
+                hist[b]++;
+            }
+            printf("hull max per tile histogram (<2,<4,..,>=256):");
+            for (int b = 0; b < 9; ++b) printf(" %lld", hist[b]);
+            printf("\n");
         }
         printf("pass %d: %lld tiles; mean cycles: tma_wait %.0f  phaseA %.0f  merges %.0f  phaseC %.0f  "
                "phaseD(warp0) %.0f  tail %.0f  total %.0f\n", pass, cnt, acc[0] / cnt, acc[1] / cnt,
