@@ -993,7 +993,10 @@ extern "C" int vx_cycle_destroy(vx_cycle *cy) {
     return VX_OK;
 }
 
-static cudaError_t edt_passes(vx_cycle *cy, const uint8_t *occ, int32_t *site, bool marks) {
+// src: the grid whose occupancy this is; when its touched list covers every
+// occupied voxel the slice flags come from that list
+static cudaError_t edt_passes(vx_cycle *cy, const vx_grid *src, int32_t *site, bool marks) {
+    const uint8_t *occ = src->occ;
     unsigned char *base = static_cast<unsigned char *>(cy->scratch);
     const EdtPlan &p = cy->plan;
     const size_t n = (size_t)p.nx * p.ny * p.nz;
@@ -1007,7 +1010,8 @@ static cudaError_t edt_passes(vx_cycle *cy, const uint8_t *occ, int32_t *site, b
     cudaError_t e = cudaSuccess;
     if (sparse) {
         sp = sparse_rows_at(base + s1b + s2b + p.gstack_bytes, p);
-        e = launch_slice_list(occ, p, sp, st);
+        if (src->sparse_ok) e = launch_slice_list_touched(src->touched, src->ctr, occ, p, sp, st);
+        else e = launch_slice_list(occ, p, sp, st);
         cy->ctx->launches += 2;
     }
     if (e == cudaSuccess) e = launch_pass1(occ, s1, p.nx, p.ny, p.nz, st, sparse ? sp.sflag : nullptr);
@@ -1038,7 +1042,7 @@ static int cycle_main_seq(vx_cycle *cy, const double *d_pts, long long npts, con
     if ((npts || n_dev) && (rc = insert_device(cy->env, d_pts, npts, n_dev, hit, thr, cy->mask))) return rc;
     if (!npts && !n_dev) VX_CUDA(cudaMemsetAsync(cy->env->ctr, 0, 3 * sizeof(unsigned long long), st));
     if (marks) cy->mark(4);
-    cudaError_t e = edt_passes(cy, cy->env->occ, cy->env_f.site, marks);
+    cudaError_t e = edt_passes(cy, cy->env, cy->env_f.site, marks);
     if (e != cudaSuccess) return cuda_fail(e, "edt(env)");
     const GridGeom g = cy->env->g;
     e = launch_site_world(cy->env_f.site, g, cy->d_centers, s, cy->d_lin, cy->d_world, cy->d_dist, st);
@@ -1093,7 +1097,7 @@ static int cycle_step(vx_cycle *cy, const double *pts, const double *d_pts_in, i
         if (cy->nself && (rc = stamp_sets(cy->self, cy->nself, cy->ijk_self, cy->off_self, cy->org_self,
                                           cy->vs_self, cy->T_self, kLMax, cy->total_self)))
             return rc;
-        cudaError_t e = edt_passes(cy, cy->self->occ, cy->self_f.site, false);
+        cudaError_t e = edt_passes(cy, cy->self, cy->self_f.site, false);
         if (e != cudaSuccess) return cuda_fail(e, "edt(self)");
         cy->last_self_T = Ts;
         cy->self_valid = true;

@@ -817,29 +817,29 @@ constexpr int kWarpCtaThreads = 1024;
 // k_column_tma (launched right after it) does the pass.
 constexpr int kStreamCap = VX_STREAM_CAP;
 
-template <typename FT, bool CMP>
+template <typename FT, bool XW>
 __global__ void __launch_bounds__(kWarpCtaThreads, 1) k_pass3_stream(const uint32_t *__restrict__ in,
                                                                      int32_t *__restrict__ out,
                                                                      uint32_t *__restrict__ ovf, const ColParams P) {
     extern __shared__ __align__(128) unsigned char smem[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    int m = P.L;
-    bool all_rows = true;
-    if constexpr (CMP) {
-        m = __ldg(P.hdr);
-        if (m > P.stream_max) return;
-        all_rows = m == P.L;
-    }
+    const int m = __ldg(P.hdr);
+    if (m > P.stream_max) return;
+    const bool all_rows = m == P.L;
     uint32_t *sst = reinterpret_cast<uint32_t *>(smem) + (size_t)w * kStreamCap * 32 + lane;
     const long long gw = (long long)blockIdx.x * nw + w;
     uint32_t *gst = ovf + gw * (long long)max(P.L - kStreamCap, 0) * 32 + lane - (long long)kStreamCap * 32;
-    // shared entries stay LDS/STS (no generic-pointer select); spills bypass L1
     auto ent = [&](int i) -> uint32_t { return i < kStreamCap ? sst[i * 32] : gst[(long long)i * 32]; };
     auto put = [&](int i, uint32_t e) {
         if (i < kStreamCap) sst[i * 32] = e;
         else gst[(long long)i * 32] = e;
     };
-    const uint32_t yzb = (uint32_t)P.yzb, zb = (uint32_t)P.zb, zmask = P.zmask, ymask = P.ymask;
+    // entry: XW (x << wb) | w with w = (j-y)^2 + (k-z)^2, F = x^2 + w (the
+    // winner's s2 code is re-read from the input); else (x << yzb) | code
+    const uint32_t eb = XW ? (uint32_t)P.wb : (uint32_t)P.yzb;
+    const uint32_t zb = (uint32_t)P.zb, zmask = P.zmask, ymask = P.ymask, wmask = P.wmask;
+    const long long plane = P.plane, splane = P.splane;
+    const int nz = P.nz, L = P.L;
     constexpr FT kNever = sizeof(FT) == 4 ? (FT)0x7fffffff : (FT)0x7fffffffffffffffLL;
     const long long step = (long long)gridDim.x * nw;
     for (long long tile = gw; tile < P.ntiles; tile += step) {
@@ -849,29 +849,34 @@ __global__ void __launch_bounds__(kWarpCtaThreads, 1) k_pass3_stream(const uint3
         const int jl = (int)(outer - (long long)scene * P.nyl);
         const int jq = P.j0 + jl;
         const int k = kt * 32 + lane;
-        if (k >= P.nz) continue;   // lanes only; no warp-wide sync below
-        const long long base = (long long)scene * P.nvox + (long long)jl * P.nz + k;
+        if (k >= nz) continue;   // lanes only; no warp-wide sync below
+        const long long base = (long long)scene * P.nvox + (long long)jl * nz + k;
         const uint32_t *src = in + base;
         VX_PTW(tile, 0);
         VX_PTW(tile, 1);
+        auto wof = [&](uint32_t v) -> FT {   // (j - y)^2 + (k - z)^2 of an s2 code
+            const FT dy = (FT)(jq - (int)((v >> zb) & ymask)), dz = (FT)(k - (int)(v & zmask));
+            return dy * dy + dz * dz;
+        };
         auto Fof = [&](uint32_t e) -> FT {
-            const int x = (int)(e >> yzb), sy = (int)((e >> zb) & ymask), sz = (int)(e & zmask);
-            const FT dy = (FT)(jq - sy), dz = (FT)(k - sz);
-            return dy * dy + dz * dz + (FT)x * (FT)x;
+            const FT x = (FT)(int)(e >> eb);
+            if constexpr (XW) return x * x + (FT)(e & wmask);
+            else return x * x + wof(e);
         };
         int n = 0, ya = 0, yb = 0;
         FT Fa = 0, Fb = 0;
         auto consume = [&](uint32_t v, int yc) {
             if (v == 0xffffffffu) return;
-            const uint32_t ec = ((uint32_t)yc << yzb) | v;
-            const FT Fc = Fof(ec);
+            const FT wc = wof(v);
+            const uint32_t ec = ((uint32_t)yc << eb) | (XW ? (uint32_t)wc : v);
+            const FT Fc = (FT)yc * (FT)yc + wc;
             while (n >= 2 && dominated<FT>(ya, Fa, yb, Fb, yc, Fc)) {
                 --n;
                 yb = ya;
                 Fb = Fa;
                 if (n >= 2) {
                     const uint32_t e = ent(n - 2);
-                    ya = (int)(e >> yzb);
+                    ya = (int)(e >> eb);
                     Fa = Fof(e);
                 }
             }
@@ -890,7 +895,7 @@ __global__ void __launch_bounds__(kWarpCtaThreads, 1) k_pass3_stream(const uint3
             for (int u = 0; u < U; ++u) {
                 const int t = t0 + u;
                 yr[u] = t < m ? (all_rows ? t : __ldg(P.xs + t)) : 0;
-                v[u] = t < m ? __ldg(src + (long long)yr[u] * P.splane) : 0xffffffffu;
+                v[u] = t < m ? __ldg(src + (long long)yr[u] * splane) : 0xffffffffu;
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) consume(v[u], yr[u]);
@@ -905,56 +910,61 @@ __global__ void __launch_bounds__(kWarpCtaThreads, 1) k_pass3_stream(const uint3
 #endif
         VX_PTW(tile, 2);
         // ---- queries: first minimiser at every row, stepped walk
-        // 32-bit row offsets: nx * ny * nz < 2^31 (int32 sites)
         int32_t *dst = out + base;
-        const uint32_t ostep = (uint32_t)P.splane;
-        uint32_t off = 0;
         if (n == 0) {
-            for (int y = 0; y < P.L; ++y, off += ostep) dst[off] = -1;
+            for (int y = 0; y < L; ++y, dst += splane) *dst = -1;
         } else {
+            auto site_of = [&](uint32_t e, uint32_t code) -> int32_t {
+                const long long x = (long long)(e >> eb);
+                const uint32_t c = XW ? code : e;
+                return (int32_t)(x * plane + (long long)((c >> zb) & ymask) * nz + (long long)(c & zmask));
+            };
+            auto code_of = [&](uint32_t e) -> uint32_t {   // XW: the s2 code at the entry's row
+                if constexpr (XW) return __ldg(src + (long long)(e >> eb) * splane);
+                else return 0u;
+            };
             int pos = 0;
             uint32_t cur = ent(0);
-            int yc = (int)(cur >> yzb);
+            int yc = (int)(cur >> eb);
             FT Fc = Fof(cur);
-            auto site_of = [&](uint32_t e) -> int32_t {
-                const long long x = (long long)(e >> yzb), sy = (long long)((e >> zb) & ymask);
-                return (int32_t)(x * P.plane + sy * P.nz + (long long)(e & zmask));   // edt.py:417
-            };
-            int32_t ocur = site_of(cur);
+            int32_t ocur = site_of(cur, code_of(cur));
             bool has = n > 1;
-            uint32_t sent = 0;
+            uint32_t sent = 0, scode = 0;
             int ys = 0;
             FT Fs = 0;
             if (has) {
                 sent = ent(1);
-                ys = (int)(sent >> yzb);
+                ys = (int)(sent >> eb);
                 Fs = Fof(sent);
+                scode = code_of(sent);   // prefetched for the advance
             }
             FT dN = has ? Fs - Fc : kNever;
             FT tt = has ? (FT)2 * (FT)(ys - yc) : (FT)0;
             FT rhs = 0;
-#pragma unroll 4
-            for (int y = 0; y < P.L; ++y) {
+            for (int y = 0; y < L; ++y) {
                 if (dN < rhs) {   // successor strictly closer at row y (edt.py:311)
+                    uint32_t ccode;
                     do {
                         cur = sent;
+                        ccode = scode;
                         yc = ys;
                         Fc = Fs;
                         ++pos;
                         has = pos + 1 < n;
                         if (has) {
                             sent = ent(pos + 1);
-                            ys = (int)(sent >> yzb);
+                            ys = (int)(sent >> eb);
                             Fs = Fof(sent);
+                            scode = code_of(sent);
                         }
                     } while (has && better<FT>(ys, Fs, yc, Fc, y));
-                    ocur = site_of(cur);
+                    ocur = site_of(cur, ccode);
                     dN = has ? Fs - Fc : kNever;
                     tt = has ? (FT)2 * (FT)(ys - yc) : (FT)0;
                     rhs = (FT)y * tt;
                 }
-                dst[off] = ocur;
-                off += ostep;
+                *dst = ocur;
+                dst += splane;
                 rhs += tt;
             }
         }
@@ -1094,10 +1104,15 @@ cudaError_t launch_col(const void *in, void *out, void *gstack, const EdtPlan &p
                     // its spill slab
                     const long long spill = std::min<long long>(P.ntiles, (long long)num_sms() * 32) *
                                             std::max(P.L - kStreamCap, 0) * 32 * 4;
-                    if (cmp && gstack && p.xb + p.yb + p.zb <= 32 && spill <= (long long)p.s1_bytes) {
+                    // only with tiles enough for >= 16 warps per SM: each warp walks
+                    // its tile alone, so small grids keep the banded kernel
+                    const char *xw = getenv("VX_STREAM_XW");
+                    const bool use_xw = xw && atoi(xw) != 0 && p.xb + p.wb <= 32;   // re-read variant: slower here
+                    if (cmp && gstack && (use_xw || p.xb + p.yb + p.zb <= 32) && spill <= (long long)p.s1_bytes &&
+                        P.ntiles >= 16LL * num_sms()) {
                         const char *sm = getenv("VX_STREAM_MAX");
-                        P.stream_max = sm ? atoi(sm) : kStreamMaxRows;
-                        auto kern = k_pass3_stream<typename C::FT, true>;
+                        P.stream_max = sm ? atoi(sm) : std::min(kStreamMaxRows, P.L / 2);
+                        auto kern = use_xw ? k_pass3_stream<typename C::FT, true> : k_pass3_stream<typename C::FT, false>;
                         cudaError_t e = allow_smem(kern);
                         if (e != cudaSuccess) return e;
                         const int ssm = 32 * kStreamCap * 32 * 4;
@@ -1335,6 +1350,37 @@ __global__ void __launch_bounds__(1024) k_slice_list(const uint8_t *__restrict__
         __syncthreads();
     }
     if (threadIdx.x == 0) hdr[0] = base_s;
+}
+
+// slice flags from a grid's touched list (every voxel written since its last
+// reset, so every occupied voxel): a few hundred thousand entries instead of
+// a pass over the whole occupancy array
+__global__ void k_slice_flags_touched(const int32_t *__restrict__ touched, const DevCounters *__restrict__ ctr,
+                                      const uint8_t *__restrict__ occ, long long plane, long long n,
+                                      uint8_t *__restrict__ sflag) {
+    const long long nth = (long long)gridDim.x * blockDim.x;
+    const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (ctr->overflow) {   // the list is incomplete: scan every voxel
+        for (long long v = tid; v < n; v += nth)
+            if (occ[v]) sflag[v / plane] = 1;
+        return;
+    }
+    const int cnt = ctr->touched;
+    for (long long t = tid; t < cnt; t += nth) {
+        const int v = touched[t];
+        if (occ[v]) sflag[v / plane] = 1;
+    }
+}
+
+cudaError_t launch_slice_list_touched(const int32_t *touched, const DevCounters *ctr, const uint8_t *occ,
+                                      const EdtPlan &p, const SparseRows &sp, cudaStream_t st) {
+    cudaError_t e = cudaMemsetAsync(const_cast<uint8_t *>(sp.sflag), 0, (size_t)p.nx, st);
+    if (e != cudaSuccess) return e;
+    k_slice_flags_touched<<<2 * num_sms(), 256, 0, st>>>(touched, ctr, occ, (long long)p.ny * p.nz,
+                                                         (long long)p.nx * p.ny * p.nz,
+                                                         const_cast<uint8_t *>(sp.sflag));
+    k_slice_list<<<1, 1024, 0, st>>>(sp.sflag, p.nx, const_cast<int *>(sp.xs), const_cast<int *>(sp.hdr));
+    return cudaGetLastError();
 }
 
 cudaError_t launch_slice_list(const uint8_t *occ, const EdtPlan &p, const SparseRows &sp, cudaStream_t st) {

@@ -62,6 +62,10 @@ cudaError_t launch_pass3(const void *s2, int32_t *site, void *gstack, const EdtP
 bool sparse_ok(const EdtPlan &p, int nscenes);
 SparseRows sparse_rows_at(void *where, const EdtPlan &p);
 cudaError_t launch_slice_list(const uint8_t *occ, const EdtPlan &p, const SparseRows &sp, cudaStream_t st);
+struct DevCounters;
+// same from a grid's touched list (valid when it covers every occupied voxel)
+cudaError_t launch_slice_list_touched(const int32_t *touched, const DevCounters *ctr, const uint8_t *occ,
+                                      const EdtPlan &p, const SparseRows &sp, cudaStream_t st);
 size_t scratch_bytes_for(const EdtPlan &p, int nscenes);
 // Full EDT: occ (device) -> site (device); scratch >= scratch_bytes_for(p, n).
 cudaError_t edt_device(const uint8_t *occ, int32_t *site, void *scratch, const EdtPlan &p,
