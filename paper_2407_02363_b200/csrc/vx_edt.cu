@@ -76,7 +76,10 @@ constexpr bool kP3XW = VX_P3_XW != 0;
 #define VX_CMP_GROUP_ROWS 24   // target candidates per group in compact pass 3
 #endif
 #ifndef VX_STREAM_CAP
-#define VX_STREAM_CAP 48   // shared-memory stack entries per column (k_pass3_stream)
+#define VX_STREAM_CAP 55   // shared-memory stack entries per column (k_pass3_stream; 32 warps x 55 x 128 B)
+#endif
+#ifndef VX_STREAM_U
+#define VX_STREAM_U 16
 #endif
 #ifndef VX_STREAM_MAX_ROWS
 #define VX_STREAM_MAX_ROWS 256   // occupied slices up to which pass 3 runs one warp per tile
@@ -887,7 +890,7 @@ __global__ void __launch_bounds__(kWarpCtaThreads, 1) k_pass3_stream(const uint3
             Fb = Fc;
             ++n;
         };
-        constexpr int U = 8;
+        constexpr int U = VX_STREAM_U;   // candidate rows in flight per lane
         for (int t0 = 0; t0 < m; t0 += U) {
             uint32_t v[U];
             int yr[U];
