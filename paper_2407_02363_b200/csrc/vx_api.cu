@@ -861,6 +861,10 @@ struct vx_cycle {
     // EDT, gather); the cloud size is read from d_npts on the device
     bool use_graph = true;
     long long *d_npts = nullptr, *h_npts = nullptr;  // device / pinned host point count
+    // occupied-slice count of the last env EDT (host-mapped, written by the
+    // device) -> which pass-3 kernels the next tick launches
+    int *h_m = nullptr, *d_m = nullptr;
+    int p3_mode = 0, g_mode = -1;
     cudaGraphExec_t gexec = nullptr;
     int g_s = -1;
     float g_hit = 0.f;
@@ -952,6 +956,11 @@ extern "C" int vx_cycle_create(vx_ctx *c, int nx, int ny, int nz, double vs, con
     if (e == cudaSuccess) e = cudaMalloc(&cy->d_dist, 2 * S * 8);
     if (e == cudaSuccess) e = cudaMalloc(&cy->d_npts, sizeof(long long));
     if (e == cudaSuccess) e = cudaHostAlloc(&cy->h_npts, sizeof(long long), cudaHostAllocPortable);
+    if (e == cudaSuccess) e = cudaHostAlloc(&cy->h_m, sizeof(int), cudaHostAllocMapped | cudaHostAllocPortable);
+    if (e == cudaSuccess) {
+        *cy->h_m = -1;
+        e = cudaHostGetDevicePointer(&cy->d_m, cy->h_m, 0);
+    }
     for (vx_field *f : {&cy->env_f, &cy->self_f}) {
         f->ctx = c;
         f->nx = nx; f->ny = ny; f->nz = nz;
@@ -982,6 +991,7 @@ extern "C" int vx_cycle_destroy(vx_cycle *cy) {
     av_free(cy);
     cudaFree(cy->d_npts);
     if (cy->h_npts) cudaFreeHost(cy->h_npts);
+    if (cy->h_m) cudaFreeHost(cy->h_m);
     if (cy->gexec) cudaGraphExecDestroy(cy->gexec);
     cudaFree(cy->env_f.site);
     cudaFree(cy->self_f.site);
@@ -1010,6 +1020,10 @@ static cudaError_t edt_passes(vx_cycle *cy, const vx_grid *src, int32_t *site, b
     cudaError_t e = cudaSuccess;
     if (sparse) {
         sp = sparse_rows_at(base + s1b + s2b + p.gstack_bytes, p);
+        if (src == cy->env) {   // the per-tick map: feed and use the count hint
+            sp.m_mirror = cy->d_m;
+            sp.p3_mode = cy->p3_mode;
+        }
         if (src->sparse_ok) e = launch_slice_list_touched(src->touched, src->ctr, occ, p, sp, st);
         else e = launch_slice_list(occ, p, sp, st);
         cy->ctx->launches += 2;
@@ -1110,7 +1124,8 @@ static int cycle_step(vx_cycle *cy, const double *pts, const double *d_pts_in, i
             VX_CUDA(cudaMemcpyAsync(cy->d_pts, d_pts_in, (size_t)npts * 24, cudaMemcpyDeviceToDevice, st));
         *cy->h_npts = npts;
         VX_CUDA(cudaMemcpyAsync(cy->d_npts, cy->h_npts, sizeof(long long), cudaMemcpyHostToDevice, st));
-        if (!cy->gexec || cy->g_s != s || cy->g_hit != hit || cy->g_thr != thr) {
+        cy->p3_mode = pass3_mode_hint(cy->plan, *(volatile int *)cy->h_m);
+        if (!cy->gexec || cy->g_s != s || cy->g_hit != hit || cy->g_thr != thr || cy->g_mode != cy->p3_mode) {
             if (cy->gexec) cudaGraphExecDestroy(cy->gexec);
             cy->gexec = nullptr;
             const long long l0 = c->launches;
@@ -1129,12 +1144,14 @@ static int cycle_step(vx_cycle *cy, const double *pts, const double *d_pts_in, i
             cy->g_kernels = c->launches - l0;
             c->launches = l0;
             cy->g_s = s;
+            cy->g_mode = cy->p3_mode;
             cy->g_hit = hit;
             cy->g_thr = thr;
         }
         VX_CUDA(cudaGraphLaunch(cy->gexec, st));
         c->launches += cy->g_kernels;
     } else {
+        cy->p3_mode = pass3_mode_hint(cy->plan, *(volatile int *)cy->h_m);
         if ((rc = cycle_main_seq(cy, d_pts, npts, nullptr, hit, thr, s, true))) return rc;
     }
     if (cy->profiling && cy->ring_n < vx_cycle::kRing) cy->ring_n++;

@@ -1111,10 +1111,11 @@ cudaError_t launch_col(const void *in, void *out, void *gstack, const EdtPlan &p
                     // its tile alone, so small grids keep the banded kernel
                     const char *xw = getenv("VX_STREAM_XW");
                     const bool use_xw = xw && atoi(xw) != 0 && p.xb + p.wb <= 32;   // re-read variant: slower here
-                    if (cmp && gstack && (use_xw || p.xb + p.yb + p.zb <= 32) && spill <= (long long)p.s1_bytes &&
-                        P.ntiles >= 16LL * num_sms()) {
+                    const int mode = sp ? sp->p3_mode : 0;
+                    if (mode != 2 && cmp && gstack && (use_xw || p.xb + p.yb + p.zb <= 32) &&
+                        spill <= (long long)p.s1_bytes && P.ntiles >= 16LL * num_sms()) {
                         const char *sm = getenv("VX_STREAM_MAX");
-                        P.stream_max = sm ? atoi(sm) : std::min(kStreamMaxRows, P.L / 2);
+                        P.stream_max = mode == 1 ? 0x7fffffff : sm ? atoi(sm) : std::min(kStreamMaxRows, P.L / 2);
                         auto kern = use_xw ? k_pass3_stream<typename C::FT, true> : k_pass3_stream<typename C::FT, false>;
                         cudaError_t e = allow_smem(kern);
                         if (e != cudaSuccess) return e;
@@ -1124,7 +1125,9 @@ cudaError_t launch_col(const void *in, void *out, void *gstack, const EdtPlan &p
                                                                  reinterpret_cast<int32_t *>(out),
                                                                  reinterpret_cast<uint32_t *>(gstack), P);
                         e = cudaGetLastError();
-                        if (e != cudaSuccess) return e;
+                        if (e != cudaSuccess || mode == 1) return e;   // mode 1: no banded launch
+                    } else {
+                        P.stream_max = -1;
                     }
                 }
                 const size_t smem = PASS == 2 ? p.smem2 : p.smem3;
@@ -1328,7 +1331,8 @@ __global__ void __launch_bounds__(256) k_slice_flags(const uint8_t *__restrict__
 
 // ascending list of occupied slices (one CTA, block-wide prefix sums)
 __global__ void __launch_bounds__(1024) k_slice_list(const uint8_t *__restrict__ sflag, int nslices,
-                                                     int *__restrict__ xs, int *__restrict__ hdr) {
+                                                     int *__restrict__ xs, int *__restrict__ hdr,
+                                                     int *__restrict__ m_mirror) {
     __shared__ int wsum[32];
     __shared__ int base_s;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1352,7 +1356,10 @@ __global__ void __launch_bounds__(1024) k_slice_list(const uint8_t *__restrict__
         if (threadIdx.x == 0) base_s = base + tot;
         __syncthreads();
     }
-    if (threadIdx.x == 0) hdr[0] = base_s;
+    if (threadIdx.x == 0) {
+        hdr[0] = base_s;
+        if (m_mirror) *(volatile int *)m_mirror = base_s;   // host-mapped hint
+    }
 }
 
 // slice flags from a grid's touched list (every voxel written since its last
@@ -1382,14 +1389,33 @@ cudaError_t launch_slice_list_touched(const int32_t *touched, const DevCounters 
     k_slice_flags_touched<<<2 * num_sms(), 256, 0, st>>>(touched, ctr, occ, (long long)p.ny * p.nz,
                                                          (long long)p.nx * p.ny * p.nz,
                                                          const_cast<uint8_t *>(sp.sflag));
-    k_slice_list<<<1, 1024, 0, st>>>(sp.sflag, p.nx, const_cast<int *>(sp.xs), const_cast<int *>(sp.hdr));
+    k_slice_list<<<1, 1024, 0, st>>>(sp.sflag, p.nx, const_cast<int *>(sp.xs), const_cast<int *>(sp.hdr),
+                                     sp.m_mirror);
     return cudaGetLastError();
 }
 
 cudaError_t launch_slice_list(const uint8_t *occ, const EdtPlan &p, const SparseRows &sp, cudaStream_t st) {
     k_slice_flags<<<(unsigned)p.nx, 256, 0, st>>>(occ, (long long)p.ny * p.nz, const_cast<uint8_t *>(sp.sflag));
-    k_slice_list<<<1, 1024, 0, st>>>(sp.sflag, p.nx, const_cast<int *>(sp.xs), const_cast<int *>(sp.hdr));
+    k_slice_list<<<1, 1024, 0, st>>>(sp.sflag, p.nx, const_cast<int *>(sp.xs), const_cast<int *>(sp.hdr),
+                                     sp.m_mirror);
     return cudaGetLastError();
+}
+
+// which pass-3 kernels to launch given a predicted occupied-slice count m
+// (the previous call's, read from SparseRows::m_mirror): mirrors the gates of
+// launch_col.  Any mode is correct for any m; a wrong guess only costs time.
+int pass3_mode_hint(const EdtPlan &p, int m) {
+    if (m < 0) return 0;
+    const long long ntiles = (long long)((p.nz + 31) / 32) * p.ny;
+    const long long spill = std::min<long long>(ntiles, (long long)num_sms() * 32) *
+                            std::max(p.nx - kStreamCap, 0) * 32 * 4;
+    const bool ok = p.tma2 && p.tma3 && !p.gstack3 && !p.s2_wide && !p.e3_wide &&
+                    p.xb + p.yb + p.zb <= 32 && spill <= (long long)p.s1_bytes &&
+                    ntiles >= 16LL * num_sms();
+    if (!ok) return 2;
+    const char *sm = getenv("VX_STREAM_MAX");
+    const int smax = sm ? atoi(sm) : std::min(kStreamMaxRows, p.nx / 2);
+    return m <= smax ? 1 : 2;
 }
 
 size_t sparse_bytes(const EdtPlan &p) {

@@ -43,6 +43,9 @@ struct SparseRows {
     const uint8_t *sflag;   // [nx] 1 if slice i holds an occupied voxel
     const int *xs;          // [nx] ascending occupied slice indices
     const int *hdr;         // hdr[0] = count
+    int *m_mirror = nullptr;  // optional host-mapped copy of hdr[0] (the next call's hint)
+    int p3_mode = 0;          // pass 3: 0 both kernels, gated on the device by the
+                              // count; 1 one warp per tile only; 2 banded only
 };
 
 // Pass launchers (stream-ordered, no host sync).  Return cudaError_t.
@@ -62,6 +65,7 @@ cudaError_t launch_pass3(const void *s2, int32_t *site, void *gstack, const EdtP
 bool sparse_ok(const EdtPlan &p, int nscenes);
 SparseRows sparse_rows_at(void *where, const EdtPlan &p);
 cudaError_t launch_slice_list(const uint8_t *occ, const EdtPlan &p, const SparseRows &sp, cudaStream_t st);
+int pass3_mode_hint(const EdtPlan &p, int m);   // SparseRows::p3_mode from a predicted count
 struct DevCounters;
 // same from a grid's touched list (valid when it covers every occupied voxel)
 cudaError_t launch_slice_list_touched(const int32_t *touched, const DevCounters *ctr, const uint8_t *occ,
