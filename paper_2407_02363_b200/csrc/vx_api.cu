@@ -1028,7 +1028,7 @@ static cudaError_t edt_passes(vx_cycle *cy, const vx_grid *src, int32_t *site, b
         else e = launch_slice_list(occ, p, sp, st);
         cy->ctx->launches += 2;
     }
-    if (e == cudaSuccess) e = launch_pass1(occ, s1, p.nx, p.ny, p.nz, st, sparse ? sp.sflag : nullptr);
+    if (e == cudaSuccess) e = launch_pass1(occ, s1, p.nx, p.ny, p.nz, st, sparse ? &sp : nullptr);
     if (marks) cy->mark(5);
     if (e == cudaSuccess) e = launch_pass2(s1, s2, gs, p, p.nx, st, sparse ? &sp : nullptr);
     if (marks) cy->mark(6);

@@ -171,17 +171,27 @@ template <int CMAX, int LPW>
 __global__ void __launch_bounds__(256) k_pass1_v4(const uint8_t *__restrict__ occ,
                                                   int32_t *__restrict__ s1,
                                                   long long nlines, int nz,
-                                                  const uint8_t *__restrict__ sflag, int ny) {
+                                                  const uint8_t *__restrict__ sflag, int ny,
+                                                  const int *__restrict__ xs, const int *__restrict__ hdr) {
     const int lane = threadIdx.x & 31;
     const long long line0 = ((long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * LPW;
     const int nq = nz >> 2;
     uint32_t nib[LPW][CMAX];
     bool act[LPW];
+    long long lines[LPW];
+    const int m = xs ? __ldg(hdr) : 0;
 #pragma unroll
     for (int l = 0; l < LPW; ++l) {
-        const long long line = line0 + l;
+        long long line = line0 + l;
         // warp-uniform; empty slices are skipped (nothing downstream reads them)
-        act[l] = line < nlines && (!sflag || sflag[(uint32_t)line / (uint32_t)ny]);
+        if (xs) {   // lines of occupied slices first (slot-major), the surplus idles
+            const uint32_t slot = (uint32_t)line / (uint32_t)ny;
+            act[l] = (int)slot < m;
+            if (act[l]) line = (long long)__ldg(xs + slot) * ny + (line - (long long)slot * ny);
+        } else {
+            act[l] = line < nlines && (!sflag || sflag[(uint32_t)line / (uint32_t)ny]);
+        }
+        lines[l] = line;
         const uint32_t *src = reinterpret_cast<const uint32_t *>(occ + line * nz);
 #pragma unroll
         for (int c = 0; c < CMAX; ++c) {
@@ -191,7 +201,7 @@ __global__ void __launch_bounds__(256) k_pass1_v4(const uint8_t *__restrict__ oc
     }
 #pragma unroll
     for (int l = 0; l < LPW; ++l)
-        if (act[l]) pass1_line<CMAX>(nib[l], reinterpret_cast<int4 *>(s1 + (line0 + l) * nz), nq, lane);
+        if (act[l]) pass1_line<CMAX>(nib[l], reinterpret_cast<int4 *>(s1 + lines[l] * nz), nq, lane);
 }
 
 // Pass 1, generic path (any nz): 32-voxel chunks with ballots; the forward
@@ -732,11 +742,18 @@ __global__ void __launch_bounds__(MAXT, MAXT >= 1024 ? 1 : kColMinBlocks) k_colu
     EntT *stk = reinterpret_cast<EntT *>(smem);
     int *meta = reinterpret_cast<int *>(smem + (size_t)P.rows_alloc * 32 * sizeof(EntT));
     uint64_t *bar = reinterpret_cast<uint64_t *>(meta + 3 * P.B * 32 + 32);
-    const long long tile = blockIdx.x;
+    long long tile = blockIdx.x;
     const int kt = (int)(tile % P.nkt);
-    const long long outer = tile / P.nkt;
+    long long outer = tile / P.nkt;
     if constexpr (PASS == 2) {
-        if (P.sflag && !P.sflag[outer]) return;   // empty slice: pass 3 never reads it
+        if (P.xs) {   // occupied-slice list: CTA rows map to occupied slices, the
+                      // surplus CTAs (empty slices) all sit at the end of the grid
+            if (outer >= __ldg(P.hdr)) return;
+            outer = __ldg(P.xs + outer);
+            tile = outer * P.nkt + kt;
+        } else if (P.sflag && !P.sflag[outer]) {
+            return;   // empty slice: pass 3 never reads it
+        }
     }
     VX_PT(0);
     bool all_rows = true;
@@ -1088,7 +1105,8 @@ cudaError_t launch_col(const void *in, void *out, void *gstack, const EdtPlan &p
     ColParams P = col_params(p, PASS, nouter, nyl, j0);
     if (sp) {   // the caller only passes one when both column passes are TMA-staged
         if (PASS == 2) P.sflag = sp->sflag;
-        else { P.xs = sp->xs; P.hdr = sp->hdr; }
+        P.xs = sp->xs;
+        P.hdr = sp->hdr;
     }
     if (P.ntiles == 0) return cudaSuccess;
     const dim3 block(32, P.B);
@@ -1271,17 +1289,19 @@ bool make_plan(int nx, int ny, int nz, EdtPlan *p, int force_global_stack) {
 
 
 cudaError_t launch_pass1(const uint8_t *occ, int32_t *s1, long long nslices, int ny, int nz,
-                         cudaStream_t st, const uint8_t *sflag) {
+                         cudaStream_t st, const SparseRows *sp) {
     const long long nlines = nslices * ny;
     if (nlines == 0) return cudaSuccess;
+    const uint8_t *sflag = sp ? sp->sflag : nullptr;
+    const int *xs = sp ? sp->xs : nullptr, *hdr = sp ? sp->hdr : nullptr;
     const unsigned grid = (unsigned)((nlines + 7) / 8);
     const unsigned grid2 = (unsigned)((nlines + 15) / 16);
     const bool vec = (nz % 4 == 0) && ((uintptr_t)occ % 16 == 0) && ((uintptr_t)s1 % 16 == 0);
-    if (vec && nz <= 128) k_pass1_v4<1, 2><<<grid2, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny);
-    else if (vec && nz <= 256) k_pass1_v4<2, 2><<<grid2, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny);
-    else if (vec && nz <= 512) k_pass1_v4<4, 2><<<grid2, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny);
-    else if (vec && nz <= 1024) k_pass1_v4<8, 1><<<grid, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny);
-    else if (vec && nz <= 2048) k_pass1_v4<16, 1><<<grid, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny);
+    if (vec && nz <= 128) k_pass1_v4<1, 2><<<grid2, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny, xs, hdr);
+    else if (vec && nz <= 256) k_pass1_v4<2, 2><<<grid2, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny, xs, hdr);
+    else if (vec && nz <= 512) k_pass1_v4<4, 2><<<grid2, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny, xs, hdr);
+    else if (vec && nz <= 1024) k_pass1_v4<8, 1><<<grid, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny, xs, hdr);
+    else if (vec && nz <= 2048) k_pass1_v4<16, 1><<<grid, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny, xs, hdr);
     else k_pass1_generic<<<grid, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny);
     return cudaGetLastError();
 }
@@ -1457,7 +1477,7 @@ cudaError_t edt_device_batched(const uint8_t *occ, int32_t *site, void *scratch,
     if (sparse_ok(p, nscenes)) {
         const SparseRows sp = sparse_rows_at(base + s1b + s2b + p.gstack_bytes, p);
         e = launch_slice_list(occ, p, sp, st);
-        if (e == cudaSuccess) e = launch_pass1(occ, s1, p.nx, p.ny, p.nz, st, sp.sflag);
+        if (e == cudaSuccess) e = launch_pass1(occ, s1, p.nx, p.ny, p.nz, st, &sp);
         if (e == cudaSuccess) e = launch_pass2(s1, s2, gs, p, p.nx, st, &sp);
         // pass 3 of the sparse path: s1 is dead by now and serves as the
         // spill slab of the per-warp column stacks

@@ -51,7 +51,7 @@ struct SparseRows {
 // Pass launchers (stream-ordered, no host sync).  Return cudaError_t.
 // nslices: number of (ny, nz) slices stacked along i (scenes * local nx).
 cudaError_t launch_pass1(const uint8_t *occ, int32_t *s1, long long nslices, int ny, int nz,
-                         cudaStream_t st, const uint8_t *sflag = nullptr);
+                         cudaStream_t st, const SparseRows *sp = nullptr);
 cudaError_t launch_pass2(const int32_t *s1, void *s2, void *gstack, const EdtPlan &p,
                          long long nslices, cudaStream_t st, const SparseRows *sp = nullptr);
 // pass 2 with the fused exchange epilogue (slab mode)

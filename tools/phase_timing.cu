@@ -40,7 +40,7 @@ int main(int argc, char **argv) {
         float t1 = 0, t2 = 0, t3 = 0;
         for (int rep = 0; rep < 6; ++rep) {
             cudaEventRecord(e[0]);
-            vx::launch_pass1(occ, s1, nx, ny, nz, 0, sparse ? sp.sflag : nullptr);
+            vx::launch_pass1(occ, s1, nx, ny, nz, 0, spp);
             cudaEventRecord(e[1]);
             vx::launch_pass2(s1, s2, nullptr, p, nx, 0, spp);
             cudaEventRecord(e[2]);
@@ -58,7 +58,7 @@ int main(int argc, char **argv) {
     }
     for (int pass = 2; pass <= 3; ++pass) {
         for (int rep = 0; rep < 3; ++rep) {
-            vx::launch_pass1(occ, s1, nx, ny, nz, 0, sparse ? sp.sflag : nullptr);
+            vx::launch_pass1(occ, s1, nx, ny, nz, 0, spp);
             vx::launch_pass2(s1, s2, nullptr, p, nx, 0, spp);
             if (pass == 3) {
                 cudaMemset(buf, 0, tiles * 64);
