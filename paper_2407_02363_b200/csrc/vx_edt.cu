@@ -847,6 +847,10 @@ __global__ void __launch_bounds__(kWarpCtaThreads, 1) k_pass3_stream(const uint3
     if (m > P.stream_max) return;
     const bool all_rows = m == P.L;
     uint32_t *sst = reinterpret_cast<uint32_t *>(smem) + (size_t)w * kStreamCap * 32 + lane;
+    // candidate rows, staged once per CTA (every tile of the pass scans the same list)
+    int *rows_s = reinterpret_cast<int *>(smem + (size_t)nw * kStreamCap * 32 * 4);
+    for (int t = threadIdx.x; t < m; t += blockDim.x) rows_s[t] = all_rows ? t : __ldg(P.xs + t);
+    __syncthreads();
     const long long gw = (long long)blockIdx.x * nw + w;
     uint32_t *gst = ovf + gw * (long long)max(P.L - kStreamCap, 0) * 32 + lane - (long long)kStreamCap * 32;
     auto ent = [&](int i) -> uint32_t { return i < kStreamCap ? sst[i * 32] : gst[(long long)i * 32]; };
@@ -908,17 +912,22 @@ __global__ void __launch_bounds__(kWarpCtaThreads, 1) k_pass3_stream(const uint3
             ++n;
         };
         constexpr int U = VX_STREAM_U;   // candidate rows in flight per lane
-        for (int t0 = 0; t0 < m; t0 += U) {
+        const uint32_t ssp = (uint32_t)splane;   // row offsets fit 32 bits (int32 sites)
+        int t0 = 0;
+        for (; t0 + U <= m; t0 += U) {
             uint32_t v[U];
             int yr[U];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-                const int t = t0 + u;
-                yr[u] = t < m ? (all_rows ? t : __ldg(P.xs + t)) : 0;
-                v[u] = t < m ? __ldg(src + (long long)yr[u] * splane) : 0xffffffffu;
+                yr[u] = rows_s[t0 + u];
+                v[u] = __ldg(src + (uint32_t)yr[u] * ssp);
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) consume(v[u], yr[u]);
+        }
+        for (; t0 < m; ++t0) {
+            const int yr = rows_s[t0];
+            consume(__ldg(src + (uint32_t)yr * ssp), yr);
         }
 #ifdef VX_PHASE_TIMING
         {   // hull size (max over the warp's columns) for tools/phase_timing
@@ -1130,14 +1139,14 @@ cudaError_t launch_col(const void *in, void *out, void *gstack, const EdtPlan &p
                     const char *xw = getenv("VX_STREAM_XW");
                     const bool use_xw = xw && atoi(xw) != 0 && p.xb + p.wb <= 32;   // re-read variant: slower here
                     const int mode = sp ? sp->p3_mode : 0;
+                    const size_t ssm = (size_t)32 * kStreamCap * 32 * 4 + (size_t)P.L * 4;   // stacks + row list
                     if (mode != 2 && cmp && gstack && (use_xw || p.xb + p.yb + p.zb <= 32) &&
-                        spill <= (long long)p.s1_bytes && P.ntiles >= 16LL * num_sms()) {
+                        spill <= (long long)p.s1_bytes && P.ntiles >= 16LL * num_sms() && ssm <= kSmemLimit) {
                         const char *sm = getenv("VX_STREAM_MAX");
                         P.stream_max = mode == 1 ? 0x7fffffff : sm ? atoi(sm) : std::min(kStreamMaxRows, P.L / 2);
                         auto kern = use_xw ? k_pass3_stream<typename C::FT, true> : k_pass3_stream<typename C::FT, false>;
                         cudaError_t e = allow_smem(kern);
                         if (e != cudaSuccess) return e;
-                        const int ssm = 32 * kStreamCap * 32 * 4;
                         const unsigned grid = (unsigned)std::min<long long>((P.ntiles + 31) / 32, num_sms());
                         kern<<<grid, kWarpCtaThreads, ssm, st>>>(reinterpret_cast<const uint32_t *>(in),
                                                                  reinterpret_cast<int32_t *>(out),
@@ -1385,30 +1394,47 @@ __global__ void __launch_bounds__(1024) k_slice_list(const uint8_t *__restrict__
 // slice flags from a grid's touched list (every voxel written since its last
 // reset, so every occupied voxel): a few hundred thousand entries instead of
 // a pass over the whole occupancy array
-__global__ void k_slice_flags_touched(const int32_t *__restrict__ touched, const DevCounters *__restrict__ ctr,
-                                      const uint8_t *__restrict__ occ, long long plane, long long n,
-                                      uint8_t *__restrict__ sflag) {
+__global__ void __launch_bounds__(1024) k_slice_flags_touched(const int32_t *__restrict__ touched,
+                                                             const DevCounters *__restrict__ ctr,
+                                                             const uint8_t *__restrict__ occ, long long plane,
+                                                             long long n, int nx, uint8_t *__restrict__ sflag) {
+    // per-CTA bitmap of slices (nx <= 32768): one global store per slice
+    // and CTA instead of one per occupied voxel on a handful of hot bytes
+    __shared__ unsigned bits[1024];
+    const bool local = nx <= 32768;
+    if (local)
+        for (int w = threadIdx.x; w < (nx + 31) / 32; w += blockDim.x) bits[w] = 0u;
+    __syncthreads();
     const long long nth = (long long)gridDim.x * blockDim.x;
     const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    auto mark = [&](long long v) {
+        const int i = (int)(v / plane);
+        if (local) atomicOr(&bits[i >> 5], 1u << (i & 31));
+        else sflag[i] = 1;
+    };
     if (ctr->overflow) {   // the list is incomplete: scan every voxel
         for (long long v = tid; v < n; v += nth)
-            if (occ[v]) sflag[v / plane] = 1;
-        return;
+            if (occ[v]) mark(v);
+    } else {
+        const int cnt = ctr->touched;
+        for (long long t = tid; t < cnt; t += nth) {
+            const int v = touched[t];
+            if (occ[v]) mark(v);
+        }
     }
-    const int cnt = ctr->touched;
-    for (long long t = tid; t < cnt; t += nth) {
-        const int v = touched[t];
-        if (occ[v]) sflag[v / plane] = 1;
-    }
+    if (!local) return;
+    __syncthreads();
+    for (int w = threadIdx.x; w < (nx + 31) / 32; w += blockDim.x)
+        for (unsigned b = bits[w]; b; b &= b - 1) sflag[w * 32 + __ffs(b) - 1] = 1;
 }
 
 cudaError_t launch_slice_list_touched(const int32_t *touched, const DevCounters *ctr, const uint8_t *occ,
                                       const EdtPlan &p, const SparseRows &sp, cudaStream_t st) {
     cudaError_t e = cudaMemsetAsync(const_cast<uint8_t *>(sp.sflag), 0, (size_t)p.nx, st);
     if (e != cudaSuccess) return e;
-    k_slice_flags_touched<<<2 * num_sms(), 256, 0, st>>>(touched, ctr, occ, (long long)p.ny * p.nz,
-                                                         (long long)p.nx * p.ny * p.nz,
-                                                         const_cast<uint8_t *>(sp.sflag));
+    k_slice_flags_touched<<<std::max(1, num_sms() / 4), 1024, 0, st>>>(
+        touched, ctr, occ, (long long)p.ny * p.nz, (long long)p.nx * p.ny * p.nz, p.nx,
+        const_cast<uint8_t *>(sp.sflag));
     k_slice_list<<<1, 1024, 0, st>>>(sp.sflag, p.nx, const_cast<int *>(sp.xs), const_cast<int *>(sp.hdr),
                                      sp.m_mirror);
     return cudaGetLastError();
@@ -1431,7 +1457,8 @@ int pass3_mode_hint(const EdtPlan &p, int m) {
                             std::max(p.nx - kStreamCap, 0) * 32 * 4;
     const bool ok = p.tma2 && p.tma3 && !p.gstack3 && !p.s2_wide && !p.e3_wide &&
                     p.xb + p.yb + p.zb <= 32 && spill <= (long long)p.s1_bytes &&
-                    ntiles >= 16LL * num_sms();
+                    ntiles >= 16LL * num_sms() &&
+                    (size_t)32 * kStreamCap * 32 * 4 + (size_t)p.nx * 4 <= kSmemLimit;
     if (!ok) return 2;
     const char *sm = getenv("VX_STREAM_MAX");
     const int smax = sm ? atoi(sm) : std::min(kStreamMaxRows, p.nx / 2);

@@ -105,21 +105,31 @@ __global__ void k_scatter(const double *__restrict__ pts, long long npts,
     const long long trips = (n + nth - 1) / nth;
     for (long long it = 0; it < trips; ++it) {
         const long long p = start + it * nth;
-        bool oob = false, skip = false, ins = false;
+        bool oob = false, skip = false, ins = false, first = false;
+        long long lin = -1;
         if (p < n && (!keep || keep[p])) {   // outliers were removed before discretising (grids.py:166-170)
             const double x = pts[3 * p], y = pts[3 * p + 1], z = pts[3 * p + 2];
-            const long long lin = discretize(x, y, z, g);
+            lin = discretize(x, y, z, g);
             if (lin < 0) {
                 oob = true;                                          // grids.py:171
             } else if (mask_cells && mask_cells[lin] > thr) {
                 skip = true;                                         // grids.py:178-182
             } else {
                 ins = true;
-                if (atomicAdd(&counts[lin], 1u) == 0u) {            // first touch
-                    const int slot = atomicAdd(&ctr->pending, 1);
-                    if (base + slot < capacity) touched[base + slot] = (int32_t)lin;
-                    else ctr->overflow = 1;
-                }
+                first = atomicAdd(&counts[lin], 1u) == 0u;          // first touch
+            }
+        }
+        // first touches join the touched list with one atomic per warp
+        const unsigned fm = __ballot_sync(VX_FULL_MASK, first);
+        if (fm) {
+            const int lane = threadIdx.x & 31, leader = __ffs(fm) - 1;
+            int wbase = 0;
+            if (lane == leader) wbase = atomicAdd(&ctr->pending, __popc(fm));
+            wbase = __shfl_sync(VX_FULL_MASK, wbase, leader);
+            if (first) {
+                const int slot = base + wbase + __popc(fm & ((1u << lane) - 1u));
+                if (slot < capacity) touched[slot] = (int32_t)lin;
+                else ctr->overflow = 1;
             }
         }
         warp_count(&ctr->oob, oob);
