@@ -309,10 +309,24 @@ def run_gpu(args, world, rank, local):
         step(s)
     torch.cuda.synchronize()
 
-    # --- device-timed region: inputs resident (the per-step H2D of the
-    # cloud / frames / centres is the only host traffic and is inside the
-    # step; results stay on the device) ---
+    # --- per-phase breakdown: a separate profiled run (event marks between
+    # the phases, so no CUDA graph); not the timed region ---
     _lib.check(L.vx_cycle_profile(cyc._h, 1))
+    for s in range(min(args.steps, 16)):
+        step(args.warmup + s)
+    torch.cuda.synchronize()
+    ph = np.zeros(len(_lib.CYCLE_PHASES), np.float64)
+    nprof = ctypes.c_int()
+    _lib.check(L.vx_cycle_phase_ms(cyc._h, _lib.ptr(ph), ctypes.byref(nprof)))
+    _lib.check(L.vx_cycle_profile(cyc._h, 0))
+    phases = dict(zip(_lib.CYCLE_PHASES, (float(v) for v in ph)))
+    for s in range(2):   # back on the graph path
+        step(args.warmup + s)
+    torch.cuda.synchronize()
+
+    # --- device-timed region: inputs resident (the per-step H2D of the
+    # frames / centres is the only host traffic and is inside the step;
+    # results stay on the device); the tick replays its CUDA graph ---
     launches0 = ctx.launches()
     barrier(world)
     torch.cuda.synchronize()
@@ -327,11 +341,6 @@ def run_gpu(args, world, rank, local):
     barrier(world)
     launches = ctx.launches() - launches0
     t_dev = e0.elapsed_time(e1) / 1e3 / args.steps
-    ph = np.zeros(len(_lib.CYCLE_PHASES), np.float64)
-    nprof = ctypes.c_int()
-    _lib.check(L.vx_cycle_phase_ms(cyc._h, _lib.ptr(ph), ctypes.byref(nprof)))
-    _lib.check(L.vx_cycle_profile(cyc._h, 0))
-    phases = dict(zip(_lib.CYCLE_PHASES, (float(v) for v in ph)))
     t_max = allmax(world, t_dev)
 
     # --- e2e: public API, host inputs and result read-back every step ---
@@ -342,9 +351,15 @@ def run_gpu(args, world, rank, local):
     ev1 = torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
     res = None
+    # each step's cloud is uploaded while the previous tick computes
+    # (MapCycle.prefetch, a copy stream); its results are read back before
+    # the next step is issued
+    cyc.prefetch(host[args.warmup % nsteps_inputs][0].array)
     for s in range(args.steps):
         hp, hf, hc = host[(args.warmup + s) % nsteps_inputs]
         cyc.step(hp.array, hf.array, hc.array, sync=False)
+        if s + 1 < args.steps:
+            cyc.prefetch(host[(args.warmup + s + 1) % nsteps_inputs][0].array)
         res = cyc.wait()
     ev1.record(stream)
     torch.cuda.synchronize()
@@ -393,7 +408,7 @@ def run_gpu(args, world, rank, local):
         "e2e": {"value": world * n / t_e2e_max / 1e9, "unit": "Gvoxel/s",
                 "ms_per_step": t_e2e_max * 1e3, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h,
-                "api": "paper_2407_02363_b200.engine.MapCycle.step + wait (vx_cycle_step/wait)"},
+                "api": "paper_2407_02363_b200.engine.MapCycle.prefetch + step + wait (vx_cycle_prefetch/step/wait; next cloud uploaded during the current tick)"},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
         "last_stats": {k: res[k] for k in ("inserted", "robot_skipped", "out_of_bounds")} if res else None,
@@ -410,7 +425,8 @@ def run_gpu(args, world, rank, local):
 def small_configs(d, steps: int = 20):
     """Configs C1 (128^3, 50k-pt sphere, 30 spheres) and C2 (256^3, 300k-pt
     depth camera): device time per camera tick (inputs resident) and end-to-end
-    time through MapCycle.step + wait (host inputs, results read back)."""
+    time through MapCycle.prefetch + step + wait (host inputs, the next cloud
+    uploaded during the current tick, results read back)."""
     import torch
     from paper_2407_02363_b200 import _lib, synth
     from paper_2407_02363_b200.engine import MapCycle
@@ -456,8 +472,11 @@ def small_configs(d, steps: int = 20):
             pa.array[...] = c
             pinned.append(pa)
         t0 = time.perf_counter()
+        cyc.prefetch(pinned[0].array)
         for s in range(steps):
             cyc.step(pinned[s % 4].array, frames[s % 4], centers[s % 4], sync=False)
+            if s + 1 < steps:
+                cyc.prefetch(pinned[(s + 1) % 4].array)
             cyc.wait()
         e2e_ms = (time.perf_counter() - t0) / steps * 1e3
         out[name] = {"device_ms_per_tick": dev_ms, "e2e_ms_per_tick": e2e_ms,

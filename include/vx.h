@@ -204,6 +204,11 @@ int vx_cycle_step(vx_cycle *c, const double *pts, int64_t npts, const double *li
 int vx_cycle_step_device(vx_cycle *c, const double *d_pts, int64_t npts, const double *link_T,
                          float hit_logodds, double occupancy_threshold, const double *centers,
                          int s, int sync);
+/* Stage the NEXT tick's cloud (pinned host memory, npts points) on a copy
+ * stream while the current tick computes: the next vx_cycle_step called with
+ * the same pointer and count reads the staged copy instead of uploading it.
+ * Two slots; the host buffer must stay unchanged until that step. */
+int vx_cycle_prefetch(vx_cycle *c, const double *pts, int64_t npts);
 int vx_cycle_wait(vx_cycle *c, vx_cycle_result *res, int32_t *site_lin /* 2*s */,
                   double *site_world /* 2*s*3 */, double *dist /* 2*s */);
 /* Per-phase CUDA-event timing of vx_cycle_step (bench evidence).  Phases:

@@ -823,6 +823,8 @@ extern "C" int vx_edt_pass3_device(vx_ctx *c, const void *d_s2, int nx, int ny, 
     return VX_OK;
 }
 
+__global__ void k_set_count(long long *dst, long long v) { *dst = v; }
+
 // ---- camera-tick pipeline (engine.py:233-280) ----------------------------------------
 struct vx_cycle {
     vx_ctx *ctx = nullptr;
@@ -865,6 +867,14 @@ struct vx_cycle {
     // device) -> which pass-3 kernels the next tick launches
     int *h_m = nullptr, *d_m = nullptr;
     int p3_mode = 0, g_mode = -1;
+    // vx_cycle_prefetch: the next cloud is uploaded on a copy stream into one
+    // of two device slots while the current tick computes
+    cudaStream_t cst = nullptr;
+    double *d_pb[2] = {nullptr, nullptr};
+    cudaEvent_t ev_up[2] = {nullptr, nullptr}, ev_used[2] = {nullptr, nullptr};
+    const double *pf_host[2] = {nullptr, nullptr};
+    long long pf_n[2] = {-1, -1};
+    int pf_next = 0;
     cudaGraphExec_t gexec = nullptr;
     int g_s = -1;
     float g_hit = 0.f;
@@ -992,6 +1002,12 @@ extern "C" int vx_cycle_destroy(vx_cycle *cy) {
     cudaFree(cy->d_npts);
     if (cy->h_npts) cudaFreeHost(cy->h_npts);
     if (cy->h_m) cudaFreeHost(cy->h_m);
+    for (int b = 0; b < 2; ++b) {
+        cudaFree(cy->d_pb[b]);
+        if (cy->ev_up[b]) cudaEventDestroy(cy->ev_up[b]);
+        if (cy->ev_used[b]) cudaEventDestroy(cy->ev_used[b]);
+    }
+    if (cy->cst) cudaStreamDestroy(cy->cst);
     if (cy->gexec) cudaGraphExecDestroy(cy->gexec);
     cudaFree(cy->env_f.site);
     cudaFree(cy->self_f.site);
@@ -1091,6 +1107,17 @@ static int cycle_step(vx_cycle *cy, const double *pts, const double *d_pts_in, i
         cy->ring_used = cy->ring_n + 1;
     }
     cy->mark(0);
+    // a cloud staged by vx_cycle_prefetch: the tick reads that device slot
+    int pf_slot = -1;
+    if (npts && pts && !d_pts_in)
+        for (int b = 0; b < 2; ++b)
+            if (cy->pf_host[b] == pts && cy->pf_n[b] == npts) pf_slot = b;
+    if (pf_slot >= 0) {
+        VX_CUDA(cudaStreamWaitEvent(st, cy->ev_up[pf_slot], 0));
+        d_pts_in = cy->d_pb[pf_slot];
+        cy->pf_host[pf_slot] = nullptr;   // consumed
+        cy->pf_n[pf_slot] = -1;
+    }
     // H2D: FK frames of every link, the self subset, the cloud, the centres
     if (cy->nlinks) VX_CUDA(cudaMemcpyAsync(cy->T_all, link_T, 128 * cy->nlinks, cudaMemcpyHostToDevice, st));
     std::vector<double> Ts(16 * cy->nself);
@@ -1122,8 +1149,9 @@ static int cycle_step(vx_cycle *cy, const double *pts, const double *d_pts_in, i
         // cloud into the fixed buffer the graph reads; its size via d_npts
         if (npts && d_pts_in)
             VX_CUDA(cudaMemcpyAsync(cy->d_pts, d_pts_in, (size_t)npts * 24, cudaMemcpyDeviceToDevice, st));
-        *cy->h_npts = npts;
-        VX_CUDA(cudaMemcpyAsync(cy->d_npts, cy->h_npts, sizeof(long long), cudaMemcpyHostToDevice, st));
+        // by-value kernel argument: a later step cannot overwrite it before it runs
+        k_set_count<<<1, 1, 0, st>>>(cy->d_npts, npts);
+        VX_CUDA(cudaGetLastError());
         cy->p3_mode = pass3_mode_hint(cy->plan, *(volatile int *)cy->h_m);
         if (!cy->gexec || cy->g_s != s || cy->g_hit != hit || cy->g_thr != thr || cy->g_mode != cy->p3_mode) {
             if (cy->gexec) cudaGraphExecDestroy(cy->gexec);
@@ -1148,11 +1176,13 @@ static int cycle_step(vx_cycle *cy, const double *pts, const double *d_pts_in, i
             cy->g_hit = hit;
             cy->g_thr = thr;
         }
+        if (pf_slot >= 0) VX_CUDA(cudaEventRecord(cy->ev_used[pf_slot], st));   // slot copied out
         VX_CUDA(cudaGraphLaunch(cy->gexec, st));
         c->launches += cy->g_kernels;
     } else {
         cy->p3_mode = pass3_mode_hint(cy->plan, *(volatile int *)cy->h_m);
         if ((rc = cycle_main_seq(cy, d_pts, npts, nullptr, hit, thr, s, true))) return rc;
+        if (pf_slot >= 0) VX_CUDA(cudaEventRecord(cy->ev_used[pf_slot], st));
     }
     if (cy->profiling && cy->ring_n < vx_cycle::kRing) cy->ring_n++;
     cy->last_s = s;
@@ -1168,6 +1198,33 @@ extern "C" int vx_cycle_step(vx_cycle *cy, const double *pts, int64_t npts, cons
 extern "C" int vx_cycle_step_device(vx_cycle *cy, const double *d_pts, int64_t npts, const double *link_T,
                                     float hit, double thr, const double *centers, int s, int sync) {
     return cycle_step(cy, nullptr, d_pts, npts, link_T, hit, thr, centers, s, sync);
+}
+
+// Stage the next tick's cloud (pinned host memory) on a copy stream while the
+// current tick computes; the next vx_cycle_step with the same pointer and
+// count reads the staged copy.  The host buffer must not change until then.
+extern "C" int vx_cycle_prefetch(vx_cycle *cy, const double *pts, int64_t npts) {
+    if (!cy || npts < 0 || npts > cy->max_points || (npts && !pts))
+        return fail(VX_EINVAL, "bad argument (npts %lld of max %lld)", (long long)npts,
+                    (long long)(cy ? cy->max_points : 0));
+    if (!npts) return VX_OK;
+    if (!cy->cst) {
+        VX_CUDA(cudaStreamCreateWithFlags(&cy->cst, cudaStreamNonBlocking));
+        for (int b = 0; b < 2; ++b) {
+            VX_CUDA(cudaMalloc(&cy->d_pb[b], (size_t)cy->max_points * 24));
+            VX_CUDA(cudaEventCreateWithFlags(&cy->ev_up[b], cudaEventDisableTiming));
+            VX_CUDA(cudaEventCreateWithFlags(&cy->ev_used[b], cudaEventDisableTiming));
+            VX_CUDA(cudaEventRecord(cy->ev_used[b], cy->ctx->stream));
+        }
+    }
+    const int b = cy->pf_next;
+    cy->pf_next ^= 1;
+    VX_CUDA(cudaStreamWaitEvent(cy->cst, cy->ev_used[b], 0));   // the tick that read slot b is past it
+    VX_CUDA(cudaMemcpyAsync(cy->d_pb[b], pts, (size_t)npts * 24, cudaMemcpyHostToDevice, cy->cst));
+    VX_CUDA(cudaEventRecord(cy->ev_up[b], cy->cst));
+    cy->pf_host[b] = pts;
+    cy->pf_n[b] = npts;
+    return VX_OK;
 }
 
 extern "C" int vx_cycle_use_graph(vx_cycle *cy, int enable) {

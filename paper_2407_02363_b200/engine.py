@@ -104,6 +104,15 @@ class MapCycle:
         self._keep = (pts, T, c)   # host buffers must outlive an async copy
         return self
 
+    def prefetch(self, points):
+        """Upload the NEXT tick's cloud while the current one computes
+        (vx_cycle_prefetch).  points must be the pinned array later passed to
+        step() unchanged; it is kept alive here until then."""
+        pts = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 3)
+        _lib.check(_lib.load().vx_cycle_prefetch(self._h, _lib.ptr(pts), pts.shape[0]))
+        self._pf = getattr(self, "_pf", [])[-1:] + [pts]
+        return self
+
     def wait(self):
         """Results of the last step: dict with stats and per-map (lin, world, dist)."""
         res = _lib.CycleResultC()

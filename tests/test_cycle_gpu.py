@@ -106,3 +106,40 @@ def test_graph_and_direct_launch_agree():
         outs.append(res)
         cyc.close()
     assert outs[0] == outs[1]
+
+
+def test_prefetch_matches_plain_step():
+    """vx_cycle_prefetch: the staged cloud gives the same tick as a plain step
+    (and a stale / mismatched prefetch is ignored, not used)."""
+    from paper_2407_02363_b200 import _lib
+    s = synth.C1
+    d = desk7()
+    frames = d["frames"][0]
+    centers = synth.sphere_centers(frames, d["sphere_link"], d["sphere_center"])
+    clouds = []
+    for f in (0, 5, 17):
+        pa = _lib.PinnedArray((s["points"], 3), np.float64)
+        pa.array[...] = synth.c1_cloud(f / 30.0)
+        clouds.append(pa)
+    ref, _ = _c1_cycle()
+    want = []
+    for pa in clouds:
+        ref.step(pa.array, frames, centers)
+        r = ref.wait()
+        fe, _ = ref.fields()
+        want.append((r["inserted"], digest(fe.site), r["env"][2].copy()))
+    cyc, _ = _c1_cycle()
+    cyc.prefetch(clouds[0].array)
+    for q, pa in enumerate(clouds):
+        cyc.step(pa.array, frames, centers, sync=False)
+        if q + 1 < len(clouds):
+            cyc.prefetch(clouds[q + 1].array)
+        r = cyc.wait()
+        fe, _ = cyc.fields()
+        assert (r["inserted"], digest(fe.site)) == want[q][:2], q
+        assert np.array_equal(r["env"][2], want[q][2])
+    # a prefetch of a different buffer does not leak into a step
+    cyc.prefetch(clouds[2].array)
+    cyc.step(clouds[0].array, frames, centers)
+    r = cyc.wait()
+    assert r["inserted"] == want[0][0]
