@@ -825,6 +825,28 @@ extern "C" int vx_edt_pass3_device(vx_ctx *c, const void *d_s2, int nx, int ny, 
 
 __global__ void k_set_count(long long *dst, long long v) { *dst = v; }
 
+// tick results packed into host-mapped memory by the tick itself, so
+// vx_cycle_wait is one stream sync: header {inserted, skipped, oob}, then
+// lin[2s] i32, world[2s*3] f64, dist[2s] f64
+__global__ void k_pack_results(const int32_t *__restrict__ lin, const double *__restrict__ world,
+                               const double *__restrict__ dist, int s, const DevCounters *__restrict__ ctr,
+                               unsigned char *__restrict__ out) {
+    long long *hdr = reinterpret_cast<long long *>(out);
+    if (threadIdx.x == 0) {
+        hdr[0] = (long long)ctr->inserted;
+        hdr[1] = (long long)ctr->skipped;
+        hdr[2] = (long long)ctr->oob;
+    }
+    int32_t *ol = reinterpret_cast<int32_t *>(out + 64);
+    double *ow = reinterpret_cast<double *>(out + 64 + (((size_t)2 * s * 4 + 7) & ~(size_t)7));
+    double *od = ow + (size_t)6 * s;
+    for (int i = threadIdx.x; i < 2 * s; i += blockDim.x) {
+        ol[i] = lin[i];
+        od[i] = dist[i];
+    }
+    for (int i = threadIdx.x; i < 6 * s; i += blockDim.x) ow[i] = world[i];
+}
+
 // ---- camera-tick pipeline (engine.py:233-280) ----------------------------------------
 struct vx_cycle {
     vx_ctx *ctx = nullptr;
@@ -867,6 +889,7 @@ struct vx_cycle {
     // device) -> which pass-3 kernels the next tick launches
     int *h_m = nullptr, *d_m = nullptr;
     int p3_mode = 0, g_mode = -1;
+    unsigned char *h_out = nullptr, *d_out = nullptr;   // packed results (host-mapped)
     // vx_cycle_prefetch: the next cloud is uploaded on a copy stream into one
     // of two device slots while the current tick computes
     cudaStream_t cst = nullptr;
@@ -967,6 +990,9 @@ extern "C" int vx_cycle_create(vx_ctx *c, int nx, int ny, int nz, double vs, con
     if (e == cudaSuccess) e = cudaMalloc(&cy->d_npts, sizeof(long long));
     if (e == cudaSuccess) e = cudaHostAlloc(&cy->h_npts, sizeof(long long), cudaHostAllocPortable);
     if (e == cudaSuccess) e = cudaHostAlloc(&cy->h_m, sizeof(int), cudaHostAllocMapped | cudaHostAllocPortable);
+    if (e == cudaSuccess)
+        e = cudaHostAlloc(&cy->h_out, 64 + 8 + S * 2 * 36, cudaHostAllocMapped | cudaHostAllocPortable);
+    if (e == cudaSuccess) e = cudaHostGetDevicePointer(&cy->d_out, cy->h_out, 0);
     if (e == cudaSuccess) {
         *cy->h_m = -1;
         e = cudaHostGetDevicePointer(&cy->d_m, cy->h_m, 0);
@@ -1002,6 +1028,7 @@ extern "C" int vx_cycle_destroy(vx_cycle *cy) {
     cudaFree(cy->d_npts);
     if (cy->h_npts) cudaFreeHost(cy->h_npts);
     if (cy->h_m) cudaFreeHost(cy->h_m);
+    if (cy->h_out) cudaFreeHost(cy->h_out);
     for (int b = 0; b < 2; ++b) {
         cudaFree(cy->d_pb[b]);
         if (cy->ev_up[b]) cudaEventDestroy(cy->ev_up[b]);
@@ -1089,6 +1116,9 @@ static int cycle_main_seq(vx_cycle *cy, const double *d_pts, long long npts, con
         if (e != cudaSuccess) return cuda_fail(e, "avoidance_rows");
         c->launches += 1;
     }
+    k_pack_results<<<1, 128, 0, st>>>(cy->d_lin, cy->d_world, cy->d_dist, s, cy->env->ctr, cy->d_out);
+    VX_CUDA(cudaGetLastError());
+    c->launches += 1;
     if (marks) cy->mark(8);
     return VX_OK;
 }
@@ -1260,19 +1290,19 @@ extern "C" int vx_cycle_phase_ms(vx_cycle *cy, double *ms, int *nsteps) {
 
 extern "C" int vx_cycle_wait(vx_cycle *cy, vx_cycle_result *res, int32_t *lin, double *world, double *dist) {
     if (!cy) return fail(VX_EINVAL, "NULL cycle");
-    cudaStream_t st = cy->ctx->stream;
+    VX_CUDA(cudaStreamSynchronize(cy->ctx->stream));
+    // the tick packed its results into host-mapped memory (k_pack_results)
     const int s = cy->last_s;
-    if (s && lin) VX_CUDA(cudaMemcpyAsync(lin, cy->d_lin, (size_t)2 * s * 4, cudaMemcpyDeviceToHost, st));
-    if (s && world) VX_CUDA(cudaMemcpyAsync(world, cy->d_world, (size_t)2 * s * 24, cudaMemcpyDeviceToHost, st));
-    if (s && dist) VX_CUDA(cudaMemcpyAsync(dist, cy->d_dist, (size_t)2 * s * 8, cudaMemcpyDeviceToHost, st));
+    const unsigned char *o = cy->h_out;
+    if (s && lin) std::memcpy(lin, o + 64, (size_t)2 * s * 4);
+    const unsigned char *ow = o + 64 + (((size_t)2 * s * 4 + 7) & ~(size_t)7);
+    if (s && world) std::memcpy(world, ow, (size_t)2 * s * 24);
+    if (s && dist) std::memcpy(dist, ow + (size_t)2 * s * 24, (size_t)2 * s * 8);
     if (res) {
-        DevCounters h;
-        VX_CUDA(cudaMemcpyAsync(&h, cy->env->ctr, sizeof h, cudaMemcpyDeviceToHost, st));
-        VX_CUDA(cudaStreamSynchronize(st));
-        res->stats = vx_insert_stats{(int64_t)h.inserted, 0, (int64_t)h.skipped, (int64_t)h.oob};
+        const long long *h = reinterpret_cast<const long long *>(o);
+        res->stats = vx_insert_stats{(int64_t)h[0], 0, (int64_t)h[1], (int64_t)h[2]};
         res->self_recomputed = cy->self_recomputed;
     }
-    VX_CUDA(cudaStreamSynchronize(st));
     return VX_OK;
 }
 
