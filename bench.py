@@ -344,6 +344,10 @@ def run_gpu(args, world, rank, local):
     t_max = allmax(world, t_dev)
 
     # --- e2e: public API, host inputs and result read-back every step ---
+    for s in range(2):   # untimed: the host path's first calls
+        cyc.prefetch(host[s][0].array)
+        cyc.step(host[s][0].array, host[s][1].array, host[s][2].array, sync=False)
+        cyc.wait()
     barrier(world)
     torch.cuda.synchronize()
     t0 = time.perf_counter()

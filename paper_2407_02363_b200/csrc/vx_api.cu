@@ -225,7 +225,7 @@ extern "C" int vx_grid_destroy(vx_grid *g) {
 static int grid_clear_async(vx_grid *g) {
     cudaError_t e = launch_reset(g->cells, g->occ, g->touched, g->ctr, g->n, g->capacity,
                                  !g->sparse_ok, g->ctx->stream);
-    g->ctx->launches += 2;
+    g->ctx->launches += 1;
     if (e != cudaSuccess) return cuda_fail(e, "reset");
     g->sparse_ok = true;
     g->maybe_oor = false;
@@ -261,7 +261,7 @@ static int insert_device(vx_grid *g, const double *d_xyz, long long n, const lon
     e = launch_finalize(g->cells, g->occ, g->counts, g->touched, g->ctr, g->n, g->capacity,
                         n > 0 ? n : 1, hit, kOccThr, st);
     if (e != cudaSuccess) return cuda_fail(e, "finalize");
-    g->ctx->launches += 2;
+    g->ctx->launches += 1;
     return VX_OK;
 }
 
@@ -400,7 +400,7 @@ static int stamp_sets(vx_grid *g, int nsets, const int32_t *d_ijk, const int64_t
                                  value, kOccThr, g->touched, g->ctr, g->set_oob, g->capacity, total,
                                  c->stream);
     if (e != cudaSuccess) return cuda_fail(e, "stamp");
-    c->launches += total > 0 ? 2 : 1;
+    c->launches += 1;
     return VX_OK;
 }
 
@@ -825,28 +825,6 @@ extern "C" int vx_edt_pass3_device(vx_ctx *c, const void *d_s2, int nx, int ny, 
 
 __global__ void k_set_count(long long *dst, long long v) { *dst = v; }
 
-// tick results packed into host-mapped memory by the tick itself, so
-// vx_cycle_wait is one stream sync: header {inserted, skipped, oob}, then
-// lin[2s] i32, world[2s*3] f64, dist[2s] f64
-__global__ void k_pack_results(const int32_t *__restrict__ lin, const double *__restrict__ world,
-                               const double *__restrict__ dist, int s, const DevCounters *__restrict__ ctr,
-                               unsigned char *__restrict__ out) {
-    long long *hdr = reinterpret_cast<long long *>(out);
-    if (threadIdx.x == 0) {
-        hdr[0] = (long long)ctr->inserted;
-        hdr[1] = (long long)ctr->skipped;
-        hdr[2] = (long long)ctr->oob;
-    }
-    int32_t *ol = reinterpret_cast<int32_t *>(out + 64);
-    double *ow = reinterpret_cast<double *>(out + 64 + (((size_t)2 * s * 4 + 7) & ~(size_t)7));
-    double *od = ow + (size_t)6 * s;
-    for (int i = threadIdx.x; i < 2 * s; i += blockDim.x) {
-        ol[i] = lin[i];
-        od[i] = dist[i];
-    }
-    for (int i = threadIdx.x; i < 6 * s; i += blockDim.x) ow[i] = world[i];
-}
-
 // ---- camera-tick pipeline (engine.py:233-280) ----------------------------------------
 struct vx_cycle {
     vx_ctx *ctx = nullptr;
@@ -993,6 +971,15 @@ extern "C" int vx_cycle_create(vx_ctx *c, int nx, int ny, int nz, double vs, con
     if (e == cudaSuccess)
         e = cudaHostAlloc(&cy->h_out, 64 + 8 + S * 2 * 36, cudaHostAllocMapped | cudaHostAllocPortable);
     if (e == cudaSuccess) e = cudaHostGetDevicePointer(&cy->d_out, cy->h_out, 0);
+    // vx_cycle_prefetch slots, copy stream and events (allocated up front so
+    // the first prefetch does not allocate)
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&cy->cst, cudaStreamNonBlocking);
+    for (int b = 0; b < 2 && e == cudaSuccess; ++b) {
+        e = cudaMalloc(&cy->d_pb[b], (size_t)std::max<int64_t>(max_points, 1) * 24);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&cy->ev_up[b], cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&cy->ev_used[b], cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventRecord(cy->ev_used[b], c->stream);
+    }
     if (e == cudaSuccess) {
         *cy->h_m = -1;
         e = cudaHostGetDevicePointer(&cy->d_m, cy->h_m, 0);
@@ -1102,12 +1089,10 @@ static int cycle_main_seq(vx_cycle *cy, const double *d_pts, long long npts, con
     cudaError_t e = edt_passes(cy, cy->env, cy->env_f.site, marks);
     if (e != cudaSuccess) return cuda_fail(e, "edt(env)");
     const GridGeom g = cy->env->g;
-    e = launch_site_world(cy->env_f.site, g, cy->d_centers, s, cy->d_lin, cy->d_world, cy->d_dist, st);
-    if (e == cudaSuccess)
-        e = launch_site_world(cy->self_f.site, g, cy->d_centers, s, cy->d_lin + s, cy->d_world + 3 * s,
-                              cy->d_dist + s, st);
+    e = launch_gather_pack(cy->env_f.site, cy->self_f.site, g, cy->d_centers, s, cy->d_lin, cy->d_world,
+                           cy->d_dist, cy->env->ctr, cy->d_out, st);
     if (e != cudaSuccess) return cuda_fail(e, "site_world");
-    c->launches += s ? 2 : 0;
+    c->launches += 1;
     if (cy->av_s && s == cy->av_s) {
         e = launch_avoidance_rows(cy->d_world, cy->d_dist, cy->d_lin, cy->d_centers, s, cy->d_av_par,
                                   cy->d_av_par + s, cy->d_av_link, cy->d_frames, cy->d_frames + 3 * cy->av_nj,
@@ -1116,9 +1101,6 @@ static int cycle_main_seq(vx_cycle *cy, const double *d_pts, long long npts, con
         if (e != cudaSuccess) return cuda_fail(e, "avoidance_rows");
         c->launches += 1;
     }
-    k_pack_results<<<1, 128, 0, st>>>(cy->d_lin, cy->d_world, cy->d_dist, s, cy->env->ctr, cy->d_out);
-    VX_CUDA(cudaGetLastError());
-    c->launches += 1;
     if (marks) cy->mark(8);
     return VX_OK;
 }
@@ -1238,15 +1220,6 @@ extern "C" int vx_cycle_prefetch(vx_cycle *cy, const double *pts, int64_t npts) 
         return fail(VX_EINVAL, "bad argument (npts %lld of max %lld)", (long long)npts,
                     (long long)(cy ? cy->max_points : 0));
     if (!npts) return VX_OK;
-    if (!cy->cst) {
-        VX_CUDA(cudaStreamCreateWithFlags(&cy->cst, cudaStreamNonBlocking));
-        for (int b = 0; b < 2; ++b) {
-            VX_CUDA(cudaMalloc(&cy->d_pb[b], (size_t)cy->max_points * 24));
-            VX_CUDA(cudaEventCreateWithFlags(&cy->ev_up[b], cudaEventDisableTiming));
-            VX_CUDA(cudaEventCreateWithFlags(&cy->ev_used[b], cudaEventDisableTiming));
-            VX_CUDA(cudaEventRecord(cy->ev_used[b], cy->ctx->stream));
-        }
-    }
     const int b = cy->pf_next;
     cy->pf_next ^= 1;
     VX_CUDA(cudaStreamWaitEvent(cy->cst, cy->ev_used[b], 0));   // the tick that read slot b is past it

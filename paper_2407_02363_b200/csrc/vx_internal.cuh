@@ -91,6 +91,7 @@ struct DevCounters {                // device-resident per-grid bookkeeping
     int pending;                    // new first-touch voxels of the current insert
     int overflow;                   // touched list overflowed -> dense reset
     int dirty;                      // occupancy changed since last EDT (memo)
+    unsigned int done;              // blocks finished (last-block commit of reset/stamp/finalize)
 };
 
 cudaError_t launch_reset(float *cells, uint8_t *occ, int32_t *touched, DevCounters *ctr,
@@ -125,6 +126,10 @@ cudaError_t launch_site_world(const int32_t *site, GridGeom g, const double *cen
                               int s, int32_t *out_lin, double *out_world, double *out_dist,
                               cudaStream_t st);
 
+// the tick's gather on both maps + the packed host-mapped result block
+cudaError_t launch_gather_pack(const int32_t *site_env, const int32_t *site_self, GridGeom g,
+                               const double *centers, int s, int32_t *lin, double *world, double *dist,
+                               const DevCounters *ctr, unsigned char *out, cudaStream_t st);
 // K7: obstacle / self avoidance rows from the K6 outputs of both maps
 cudaError_t launch_avoidance_rows(const double *world, const double *dist, const int32_t *lin,
                                   const double *centers, int s, const double *radius, const double *buffer,

@@ -47,8 +47,26 @@ __device__ __forceinline__ void warp_count(unsigned long long *dst, bool pred) {
     if ((threadIdx.x & 31) == 0 && m) atomicAdd(dst, (unsigned long long)__popc(m));
 }
 
+// true in exactly one thread of the last block to finish: it commits the
+// grid's counters once every block has read them (saves a 1-thread launch)
+__device__ __forceinline__ bool last_block(DevCounters *ctr) {
+    __shared__ bool is_last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        is_last = atomicAdd(&ctr->done, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && is_last) {
+        ctr->done = 0u;
+        __threadfence();
+        return true;
+    }
+    return false;
+}
+
 __global__ void k_reset(float *__restrict__ cells, uint8_t *__restrict__ occ,
-                        const int32_t *__restrict__ touched, const DevCounters *__restrict__ ctr,
+                        const int32_t *__restrict__ touched, DevCounters *__restrict__ ctr,
                         long long n, int dense_req) {
     const bool dense = dense_req || ctr->overflow;
     const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -73,13 +91,12 @@ __global__ void k_reset(float *__restrict__ cells, uint8_t *__restrict__ occ,
             occ[v] = 0;
         }
     }
-}
-
-__global__ void k_reset_commit(DevCounters *ctr) {
-    ctr->touched = 0;
-    ctr->pending = 0;
-    ctr->overflow = 0;
-    ctr->dirty = 1;
+    if (last_block(ctr)) {   // commit
+        ctr->touched = 0;
+        ctr->pending = 0;
+        ctr->overflow = 0;
+        ctr->dirty = 1;
+    }
 }
 
 // clip untouched voxels (only needed after host writes put cells out of
@@ -151,8 +168,8 @@ __device__ __forceinline__ void apply_hits(float *cells, uint8_t *occ, uint32_t 
 
 __global__ void k_finalize(float *__restrict__ cells, uint8_t *__restrict__ occ,
                            uint32_t *__restrict__ counts, const int32_t *__restrict__ touched,
-                           const DevCounters *__restrict__ ctr, long long n, float hit,
-                           float occ_thr) {
+                           DevCounters *__restrict__ ctr, long long n, float hit,
+                           float occ_thr, int capacity) {
     const long long nth = (long long)gridDim.x * blockDim.x;
     const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (ctr->overflow) {  // the touched list is incomplete: scan every voxel
@@ -163,13 +180,12 @@ __global__ void k_finalize(float *__restrict__ cells, uint8_t *__restrict__ occ,
         for (long long t = tid; t < cnt; t += nth)
             apply_hits(cells, occ, counts, touched[base + t], hit, occ_thr);
     }
-}
-
-__global__ void k_finalize_commit(DevCounters *ctr, int capacity) {
-    const long long t = (long long)ctr->touched + ctr->pending;
-    ctr->touched = t > capacity ? capacity : (int)t;
-    ctr->pending = 0;
-    if (ctr->inserted) ctr->dirty = 1;
+    if (last_block(ctr)) {   // commit
+        const long long t = (long long)ctr->touched + ctr->pending;
+        ctr->touched = t > capacity ? capacity : (int)t;
+        ctr->pending = 0;
+        if (ctr->inserted) ctr->dirty = 1;
+    }
 }
 
 __global__ void k_stamp(const int32_t *__restrict__ ijk, const long long *__restrict__ offsets,
@@ -208,9 +224,19 @@ __global__ void k_stamp(const int32_t *__restrict__ ijk, const long long *__rest
         }
         cells[lin] = value;                                           // grids.py:202
         occ[lin] = value > occ_thr ? 1 : 0;
-        const int slot = atomicAdd(&ctr->touched, 1);
+        // one touched-list atomic per warp (lanes that took `continue` are inactive)
+        const unsigned am = __activemask();
+        const int lane = threadIdx.x & 31, leader = __ffs(am) - 1;
+        int wbase = 0;
+        if (lane == leader) wbase = atomicAdd(&ctr->touched, __popc(am));
+        wbase = __shfl_sync(am, wbase, leader);
+        const int slot = wbase + __popc(am & ((1u << lane) - 1u));
         if (slot < capacity) touched[slot] = (int32_t)lin;
         else ctr->overflow = 1;
+    }
+    if (last_block(ctr)) {   // commit
+        if (ctr->touched > capacity) ctr->touched = capacity;
+        ctr->dirty = 1;
     }
 }
 
@@ -242,8 +268,7 @@ cudaError_t launch_reset(float *cells, uint8_t *occ, int32_t *touched, DevCounte
     // the sparse count is only known on the device: size for the dense case
     // when asked, otherwise for a persistent grid-stride sweep
     const unsigned g = dense ? grid_for(n / 4 + 1, 256) : (unsigned)(num_sms() * 4);
-    k_reset<<<g, 256, 0, st>>>(cells, occ, touched, ctr, n, dense ? 1 : 0);
-    k_reset_commit<<<1, 1, 0, st>>>(ctr);
+    k_reset<<<g, 256, 0, st>>>(cells, occ, touched, ctr, n, dense ? 1 : 0);   // commits in its last block
     return cudaGetLastError();
 }
 
@@ -267,8 +292,7 @@ cudaError_t launch_finalize(float *cells, uint8_t *occ, uint32_t *counts, int32_
                             float occ_thr, cudaStream_t st) {
     // a dense (overflow) sweep needs the full grid; otherwise max_new bounds work
     k_finalize<<<grid_for(n < max_new ? n : max_new, 256), 256, 0, st>>>(cells, occ, counts, touched,
-                                                                         ctr, n, hit, occ_thr);
-    k_finalize_commit<<<1, 1, 0, st>>>(ctr, capacity);
+                                                                         ctr, n, hit, occ_thr, capacity);
     return cudaGetLastError();
 }
 
@@ -277,12 +301,13 @@ cudaError_t launch_stamp(const int32_t *ijk, const int64_t *offsets, int nsets,
                          GridGeom g, float *cells, uint8_t *occ, float value, float occ_thr,
                          int32_t *touched, DevCounters *ctr, unsigned long long *oob_per_set,
                          int capacity, int64_t total, cudaStream_t st) {
-    if (total > 0)
+    if (total > 0)   // commits in its last block
         k_stamp<<<grid_for(total, 256), 256, 0, st>>>(ijk, (const long long *)offsets, nsets,
                                                       set_origin, set_vs, T, g, cells, occ, value,
                                                       occ_thr, touched, ctr, oob_per_set, capacity,
                                                       total);
-    k_stamp_commit<<<1, 1, 0, st>>>(ctr, capacity);
+    else
+        k_stamp_commit<<<1, 1, 0, st>>>(ctr, capacity);
     return cudaGetLastError();
 }
 

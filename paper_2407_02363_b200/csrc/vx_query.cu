@@ -27,12 +27,9 @@ __device__ __forceinline__ long long clip_index(double f, int n) {
     return v;
 }
 
-__global__ void k_site_world(const int32_t *__restrict__ site, GridGeom g,
-                             const double *__restrict__ centers, int s,
-                             int32_t *__restrict__ out_lin, double *__restrict__ out_world,
-                             double *__restrict__ out_dist) {
-    const int q = blockIdx.x * blockDim.x + threadIdx.x;
-    if (q >= s) return;
+__device__ __forceinline__ void site_world_one(const int32_t *__restrict__ site, const GridGeom &g,
+                                               const double *__restrict__ centers, int q, int32_t *out_lin,
+                                               double *out_world, double *out_dist) {
     const double cx = centers[3 * q], cy = centers[3 * q + 1], cz = centers[3 * q + 2];
     const long long i = clip_index(floor(__ddiv_rn(__dsub_rn(cx, g.ox), g.vs)), g.nx);
     const long long j = clip_index(floor(__ddiv_rn(__dsub_rn(cy, g.oy), g.vs)), g.ny);
@@ -56,7 +53,51 @@ __global__ void k_site_world(const int32_t *__restrict__ site, GridGeom g,
     out_dist[q] = sqrt(dx * dx + dy * dy + dz * dz);
 }
 
+__global__ void k_site_world(const int32_t *__restrict__ site, GridGeom g,
+                             const double *__restrict__ centers, int s,
+                             int32_t *__restrict__ out_lin, double *__restrict__ out_world,
+                             double *__restrict__ out_dist) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= s) return;
+    site_world_one(site, g, centers, q, out_lin, out_world, out_dist);
+}
+
+// the camera tick's gather: both maps in one launch (row r = map * s +
+// sphere), device copies for the avoidance rows, and the packed host-mapped
+// result block {inserted, skipped, oob | lin[2s] | world[2s*3] | dist[2s]}
+__global__ void k_gather_pack(const int32_t *__restrict__ site_env, const int32_t *__restrict__ site_self,
+                              GridGeom g, const double *__restrict__ centers, int s,
+                              int32_t *__restrict__ lin, double *__restrict__ world, double *__restrict__ dist,
+                              const DevCounters *__restrict__ ctr, unsigned char *__restrict__ out) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r == 0) {
+        long long *hdr = reinterpret_cast<long long *>(out);
+        hdr[0] = (long long)ctr->inserted;
+        hdr[1] = (long long)ctr->skipped;
+        hdr[2] = (long long)ctr->oob;
+    }
+    if (r >= 2 * s) return;
+    const int m = r >= s ? 1 : 0, q = r - m * s;
+    site_world_one(m ? site_self : site_env, g, centers, q, lin + m * s, world + 3 * m * s, dist + m * s);
+    int32_t *ol = reinterpret_cast<int32_t *>(out + 64);
+    double *ow = reinterpret_cast<double *>(out + 64 + (((size_t)2 * s * 4 + 7) & ~(size_t)7));
+    double *od = ow + (size_t)6 * s;
+    ol[r] = lin[r];
+    ow[3 * r] = world[3 * r];
+    ow[3 * r + 1] = world[3 * r + 1];
+    ow[3 * r + 2] = world[3 * r + 2];
+    od[r] = dist[r];
+}
+
 }  // namespace
+
+cudaError_t launch_gather_pack(const int32_t *site_env, const int32_t *site_self, GridGeom g,
+                               const double *centers, int s, int32_t *lin, double *world, double *dist,
+                               const DevCounters *ctr, unsigned char *out, cudaStream_t st) {
+    k_gather_pack<<<(2 * s + 127) / 128 + (s ? 0 : 1), 128, 0, st>>>(site_env, site_self, g, centers, s, lin,
+                                                                     world, dist, ctr, out);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_site_world(const int32_t *site, GridGeom g, const double *centers, int s,
                               int32_t *out_lin, double *out_world, double *out_dist,
