@@ -116,6 +116,9 @@ __global__ void k_scatter(const double *__restrict__ pts, long long npts,
                           DevCounters *__restrict__ ctr, int capacity, const uint8_t *__restrict__ keep) {
     const long long n = npts_dev ? *npts_dev : npts;
     const int base = ctr->touched;
+    __shared__ int s_cnt, s_base;
+    if (threadIdx.x == 0) s_cnt = 0;
+    __syncthreads();
     const long long nth = (long long)gridDim.x * blockDim.x;
     const long long start = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     // uniform trip count so the warp-aggregated counters see full warps
@@ -136,19 +139,25 @@ __global__ void k_scatter(const double *__restrict__ pts, long long npts,
                 first = atomicAdd(&counts[lin], 1u) == 0u;          // first touch
             }
         }
-        // first touches join the touched list with one atomic per warp
+        // first touches join the touched list with one global atomic per block
+        // (a per-warp atomic on the one counter serialised ~10k requests)
         const unsigned fm = __ballot_sync(VX_FULL_MASK, first);
-        if (fm) {
-            const int lane = threadIdx.x & 31, leader = __ffs(fm) - 1;
-            int wbase = 0;
-            if (lane == leader) wbase = atomicAdd(&ctr->pending, __popc(fm));
-            wbase = __shfl_sync(VX_FULL_MASK, wbase, leader);
-            if (first) {
-                const int slot = base + wbase + __popc(fm & ((1u << lane) - 1u));
-                if (slot < capacity) touched[slot] = (int32_t)lin;
-                else ctr->overflow = 1;
-            }
+        const int lane = threadIdx.x & 31;
+        int wofs = 0;
+        if (lane == 0 && fm) wofs = atomicAdd(&s_cnt, __popc(fm));
+        wofs = __shfl_sync(VX_FULL_MASK, wofs, 0);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            s_base = s_cnt ? atomicAdd(&ctr->pending, s_cnt) : 0;
+            s_cnt = 0;
         }
+        __syncthreads();
+        if (first) {
+            const int slot = base + s_base + wofs + __popc(fm & ((1u << lane) - 1u));
+            if (slot < capacity) touched[slot] = (int32_t)lin;
+            else ctr->overflow = 1;
+        }
+        __syncthreads();   // s_base is rewritten next iteration
         warp_count(&ctr->oob, oob);
         warp_count(&ctr->skipped, skip);
         warp_count(&ctr->inserted, ins);
