@@ -200,8 +200,22 @@ __global__ void __launch_bounds__(256) k_pass1_v4(const uint8_t *__restrict__ oc
         }
     }
 #pragma unroll
-    for (int l = 0; l < LPW; ++l)
-        if (act[l]) pass1_line<CMAX>(nib[l], reinterpret_cast<int4 *>(s1 + lines[l] * nz), nq, lane);
+    for (int l = 0; l < LPW; ++l) {
+        if (!act[l]) continue;
+        int4 *dst = reinterpret_cast<int4 *>(s1 + lines[l] * nz);
+        uint32_t any = 0;
+#pragma unroll
+        for (int c = 0; c < CMAX; ++c) any |= nib[l][c];
+        if (!__any_sync(VX_FULL_MASK, any != 0u)) {   // empty line: no site anywhere (edt.py:212)
+#pragma unroll
+            for (int c = 0; c < CMAX; ++c) {
+                const int q = c * 32 + lane;
+                if (q < nq) dst[q] = make_int4(-1, -1, -1, -1);
+            }
+            continue;
+        }
+        pass1_line<CMAX>(nib[l], dst, nq, lane);
+    }
 }
 
 // Pass 1, generic path (any nz): 32-voxel chunks with ballots; the forward
