@@ -238,3 +238,62 @@ def test_monotonicity_adding_sites():                # test_edt.py:106-114
     free = np.argwhere(~occ)
     occ[tuple(free[rng.integers(0, free.shape[0])])] = True
     assert (pba_edt(occ).sq_distance_grid() <= sq).all()
+
+
+def _stream_grid(seed, deep):
+    """(256, 512, 160): 2560 pass-3 tiles (>= 16 per SM) and m <= L/2 occupied
+    slices, so pass 3 takes the one-warp kernel.  deep: every occupied slice
+    carries the same sites, so every column's hull keeps all m candidates
+    (m > the 55 shared-memory entries: the global spill path)."""
+    rng = np.random.default_rng(seed)
+    occ = np.zeros((256, 512, 160), np.uint8)
+    xs = np.sort(rng.choice(256, 100 if deep else 60, replace=False))
+    if deep:
+        pts = rng.integers(0, [512, 160], size=(40, 2))
+        for x in xs:
+            occ[x, pts[:, 0], pts[:, 1]] = 1
+    else:
+        for x in xs:
+            occ[x][rng.random((512, 160)) < 0.002] = 1
+    return occ
+
+
+@pytest.mark.parametrize("deep", [False, True], ids=["shallow", "deep-spill"])
+def test_pass3_one_warp_kernel_vs_oracle(deep, monkeypatch):
+    """k_pass3_stream (few occupied slices, many tiles), with and without
+    stack spills, bit-identical to the oracle and to the banded kernel."""
+    occ = _stream_grid(5, deep)
+    want = O.pba_edt_site(occ)
+    got = pba_edt(occ).site
+    assert np.array_equal(got, want)
+    monkeypatch.setenv("VX_STREAM_MAX", "-1")   # banded kernel only
+    assert np.array_equal(pba_edt(occ).site, want)
+
+
+def test_cycle_pass3_kernel_choice(monkeypatch):
+    """The camera tick picks its pass-3 kernel from the previous tick's
+    occupied-slice count (host-mapped hint); every choice, and every switch
+    between them (graph re-capture), gives the field of a plain EDT."""
+    from paper_2407_02363_b200.engine import MapCycle
+    dims, vs, origin = (256, 512, 160), 0.02, (-2.56, -5.12, -0.2)
+    rng = np.random.default_rng(7)
+    cyc = MapCycle(dims, vs, origin, [], vs, [], max_points=40000, max_spheres=4)
+    centers = np.zeros((4, 3))
+    for t, smax in enumerate([None, None, None, "10", "10", None]):
+        if smax is None:
+            monkeypatch.delenv("VX_STREAM_MAX", raising=False)
+        else:
+            monkeypatch.setenv("VX_STREAM_MAX", smax)   # forces the banded choice
+        # points in ~40 i-slices
+        xs = rng.choice(256, 40, replace=False)
+        i = rng.choice(xs, 40000)
+        pts = np.stack([origin[0] + (i + rng.random(40000)) * vs,
+                        origin[1] + rng.random(40000) * 512 * vs,
+                        origin[2] + rng.random(40000) * 160 * vs], axis=1)
+        cyc.step(pts, np.zeros((0, 16)), centers)
+        cyc.wait()
+        env, _, _ = cyc.grids()
+        fe, _ = cyc.fields()
+        occ = env.occupancy_mask()
+        monkeypatch.setenv("VX_STREAM_MAX", "-1")
+        assert np.array_equal(fe.site, pba_edt(occ).site), t
