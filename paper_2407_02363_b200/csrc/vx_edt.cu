@@ -835,7 +835,10 @@ __global__ void __launch_bounds__(kColThreads, kColMinBlocks) k_column_gstack(co
     }
 }
 
-constexpr int kWarpCtaThreads = 1024;
+#ifndef VX_STREAM_WARPS
+#define VX_STREAM_WARPS 32
+#endif
+constexpr int kWarpCtaThreads = 32 * VX_STREAM_WARPS;   // k_pass3_stream CTA: one per SM
 
 // ---- pass 3 with one warp per tile (few occupied slices) ----------------------
 // A warp owns a whole 32-column tile: the m candidate rows (occupied slices,
@@ -1146,14 +1149,14 @@ cudaError_t launch_col(const void *in, void *out, void *gstack, const EdtPlan &p
                     // few occupied slices: one warp per tile (k_pass3_stream) when
                     // m <= stream_max, decided on the device; s1 (gstack here) is
                     // its spill slab
-                    const long long spill = std::min<long long>(P.ntiles, (long long)num_sms() * 32) *
+                    const long long spill = std::min<long long>(P.ntiles, (long long)num_sms() * VX_STREAM_WARPS) *
                                             std::max(P.L - kStreamCap, 0) * 32 * 4;
                     // only with tiles enough for >= 16 warps per SM: each warp walks
                     // its tile alone, so small grids keep the banded kernel
                     const char *xw = getenv("VX_STREAM_XW");
                     const bool use_xw = xw && atoi(xw) != 0 && p.xb + p.wb <= 32;   // re-read variant: slower here
                     const int mode = sp ? sp->p3_mode : 0;
-                    const size_t ssm = (size_t)32 * kStreamCap * 32 * 4 + (size_t)P.L * 4;   // stacks + row list
+                    const size_t ssm = (size_t)VX_STREAM_WARPS * kStreamCap * 32 * 4 + (size_t)P.L * 4;   // stacks + row list
                     if (mode != 2 && cmp && gstack && (use_xw || p.xb + p.yb + p.zb <= 32) &&
                         spill <= (long long)p.s1_bytes && P.ntiles >= 16LL * num_sms() && ssm <= kSmemLimit) {
                         const char *sm = getenv("VX_STREAM_MAX");
@@ -1161,7 +1164,7 @@ cudaError_t launch_col(const void *in, void *out, void *gstack, const EdtPlan &p
                         auto kern = use_xw ? k_pass3_stream<typename C::FT, true> : k_pass3_stream<typename C::FT, false>;
                         cudaError_t e = allow_smem(kern);
                         if (e != cudaSuccess) return e;
-                        const unsigned grid = (unsigned)std::min<long long>((P.ntiles + 31) / 32, num_sms());
+                        const unsigned grid = (unsigned)std::min<long long>((P.ntiles + VX_STREAM_WARPS - 1) / VX_STREAM_WARPS, num_sms());
                         kern<<<grid, kWarpCtaThreads, ssm, st>>>(reinterpret_cast<const uint32_t *>(in),
                                                                  reinterpret_cast<int32_t *>(out),
                                                                  reinterpret_cast<uint32_t *>(gstack), P);
@@ -1467,12 +1470,12 @@ cudaError_t launch_slice_list(const uint8_t *occ, const EdtPlan &p, const Sparse
 int pass3_mode_hint(const EdtPlan &p, int m) {
     if (m < 0) return 0;
     const long long ntiles = (long long)((p.nz + 31) / 32) * p.ny;
-    const long long spill = std::min<long long>(ntiles, (long long)num_sms() * 32) *
+    const long long spill = std::min<long long>(ntiles, (long long)num_sms() * VX_STREAM_WARPS) *
                             std::max(p.nx - kStreamCap, 0) * 32 * 4;
     const bool ok = p.tma2 && p.tma3 && !p.gstack3 && !p.s2_wide && !p.e3_wide &&
                     p.xb + p.yb + p.zb <= 32 && spill <= (long long)p.s1_bytes &&
                     ntiles >= 16LL * num_sms() &&
-                    (size_t)32 * kStreamCap * 32 * 4 + (size_t)p.nx * 4 <= kSmemLimit;
+                    (size_t)VX_STREAM_WARPS * kStreamCap * 32 * 4 + (size_t)p.nx * 4 <= kSmemLimit;
     if (!ok) return 2;
     const char *sm = getenv("VX_STREAM_MAX");
     const int smax = sm ? atoi(sm) : std::min(kStreamMaxRows, p.nx / 2);
