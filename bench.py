@@ -375,6 +375,7 @@ def run_gpu(args, world, rank, local):
 
     # config C4 (all ranks: data-parallel scene batch, max over ranks)
     c4 = None if args.no_sweep else c4_batch(ctx, stream, rank, world)
+    c5 = None if args.no_sweep else c5_slab(rank, world)
     if rank != 0:
         return
     peak, peak_src = peaks()
@@ -421,6 +422,8 @@ def run_gpu(args, world, rank, local):
     }
     if c4 is not None:
         line["c4_batch_64x256^3"] = c4
+    if c5 is not None:
+        line["c5_slab_1024^3"] = c5
     if not args.no_sweep:
         line["edt_sweep"] = edt_sweep(ctx, stream)
         line["small_configs"] = small_configs(d)
@@ -591,6 +594,40 @@ def c4_batch(ctx, stream, rank: int, world: int):
     return {"scenes": per * world, "scenes_per_gpu": per, "ms": t * 1e3, "gvoxel_s": vox / t / 1e9,
             "hbm_frac": EDT_BYTES_PER_VOXEL * vox / t / 1e9 / peaks()[0],
             "occupancy": "Bernoulli(0.02) per scene", "scaling": "strong (64 scenes total)"}
+
+
+def c5_slab(rank: int, world: int):
+    """Config C5: one 1024^3 grid slab-decomposed across the ranks (i-slabs;
+    passes 1-2 local, the pass-2 epilogue writes the j-slab transpose into the
+    NCCL all-to-all send blocks, pass 3 on the received j-slab).  Strong
+    scaling: the whole grid is fixed, time = max over ranks of the device time
+    of one SlabEDT call.  Bernoulli(0.02) occupancy generated on the device."""
+    import torch
+    from paper_2407_02363_b200.slab import SlabEDT, even_split
+    n = 1024
+    i0, i1 = even_split(n, world)[rank], even_split(n, world)[rank + 1]
+    g = torch.Generator(device="cuda")
+    g.manual_seed(77 + rank)
+    occ = (torch.rand((i1 - i0, n, n), generator=g, device="cuda") < 0.02).to(torch.uint8)
+    slab = SlabEDT((n, n, n), exchange="nccl")
+    for _ in range(2):
+        slab(occ)
+    torch.cuda.synchronize()
+    barrier(world)
+    reps = 3
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        slab(occ)
+    e1.record()
+    torch.cuda.synchronize()
+    t = allmax(world, e0.elapsed_time(e1) / 1e3 / reps)
+    del occ, slab
+    torch.cuda.empty_cache()
+    return {"ranks": world, "ms": t * 1e3, "gvoxel_s": n ** 3 / t / 1e9,
+            "hbm_frac_per_gpu": EDT_BYTES_PER_VOXEL * n ** 3 / world / t / 1e9 / peaks()[0],
+            "exchange": "nccl all_to_all_single (pass-2 epilogue writes the send blocks)",
+            "occupancy": "Bernoulli(0.02), generated on the device", "scaling": "strong (one 1024^3 grid)"}
 
 
 def main():
