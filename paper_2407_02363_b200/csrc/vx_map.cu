@@ -17,6 +17,8 @@
 // does on this image: fma(c2, r2, fma(c1, r1, c0*r0)) + t.
 #include "vx_internal.cuh"
 
+#include <algorithm>
+
 namespace vx {
 namespace {
 
@@ -299,8 +301,11 @@ cudaError_t launch_scatter(const double *pts, int64_t npts, const int64_t *npts_
 cudaError_t launch_finalize(float *cells, uint8_t *occ, uint32_t *counts, int32_t *touched,
                             DevCounters *ctr, int64_t n, int capacity, int64_t max_new, float hit,
                             float occ_thr, cudaStream_t st) {
-    // a dense (overflow) sweep needs the full grid; otherwise max_new bounds work
-    k_finalize<<<grid_for(n < max_new ? n : max_new, 256), 256, 0, st>>>(cells, occ, counts, touched,
+    // grid-stride over the new touched entries (<= max_new; a dense overflow
+    // sweep loops): few blocks, so the last-block commit's atomic is cheap
+    const long long work = n < max_new ? n : max_new;
+    const unsigned gf = (unsigned)std::min<long long>(grid_for(work, 256), 2LL * num_sms());
+    k_finalize<<<gf, 256, 0, st>>>(cells, occ, counts, touched,
                                                                          ctr, n, hit, occ_thr, capacity);
     return cudaGetLastError();
 }
