@@ -1,3 +1,3 @@
-timeout 900 python -m pytest tests/test_cycle_gpu.py tests/test_grids_gpu.py tests/test_engine_dropin_gpu.py -x -q 2>&1 | tail -1
-for i in 1 2; do python bench.py --no-cpu-baseline --no-sweep 2>&1 | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print(d['ms_per_step'], d['e2e']['ms_per_step'], d['phase_ms']['scatter'])"; done
-ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_finalize|k_reset|k_scatter" -c 30 --csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-sweep 2>/dev/null | grep -oE "(k_finalize|k_reset|k_scatter)[^\"]*\",\"[^\"]*\",\"[^\"]*\",\"[0-9.]*\"$" | awk -F'","' '{print $1, $NF}' | tail -8
+python -c "
+import numpy as np; rng=np.random.default_rng(0); (rng.random((1024,1024,1024),dtype=np.float32)<0.02).astype(np.uint8).tofile('/tmp/b1024.raw')"
+tools/pt_base /tmp/b1024.raw 1024 1024 1024 2>&1 | grep -E "kernel|pass"
