@@ -854,7 +854,7 @@ constexpr int kWarpCtaThreads = 32 * VX_STREAM_WARPS;   // k_pass3_stream CTA: o
 // k_column_tma (launched right after it) does the pass.
 constexpr int kStreamCap = VX_STREAM_CAP;
 
-template <typename FT, bool XW>
+template <typename FT>
 __global__ void __launch_bounds__(kWarpCtaThreads, 1) k_pass3_stream(const uint32_t *__restrict__ in,
                                                                      int32_t *__restrict__ out,
                                                                      uint32_t *__restrict__ ovf, const ColParams P) {
@@ -875,10 +875,9 @@ __global__ void __launch_bounds__(kWarpCtaThreads, 1) k_pass3_stream(const uint3
         if (i < kStreamCap) sst[i * 32] = e;
         else gst[(long long)i * 32] = e;
     };
-    // entry: XW (x << wb) | w with w = (j-y)^2 + (k-z)^2, F = x^2 + w (the
-    // winner's s2 code is re-read from the input); else (x << yzb) | code
-    const uint32_t eb = XW ? (uint32_t)P.wb : (uint32_t)P.yzb;
-    const uint32_t zb = (uint32_t)P.zb, zmask = P.zmask, ymask = P.ymask, wmask = P.wmask;
+    // entry: (x << yzb) | s2 code (y << zb | z); F = x^2 + (j - y)^2 + (k - z)^2
+    const uint32_t eb = (uint32_t)P.yzb;
+    const uint32_t zb = (uint32_t)P.zb, zmask = P.zmask, ymask = P.ymask;
     const long long plane = P.plane, splane = P.splane;
     const int nz = P.nz, L = P.L;
     constexpr FT kNever = sizeof(FT) == 4 ? (FT)0x7fffffff : (FT)0x7fffffffffffffffLL;
@@ -901,15 +900,14 @@ __global__ void __launch_bounds__(kWarpCtaThreads, 1) k_pass3_stream(const uint3
         };
         auto Fof = [&](uint32_t e) -> FT {
             const FT x = (FT)(int)(e >> eb);
-            if constexpr (XW) return x * x + (FT)(e & wmask);
-            else return x * x + wof(e);
+            return x * x + wof(e);
         };
         int n = 0, ya = 0, yb = 0;
         FT Fa = 0, Fb = 0;
         auto consume = [&](uint32_t v, int yc) {
             if (v == 0xffffffffu) return;
             const FT wc = wof(v);
-            const uint32_t ec = ((uint32_t)yc << eb) | (XW ? (uint32_t)wc : v);
+            const uint32_t ec = ((uint32_t)yc << eb) | v;
             const FT Fc = (FT)yc * (FT)yc + wc;
             while (n >= 2 && dominated<FT>(ya, Fa, yb, Fb, yc, Fc)) {
                 --n;
@@ -960,39 +958,31 @@ __global__ void __launch_bounds__(kWarpCtaThreads, 1) k_pass3_stream(const uint3
         if (n == 0) {
             for (int y = 0; y < L; ++y, dst += splane) *dst = -1;
         } else {
-            auto site_of = [&](uint32_t e, uint32_t code) -> int32_t {
+            auto site_of = [&](uint32_t e) -> int32_t {   // edt.py:417
                 const long long x = (long long)(e >> eb);
-                const uint32_t c = XW ? code : e;
-                return (int32_t)(x * plane + (long long)((c >> zb) & ymask) * nz + (long long)(c & zmask));
-            };
-            auto code_of = [&](uint32_t e) -> uint32_t {   // XW: the s2 code at the entry's row
-                if constexpr (XW) return __ldg(src + (long long)(e >> eb) * splane);
-                else return 0u;
+                return (int32_t)(x * plane + (long long)((e >> zb) & ymask) * nz + (long long)(e & zmask));
             };
             int pos = 0;
             uint32_t cur = ent(0);
             int yc = (int)(cur >> eb);
             FT Fc = Fof(cur);
-            int32_t ocur = site_of(cur, code_of(cur));
+            int32_t ocur = site_of(cur);
             bool has = n > 1;
-            uint32_t sent = 0, scode = 0;
+            uint32_t sent = 0;
             int ys = 0;
             FT Fs = 0;
             if (has) {
                 sent = ent(1);
                 ys = (int)(sent >> eb);
                 Fs = Fof(sent);
-                scode = code_of(sent);   // prefetched for the advance
             }
             FT dN = has ? Fs - Fc : kNever;
             FT tt = has ? (FT)2 * (FT)(ys - yc) : (FT)0;
             FT rhs = 0;
             for (int y = 0; y < L; ++y) {
                 if (dN < rhs) {   // successor strictly closer at row y (edt.py:311)
-                    uint32_t ccode;
                     do {
                         cur = sent;
-                        ccode = scode;
                         yc = ys;
                         Fc = Fs;
                         ++pos;
@@ -1001,10 +991,9 @@ __global__ void __launch_bounds__(kWarpCtaThreads, 1) k_pass3_stream(const uint3
                             sent = ent(pos + 1);
                             ys = (int)(sent >> eb);
                             Fs = Fof(sent);
-                            scode = code_of(sent);
                         }
                     } while (has && better<FT>(ys, Fs, yc, Fc, y));
-                    ocur = site_of(cur, ccode);
+                    ocur = site_of(cur);
                     dN = has ? Fs - Fc : kNever;
                     tt = has ? (FT)2 * (FT)(ys - yc) : (FT)0;
                     rhs = (FT)y * tt;
@@ -1153,15 +1142,13 @@ cudaError_t launch_col(const void *in, void *out, void *gstack, const EdtPlan &p
                                             std::max(P.L - kStreamCap, 0) * 32 * 4;
                     // only with tiles enough for >= 16 warps per SM: each warp walks
                     // its tile alone, so small grids keep the banded kernel
-                    const char *xw = getenv("VX_STREAM_XW");
-                    const bool use_xw = xw && atoi(xw) != 0 && p.xb + p.wb <= 32;   // re-read variant: slower here
                     const int mode = sp ? sp->p3_mode : 0;
                     const size_t ssm = (size_t)VX_STREAM_WARPS * kStreamCap * 32 * 4 + (size_t)P.L * 4;   // stacks + row list
-                    if (mode != 2 && cmp && gstack && (use_xw || p.xb + p.yb + p.zb <= 32) &&
+                    if (mode != 2 && cmp && gstack && p.xb + p.yb + p.zb <= 32 &&
                         spill <= (long long)p.s1_bytes && P.ntiles >= 16LL * num_sms() && ssm <= kSmemLimit) {
                         const char *sm = getenv("VX_STREAM_MAX");
                         P.stream_max = mode == 1 ? 0x7fffffff : sm ? atoi(sm) : std::min(kStreamMaxRows, P.L / 2);
-                        auto kern = use_xw ? k_pass3_stream<typename C::FT, true> : k_pass3_stream<typename C::FT, false>;
+                        auto kern = k_pass3_stream<typename C::FT>;
                         cudaError_t e = allow_smem(kern);
                         if (e != cudaSuccess) return e;
                         const unsigned grid = (unsigned)std::min<long long>((P.ntiles + VX_STREAM_WARPS - 1) / VX_STREAM_WARPS, num_sms());
