@@ -1065,8 +1065,12 @@ cudaError_t allow_smem(K kern) {
     const auto key = std::make_pair(reinterpret_cast<const void *>(kern), dev);
     std::lock_guard<std::mutex> lock(mu);
     if (done.count(key)) return cudaSuccess;
-    const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               (int)kSmemLimit);
+    // static shared memory counts against the same 227 KB
+    cudaFuncAttributes fa;
+    cudaError_t e = cudaFuncGetAttributes(&fa, kern);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(kSmemLimit - fa.sharedSizeBytes));
     if (e == cudaSuccess) done.insert(key);
     return e;
 }
