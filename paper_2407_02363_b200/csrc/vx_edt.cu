@@ -854,6 +854,16 @@ constexpr int kWarpCtaThreads = 32 * VX_STREAM_WARPS;   // k_pass3_stream CTA: o
 // k_column_tma (launched right after it) does the pass.
 constexpr int kStreamCap = VX_STREAM_CAP;
 
+// the one-warp pass 3 needs enough tiles to keep its warps busy: each walks its
+// tile alone (VX_STREAM_MIN_TILES overrides; default 16 per SM)
+inline long long stream_min_tiles() {
+    static const long long v = [] {
+        const char *e = getenv("VX_STREAM_MIN_TILES");
+        return e ? atoll(e) : 16LL * num_sms();
+    }();
+    return v;
+}
+
 template <typename FT>
 __global__ void __launch_bounds__(kWarpCtaThreads, 1) k_pass3_stream(const uint32_t *__restrict__ in,
                                                                      int32_t *__restrict__ out,
@@ -1149,7 +1159,7 @@ cudaError_t launch_col(const void *in, void *out, void *gstack, const EdtPlan &p
                     const int mode = sp ? sp->p3_mode : 0;
                     const size_t ssm = (size_t)VX_STREAM_WARPS * kStreamCap * 32 * 4 + (size_t)P.L * 4;   // stacks + row list
                     if (mode != 2 && cmp && gstack && p.xb + p.yb + p.zb <= 32 &&
-                        spill <= (long long)p.s1_bytes && P.ntiles >= 16LL * num_sms() && ssm <= kSmemLimit) {
+                        spill <= (long long)p.s1_bytes && P.ntiles >= (long long)stream_min_tiles() && ssm <= kSmemLimit) {
                         const char *sm = getenv("VX_STREAM_MAX");
                         P.stream_max = mode == 1 ? 0x7fffffff : sm ? atoi(sm) : std::min(kStreamMaxRows, P.L / 2);
                         auto kern = k_pass3_stream<typename C::FT>;
@@ -1465,7 +1475,7 @@ int pass3_mode_hint(const EdtPlan &p, int m) {
                             std::max(p.nx - kStreamCap, 0) * 32 * 4;
     const bool ok = p.tma2 && p.tma3 && !p.gstack3 && !p.s2_wide && !p.e3_wide &&
                     p.xb + p.yb + p.zb <= 32 && spill <= (long long)p.s1_bytes &&
-                    ntiles >= 16LL * num_sms() &&
+                    ntiles >= (long long)stream_min_tiles() &&
                     (size_t)VX_STREAM_WARPS * kStreamCap * 32 * 4 + (size_t)p.nx * 4 <= kSmemLimit;
     if (!ok) return 2;
     const char *sm = getenv("VX_STREAM_MAX");
