@@ -89,6 +89,8 @@ struct vx_grid {
     int capacity = 0;
     bool sparse_ok = true;          // touched list covers every non-zero cell
     bool maybe_oor = false;         // host wrote cells outside [L_MIN, L_MAX] or NaN
+    bool fresh = false;             // every cell is +0.0f (reset, nothing written since):
+                                    // an insert may count hits in the cells themselves
 };
 
 struct vx_field {
@@ -229,6 +231,7 @@ static int grid_clear_async(vx_grid *g) {
     if (e != cudaSuccess) return cuda_fail(e, "reset");
     g->sparse_ok = true;
     g->maybe_oor = false;
+    g->fresh = true;
     return VX_OK;
 }
 
@@ -249,8 +252,13 @@ static int insert_device(vx_grid *g, const double *d_xyz, long long n, const lon
     cudaStream_t st = g->ctx->stream;
     VX_CUDA(cudaMemsetAsync(g->ctr, 0, 3 * sizeof(unsigned long long), st));
     const float thr32 = (float)logit(thr);  // numpy compares in float32
+    // a fresh grid counts hits in its own (zero) cells: finalize then reads one
+    // array per touched voxel instead of two and has no counts to clear
+    const bool fresh = g->fresh && !g->maybe_oor;
+    uint32_t *counts = fresh ? reinterpret_cast<uint32_t *>(g->cells) : g->counts;
+    g->fresh = false;
     cudaError_t e = launch_scatter(d_xyz, n, (const int64_t *)n_dev, g->g, mask ? mask->cells : nullptr,
-                                   thr32, g->counts, g->touched, g->ctr, g->capacity, st, keep);
+                                   thr32, counts, g->touched, g->ctr, g->capacity, st, keep);
     if (e != cudaSuccess) return cuda_fail(e, "scatter");
     g->ctx->launches += 1;
     if (g->maybe_oor) {
@@ -258,8 +266,8 @@ static int insert_device(vx_grid *g, const double *d_xyz, long long n, const lon
         if (e != cudaSuccess) return cuda_fail(e, "dense_clip");
         g->ctx->launches += 1;
     }
-    e = launch_finalize(g->cells, g->occ, g->counts, g->touched, g->ctr, g->n, g->capacity,
-                        n > 0 ? n : 1, hit, kOccThr, st);
+    e = launch_finalize(g->cells, g->occ, counts, g->touched, g->ctr, g->n, g->capacity,
+                        n > 0 ? n : 1, hit, kOccThr, st, fresh);
     if (e != cudaSuccess) return cuda_fail(e, "finalize");
     g->ctx->launches += 1;
     return VX_OK;
@@ -389,6 +397,7 @@ static int stamp_sets(vx_grid *g, int nsets, const int32_t *d_ijk, const int64_t
                       const double *d_origins, const double *d_vs, const double *d_T, float value,
                       int64_t total) {
     vx_ctx *c = g->ctx;
+    g->fresh = false;   // stamped cells are no longer +0.0f
     if (g->set_oob_cap < nsets) {
         cudaFree(g->set_oob);
         g->set_oob = nullptr;
@@ -466,6 +475,7 @@ extern "C" int vx_grid_write_cells(vx_grid *g, const float *in) {
     if (e != cudaSuccess) return cuda_fail(e, "occupancy");
     g->ctx->launches += 1;
     g->sparse_ok = false;  // non-zero cells are no longer all on the touched list
+    g->fresh = false;
     g->maybe_oor = g->maybe_oor || oor;
     VX_CUDA(cudaStreamSynchronize(g->ctx->stream));
     return VX_OK;
