@@ -245,8 +245,11 @@ static bool same_geometry(const vx_grid *a, const vx_grid *b) {  // grids.py:214
            a->g.ox == b->g.ox && a->g.oy == b->g.oy && a->g.oz == b->g.oz;
 }
 
+// sflag (optional, zeroed by the caller): on a fresh grid the finalize also
+// flags the occupied i-slices for the EDT; *flags_done says whether it did
 static int insert_device(vx_grid *g, const double *d_xyz, long long n, const long long *n_dev,
-                         float hit, double thr, const vx_grid *mask, const uint8_t *keep = nullptr) {
+                         float hit, double thr, const vx_grid *mask, const uint8_t *keep = nullptr,
+                         uint8_t *sflag = nullptr, bool *flags_done = nullptr) {
     if (mask && !same_geometry(g, mask))
         return fail(VX_EINVAL, "robot_mask geometry does not match this grid");
     cudaStream_t st = g->ctx->stream;
@@ -266,8 +269,10 @@ static int insert_device(vx_grid *g, const double *d_xyz, long long n, const lon
         if (e != cudaSuccess) return cuda_fail(e, "dense_clip");
         g->ctx->launches += 1;
     }
+    uint8_t *fl = fresh ? sflag : nullptr;
     e = launch_finalize(g->cells, g->occ, counts, g->touched, g->ctr, g->n, g->capacity,
-                        n > 0 ? n : 1, hit, kOccThr, st, fresh);
+                        n > 0 ? n : 1, hit, kOccThr, st, fresh, fl, (long long)g->g.ny * g->g.nz, g->g.nx);
+    if (flags_done) *flags_done = fl != nullptr;
     if (e != cudaSuccess) return cuda_fail(e, "finalize");
     g->ctx->launches += 1;
     return VX_OK;
@@ -1045,7 +1050,9 @@ extern "C" int vx_cycle_destroy(vx_cycle *cy) {
 
 // src: the grid whose occupancy this is; when its touched list covers every
 // occupied voxel the slice flags come from that list
-static cudaError_t edt_passes(vx_cycle *cy, const vx_grid *src, int32_t *site, bool marks) {
+// flags_ready: the occupied-slice flags were set by the insert's finalize
+static cudaError_t edt_passes(vx_cycle *cy, const vx_grid *src, int32_t *site, bool marks,
+                              bool flags_ready = false) {
     const uint8_t *occ = src->occ;
     unsigned char *base = static_cast<unsigned char *>(cy->scratch);
     const EdtPlan &p = cy->plan;
@@ -1064,9 +1071,14 @@ static cudaError_t edt_passes(vx_cycle *cy, const vx_grid *src, int32_t *site, b
             sp.m_mirror = cy->d_m;
             sp.p3_mode = cy->p3_mode;
         }
-        if (src->sparse_ok) e = launch_slice_list_touched(src->touched, src->ctr, occ, p, sp, st);
-        else e = launch_slice_list(occ, p, sp, st);
-        cy->ctx->launches += 2;
+        if (flags_ready) {
+            e = launch_slice_list_only(p, sp, st);
+            cy->ctx->launches += 1;
+        } else {
+            if (src->sparse_ok) e = launch_slice_list_touched(src->touched, src->ctr, occ, p, sp, st);
+            else e = launch_slice_list(occ, p, sp, st);
+            cy->ctx->launches += 2;
+        }
     }
     if (e == cudaSuccess) e = launch_pass1(occ, s1, p.nx, p.ny, p.nz, st, sparse ? &sp : nullptr);
     if (marks) cy->mark(5);
@@ -1092,11 +1104,24 @@ static int cycle_main_seq(vx_cycle *cy, const double *d_pts, long long npts, con
                                        cy->T_all, kLMax, cy->total_all)))
         return rc;
     if ((rc = grid_clear_async(cy->env))) return rc;
+    // the env EDT's occupied-slice flags come out of the (fresh-grid) finalize
+    uint8_t *sflag = nullptr;
+    if (sparse_ok(cy->plan, 1)) {
+        const EdtPlan &p = cy->plan;
+        const size_t nv = (size_t)p.nx * p.ny * p.nz;
+        const size_t s1b = (nv * 4 + 255) & ~(size_t)255, s2b = (nv * (p.s2_wide ? 8 : 4) + 255) & ~(size_t)255;
+        sflag = const_cast<uint8_t *>(
+            sparse_rows_at(static_cast<unsigned char *>(cy->scratch) + s1b + s2b + p.gstack_bytes, p).sflag);
+        VX_CUDA(cudaMemsetAsync(sflag, 0, (size_t)p.nx, st));
+    }
     if (marks) cy->mark(3);
-    if ((npts || n_dev) && (rc = insert_device(cy->env, d_pts, npts, n_dev, hit, thr, cy->mask))) return rc;
+    bool flags_ready = sflag != nullptr;   // no points: the zeroed flags are right
+    if ((npts || n_dev) &&
+        (rc = insert_device(cy->env, d_pts, npts, n_dev, hit, thr, cy->mask, nullptr, sflag, &flags_ready)))
+        return rc;
     if (!npts && !n_dev) VX_CUDA(cudaMemsetAsync(cy->env->ctr, 0, 3 * sizeof(unsigned long long), st));
     if (marks) cy->mark(4);
-    cudaError_t e = edt_passes(cy, cy->env, cy->env_f.site, marks);
+    cudaError_t e = edt_passes(cy, cy->env, cy->env_f.site, marks, flags_ready);
     if (e != cudaSuccess) return cuda_fail(e, "edt(env)");
     const GridGeom g = cy->env->g;
     e = launch_gather_pack(cy->env_f.site, cy->self_f.site, g, cy->d_centers, s, cy->d_lin, cy->d_world,

@@ -1458,6 +1458,13 @@ cudaError_t launch_slice_list_touched(const int32_t *touched, const DevCounters 
     return cudaGetLastError();
 }
 
+// the list alone, when the flags were already set (by a fresh-grid finalize)
+cudaError_t launch_slice_list_only(const EdtPlan &p, const SparseRows &sp, cudaStream_t st) {
+    k_slice_list<<<1, 1024, 0, st>>>(sp.sflag, p.nx, const_cast<int *>(sp.xs), const_cast<int *>(sp.hdr),
+                                     sp.m_mirror);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_slice_list(const uint8_t *occ, const EdtPlan &p, const SparseRows &sp, cudaStream_t st) {
     k_slice_flags<<<(unsigned)p.nx, 256, 0, st>>>(occ, (long long)p.ny * p.nz, const_cast<uint8_t *>(sp.sflag));
     k_slice_list<<<1, 1024, 0, st>>>(sp.sflag, p.nx, const_cast<int *>(sp.xs), const_cast<int *>(sp.hdr),

@@ -65,6 +65,7 @@ cudaError_t launch_pass3(const void *s2, int32_t *site, void *gstack, const EdtP
 bool sparse_ok(const EdtPlan &p, int nscenes);
 SparseRows sparse_rows_at(void *where, const EdtPlan &p);
 cudaError_t launch_slice_list(const uint8_t *occ, const EdtPlan &p, const SparseRows &sp, cudaStream_t st);
+cudaError_t launch_slice_list_only(const EdtPlan &p, const SparseRows &sp, cudaStream_t st);
 int pass3_mode_hint(const EdtPlan &p, int m);   // SparseRows::p3_mode from a predicted count
 struct DevCounters;
 // same from a grid's touched list (valid when it covers every occupied voxel)
@@ -104,7 +105,8 @@ cudaError_t launch_scatter(const double *pts, int64_t npts, const int64_t *npts_
                            cudaStream_t st, const uint8_t *keep = nullptr);
 cudaError_t launch_finalize(float *cells, uint8_t *occ, uint32_t *counts, int32_t *touched,
                             DevCounters *ctr, int64_t n, int capacity, int64_t max_new,
-                            float hit, float occ_thr, cudaStream_t st, bool fresh = false);
+                            float hit, float occ_thr, cudaStream_t st, bool fresh = false,
+                            uint8_t *sflag = nullptr, long long plane = 0, int nx = 0);
 cudaError_t launch_stamp(const int32_t *ijk, const int64_t *offsets, int nsets,
                          const double *set_origin, const double *set_vs, const double *T,
                          GridGeom g, float *cells, uint8_t *occ, float value, float occ_thr,

@@ -170,14 +170,14 @@ __global__ void k_scatter(const double *__restrict__ pts, long long npts,
 // and the scatter counted hits in the cells' own bits (counts == cells): one
 // random read and one write fewer per touched voxel.  0.0f + f32(c) * hit is
 // exactly f32(c) * hit, so the result equals the general path's.
-__device__ __forceinline__ void apply_hits(float *cells, uint8_t *occ, uint32_t *counts,
+__device__ __forceinline__ bool apply_hits(float *cells, uint8_t *occ, uint32_t *counts,
                                            long long v, float hit, float occ_thr, bool fresh) {
     const uint32_t c = counts[v];
     if (fresh) {
         const float cell = clip_logodds(__fmul_rn((float)c, hit));
         cells[v] = cell;
         occ[v] = cell > occ_thr ? 1 : 0;
-        return;
+        return cell > occ_thr;
     }
     counts[v] = 0u;
     // np.clip(flat + hits * hit, L_MIN, L_MAX): f32 multiply, f32 add (no fma)
@@ -185,21 +185,44 @@ __device__ __forceinline__ void apply_hits(float *cells, uint8_t *occ, uint32_t 
     const float cell = clip_logodds(__fadd_rn(cells[v], h));
     cells[v] = cell;
     occ[v] = cell > occ_thr ? 1 : 0;
+    return cell > occ_thr;
 }
 
 __global__ void k_finalize(float *__restrict__ cells, uint8_t *__restrict__ occ,
                            uint32_t *__restrict__ counts, const int32_t *__restrict__ touched,
                            DevCounters *__restrict__ ctr, long long n, float hit,
-                           float occ_thr, int capacity, int fresh) {
+                           float occ_thr, int capacity, int fresh, uint8_t *__restrict__ sflag,
+                           long long plane, int nx) {
+    // sflag (fresh grids only): every occupied voxel is one of this insert's,
+    // so the EDT's occupied-slice flags are set here (per-CTA bitmap, one
+    // store per slice and CTA) and need no pass over the touched list
+    __shared__ unsigned bits[1024];
+    const bool local = sflag && nx <= 32768;
+    if (local)
+        for (int w = threadIdx.x; w < (nx + 31) / 32; w += blockDim.x) bits[w] = 0u;
+    __syncthreads();
+    auto mark = [&](long long v) {
+        if (!sflag) return;
+        const int i = (int)(v / plane);
+        if (local) atomicOr(&bits[i >> 5], 1u << (i & 31));
+        else sflag[i] = 1;
+    };
     const long long nth = (long long)gridDim.x * blockDim.x;
     const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (ctr->overflow) {  // the touched list is incomplete: scan every voxel
         for (long long v = tid; v < n; v += nth)
-            if (counts[v]) apply_hits(cells, occ, counts, v, hit, occ_thr, fresh != 0);
+            if (counts[v] && apply_hits(cells, occ, counts, v, hit, occ_thr, fresh != 0)) mark(v);
     } else {
         const int base = ctr->touched, cnt = ctr->pending;
-        for (long long t = tid; t < cnt; t += nth)
-            apply_hits(cells, occ, counts, touched[base + t], hit, occ_thr, fresh != 0);
+        for (long long t = tid; t < cnt; t += nth) {
+            const int v = touched[base + t];
+            if (apply_hits(cells, occ, counts, v, hit, occ_thr, fresh != 0)) mark(v);
+        }
+    }
+    if (local) {
+        __syncthreads();
+        for (int w = threadIdx.x; w < (nx + 31) / 32; w += blockDim.x)
+            for (unsigned b = bits[w]; b; b &= b - 1) sflag[w * 32 + __ffs(b) - 1] = 1;
     }
     if (last_block(ctr)) {   // commit
         const long long t = (long long)ctr->touched + ctr->pending;
@@ -310,12 +333,14 @@ cudaError_t launch_scatter(const double *pts, int64_t npts, const int64_t *npts_
 
 cudaError_t launch_finalize(float *cells, uint8_t *occ, uint32_t *counts, int32_t *touched,
                             DevCounters *ctr, int64_t n, int capacity, int64_t max_new, float hit,
-                            float occ_thr, cudaStream_t st, bool fresh) {
+                            float occ_thr, cudaStream_t st, bool fresh, uint8_t *sflag, long long plane,
+                            int nx) {
     // grid-stride over the new touched entries (<= max_new; a dense overflow
     // sweep loops): few blocks, so the last-block commit's atomic is cheap
     const long long work = n < max_new ? n : max_new;
     const unsigned gf = (unsigned)std::min<long long>(grid_for(work, 256), 2LL * num_sms());
-    k_finalize<<<gf, 256, 0, st>>>(cells, occ, counts, touched, ctr, n, hit, occ_thr, capacity, fresh ? 1 : 0);
+    k_finalize<<<gf, 256, 0, st>>>(cells, occ, counts, touched, ctr, n, hit, occ_thr, capacity, fresh ? 1 : 0,
+                                   sflag, plane, nx);
     return cudaGetLastError();
 }
 
