@@ -113,53 +113,57 @@ __device__ __forceinline__ int pick(int k, int l, int r) {
 template <int CMAX>
 __device__ __forceinline__ void pass1_line(const uint32_t (&nib)[CMAX], int4 *__restrict__ dst, int nq,
                                            int lane) {
-    // forward: exclusive prefix max of the last occupied k
-    int exl[CMAX];
-    int carry = -1;
+    // The nearest occupied k before / after this lane's 4 voxels comes from
+    // the nearest lane holding any site: a ballot names the lanes with sites,
+    // __fls / __ffs of its masked bits picks the neighbour lane, and one
+    // shuffle reads that lane's nibble (instead of 5-step prefix scans).
+    const unsigned lt = (1u << lane) - 1u;
+    const unsigned gt = lane == 31 ? 0u : ~((2u << lane) - 1u);
+    unsigned m[CMAX];
+#pragma unroll
+    for (int c = 0; c < CMAX; ++c) m[c] = __ballot_sync(VX_FULL_MASK, nib[c] != 0u);
+    // warp-uniform carries: last site before chunk c, first site after it
+    int lastc[CMAX], firstc[CMAX];
+    int run = -1;
 #pragma unroll
     for (int c = 0; c < CMAX; ++c) {
-        const int base = (c * 32 + lane) * 4;
-        int v = nib[c] ? base + 31 - __clz(nib[c]) : -1;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const int o = __shfl_up_sync(VX_FULL_MASK, v, d);
-            if (lane >= d) v = max(v, o);
-        }
-        int ex = __shfl_up_sync(VX_FULL_MASK, v, 1);
-        if (lane == 0) ex = -1;
-        exl[c] = max(ex, carry);
-        carry = max(carry, __shfl_sync(VX_FULL_MASK, v, 31));
+        lastc[c] = run;
+        const int hl = m[c] ? 31 - __clz(m[c]) : 0;
+        const uint32_t nb = __shfl_sync(VX_FULL_MASK, nib[c], hl);
+        if (m[c]) run = (c * 32 + hl) * 4 + 31 - __clz(nb);
     }
-    // backward: exclusive suffix min of the first occupied k, then combine
-    int carr = BIG;
+    run = BIG;
 #pragma unroll
     for (int c = CMAX - 1; c >= 0; --c) {
+        firstc[c] = run;
+        const int ll = m[c] ? __ffs(m[c]) - 1 : 0;
+        const uint32_t nb = __shfl_sync(VX_FULL_MASK, nib[c], ll);
+        if (m[c]) run = (c * 32 + ll) * 4 + __ffs(nb) - 1;
+    }
+#pragma unroll
+    for (int c = 0; c < CMAX; ++c) {
         const int q = c * 32 + lane;
         const int base = q * 4;
         const uint32_t nb = nib[c];
-        int v = nb ? base + __ffs(nb) - 1 : BIG;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const int o = __shfl_down_sync(VX_FULL_MASK, v, d);
-            if (lane + d < 32) v = min(v, o);
-        }
-        int ex = __shfl_down_sync(VX_FULL_MASK, v, 1);
-        if (lane == 31) ex = BIG;
-        const int exr = min(ex, carr);
-        carr = min(carr, __shfl_sync(VX_FULL_MASK, v, 0));
+        const unsigned pm = m[c] & lt, nm = m[c] & gt;
+        const int lp = pm ? 31 - __clz(pm) : 0, ln = nm ? __ffs(nm) - 1 : 0;
+        const uint32_t nbp = __shfl_sync(VX_FULL_MASK, nb, lp);
+        const uint32_t nbn = __shfl_sync(VX_FULL_MASK, nb, ln);
+        const int exl = pm ? (c * 32 + lp) * 4 + 31 - __clz(nbp) : lastc[c];   // last site < base
+        const int exr = nm ? (c * 32 + ln) * 4 + __ffs(nbn) - 1 : firstc[c];   // first site > base + 3
         int lv[4];
-        int run = exl[c];
+        int r = exl;
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-            if ((nb >> e) & 1u) run = base + e;
-            lv[e] = run;
+            if ((nb >> e) & 1u) r = base + e;
+            lv[e] = r;
         }
         int o[4];
-        run = exr;
+        r = exr;
 #pragma unroll
         for (int e = 3; e >= 0; --e) {
-            if ((nb >> e) & 1u) run = base + e;
-            o[e] = pick(base + e, lv[e], run);
+            if ((nb >> e) & 1u) r = base + e;
+            o[e] = pick(base + e, lv[e], r);
         }
         if (q < nq) dst[q] = make_int4(o[0], o[1], o[2], o[3]);
     }
