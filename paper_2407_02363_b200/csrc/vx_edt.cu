@@ -1330,7 +1330,7 @@ cudaError_t launch_pass1(const uint8_t *occ, int32_t *s1, long long nslices, int
     const bool vec = (nz % 4 == 0) && ((uintptr_t)occ % 16 == 0) && ((uintptr_t)s1 % 16 == 0);
     if (vec && nz <= 128) k_pass1_v4<1, 2><<<grid2, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny, xs, hdr);
     else if (vec && nz <= 256) k_pass1_v4<2, 2><<<grid2, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny, xs, hdr);
-    else if (vec && nz <= 512) k_pass1_v4<4, 2><<<grid2, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny, xs, hdr);
+    else if (vec && nz <= 512) k_pass1_v4<4, 1><<<grid, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny, xs, hdr);
     else if (vec && nz <= 1024) k_pass1_v4<8, 1><<<grid, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny, xs, hdr);
     else if (vec && nz <= 2048) k_pass1_v4<16, 1><<<grid, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny, xs, hdr);
     else k_pass1_generic<<<grid, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny);
