@@ -249,11 +249,11 @@ static bool same_geometry(const vx_grid *a, const vx_grid *b) {  // grids.py:214
 // flags the occupied i-slices for the EDT; *flags_done says whether it did
 static int insert_device(vx_grid *g, const double *d_xyz, long long n, const long long *n_dev,
                          float hit, double thr, const vx_grid *mask, const uint8_t *keep = nullptr,
-                         uint8_t *sflag = nullptr, bool *flags_done = nullptr) {
+                         uint8_t *sflag = nullptr, bool *flags_done = nullptr, bool stats_zeroed = false) {
     if (mask && !same_geometry(g, mask))
         return fail(VX_EINVAL, "robot_mask geometry does not match this grid");
     cudaStream_t st = g->ctx->stream;
-    VX_CUDA(cudaMemsetAsync(g->ctr, 0, 3 * sizeof(unsigned long long), st));
+    if (!stats_zeroed) VX_CUDA(cudaMemsetAsync(g->ctr, 0, 3 * sizeof(unsigned long long), st));
     const float thr32 = (float)logit(thr);  // numpy compares in float32
     // a fresh grid counts hits in its own (zero) cells: finalize then reads one
     // array per touched voxel instead of two and has no counts to clear
@@ -398,18 +398,25 @@ extern "C" int vx_grid_insert_points_ex(vx_grid *g, const double *xyz, int64_t n
     return VX_OK;
 }
 
-static int stamp_sets(vx_grid *g, int nsets, const int32_t *d_ijk, const int64_t *d_offsets,
-                      const double *d_origins, const double *d_vs, const double *d_T, float value,
-                      int64_t total) {
-    vx_ctx *c = g->ctx;
-    g->fresh = false;   // stamped cells are no longer +0.0f
+static int ensure_set_oob(vx_grid *g, int nsets) {
     if (g->set_oob_cap < nsets) {
         cudaFree(g->set_oob);
         g->set_oob = nullptr;
         VX_CUDA(cudaMalloc(&g->set_oob, sizeof(unsigned long long) * nsets));
         g->set_oob_cap = nsets;
     }
-    VX_CUDA(cudaMemsetAsync(g->set_oob, 0, sizeof(unsigned long long) * nsets, c->stream));
+    return VX_OK;
+}
+
+// oob_zeroed: the per-set OOB counters were already cleared (camera tick)
+static int stamp_sets(vx_grid *g, int nsets, const int32_t *d_ijk, const int64_t *d_offsets,
+                      const double *d_origins, const double *d_vs, const double *d_T, float value,
+                      int64_t total, bool oob_zeroed = false) {
+    vx_ctx *c = g->ctx;
+    g->fresh = false;   // stamped cells are no longer +0.0f
+    int rc = ensure_set_oob(g, nsets);
+    if (rc) return rc;
+    if (!oob_zeroed) VX_CUDA(cudaMemsetAsync(g->set_oob, 0, sizeof(unsigned long long) * nsets, c->stream));
     cudaError_t e = launch_stamp(d_ijk, d_offsets, nsets, d_origins, d_vs, d_T, g->g, g->cells, g->occ,
                                  value, kOccThr, g->touched, g->ctr, g->set_oob, g->capacity, total,
                                  c->stream);
@@ -1099,11 +1106,6 @@ static int cycle_main_seq(vx_cycle *cy, const double *d_pts, long long npts, con
     vx_ctx *c = cy->ctx;
     cudaStream_t st = c->stream;
     int rc;
-    if ((rc = grid_clear_async(cy->mask))) return rc;
-    if (cy->nlinks && (rc = stamp_sets(cy->mask, cy->nlinks, cy->ijk_all, cy->off_all, cy->org_all, cy->vs_all,
-                                       cy->T_all, kLMax, cy->total_all)))
-        return rc;
-    if ((rc = grid_clear_async(cy->env))) return rc;
     // the env EDT's occupied-slice flags come out of the (fresh-grid) finalize
     uint8_t *sflag = nullptr;
     if (sparse_ok(cy->plan, 1)) {
@@ -1112,14 +1114,34 @@ static int cycle_main_seq(vx_cycle *cy, const double *d_pts, long long npts, con
         const size_t s1b = (nv * 4 + 255) & ~(size_t)255, s2b = (nv * (p.s2_wide ? 8 : 4) + 255) & ~(size_t)255;
         sflag = const_cast<uint8_t *>(
             sparse_rows_at(static_cast<unsigned char *>(cy->scratch) + s1b + s2b + p.gstack_bytes, p).sflag);
-        VX_CUDA(cudaMemsetAsync(sflag, 0, (size_t)p.nx, st));
     }
+    // one launch resets the mask and env grids and zeroes the slice flags, the
+    // mask's per-link OOB counters and the env insert stats
+    if (cy->nlinks && (rc = ensure_set_oob(cy->mask, cy->nlinks))) return rc;
+    {
+        const ResetArgs ra{cy->mask->cells, cy->mask->occ, cy->mask->touched, cy->mask->ctr, cy->mask->n,
+                           cy->mask->sparse_ok ? 0 : 1};
+        const ResetArgs rb{cy->env->cells, cy->env->occ, cy->env->touched, cy->env->ctr, cy->env->n,
+                           cy->env->sparse_ok ? 0 : 1};
+        cudaError_t e = launch_reset2(ra, rb, ZeroSpan{sflag, sflag ? (size_t)cy->plan.nx : 0},
+                                      ZeroSpan{cy->mask->set_oob, cy->nlinks ? (size_t)cy->nlinks * 8 : 0},
+                                      ZeroSpan{cy->env->ctr, 3 * sizeof(unsigned long long)}, st);
+        if (e != cudaSuccess) return cuda_fail(e, "reset");
+        c->launches += 1;
+        for (vx_grid *g : {cy->mask, cy->env}) {   // as grid_clear_async
+            g->sparse_ok = true;
+            g->maybe_oor = false;
+            g->fresh = true;
+        }
+    }
+    if (cy->nlinks && (rc = stamp_sets(cy->mask, cy->nlinks, cy->ijk_all, cy->off_all, cy->org_all, cy->vs_all,
+                                       cy->T_all, kLMax, cy->total_all, true)))
+        return rc;
     if (marks) cy->mark(3);
     bool flags_ready = sflag != nullptr;   // no points: the zeroed flags are right
-    if ((npts || n_dev) &&
-        (rc = insert_device(cy->env, d_pts, npts, n_dev, hit, thr, cy->mask, nullptr, sflag, &flags_ready)))
+    if ((npts || n_dev) && (rc = insert_device(cy->env, d_pts, npts, n_dev, hit, thr, cy->mask, nullptr, sflag,
+                                               &flags_ready, true)))
         return rc;
-    if (!npts && !n_dev) VX_CUDA(cudaMemsetAsync(cy->env->ctr, 0, 3 * sizeof(unsigned long long), st));
     if (marks) cy->mark(4);
     cudaError_t e = edt_passes(cy, cy->env, cy->env_f.site, marks, flags_ready);
     if (e != cudaSuccess) return cuda_fail(e, "edt(env)");

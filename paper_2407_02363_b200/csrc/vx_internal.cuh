@@ -95,6 +95,20 @@ struct DevCounters {                // device-resident per-grid bookkeeping
     unsigned int done;              // blocks finished (last-block commit of reset/stamp/finalize)
 };
 
+struct ResetArgs {   // one grid's sparse (touched-list) or dense reset
+    float *cells;
+    uint8_t *occ;
+    const int32_t *touched;
+    DevCounters *ctr;
+    long long n;
+    int dense;
+};
+struct ZeroSpan {
+    void *p;
+    size_t bytes;
+};
+cudaError_t launch_reset2(const ResetArgs &a, const ResetArgs &b, ZeroSpan z0, ZeroSpan z1, ZeroSpan z2,
+                          cudaStream_t st);
 cudaError_t launch_reset(float *cells, uint8_t *occ, int32_t *touched, DevCounters *ctr,
                          int64_t n, int capacity, bool dense, cudaStream_t st);
 cudaError_t launch_dense_clip(float *cells, const uint32_t *counts, int64_t n,

@@ -67,38 +67,51 @@ __device__ __forceinline__ bool last_block(DevCounters *ctr) {
     return false;
 }
 
-__global__ void k_reset(float *__restrict__ cells, uint8_t *__restrict__ occ,
-                        const int32_t *__restrict__ touched, DevCounters *__restrict__ ctr,
-                        long long n, int dense_req) {
-    const bool dense = dense_req || ctr->overflow;
-    const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    const long long nth = (long long)gridDim.x * blockDim.x;
+__device__ __forceinline__ void reset_body(const ResetArgs &r, long long tid, long long nth) {
+    const bool dense = r.dense || r.ctr->overflow;
     if (dense) {
-        const long long n4 = n >> 2;  // cells are 16-byte aligned (cudaMalloc)
-        float4 *c4 = reinterpret_cast<float4 *>(cells);
-        uint32_t *o4 = reinterpret_cast<uint32_t *>(occ);
+        const long long n4 = r.n >> 2;  // cells are 16-byte aligned (cudaMalloc)
+        float4 *c4 = reinterpret_cast<float4 *>(r.cells);
+        uint32_t *o4 = reinterpret_cast<uint32_t *>(r.occ);
         for (long long v = tid; v < n4; v += nth) {
             c4[v] = make_float4(0.f, 0.f, 0.f, 0.f);
             o4[v] = 0u;
         }
-        for (long long v = (n4 << 2) + tid; v < n; v += nth) {
-            cells[v] = 0.f;
-            occ[v] = 0;
+        for (long long v = (n4 << 2) + tid; v < r.n; v += nth) {
+            r.cells[v] = 0.f;
+            r.occ[v] = 0;
         }
     } else {
-        const int cnt = ctr->touched;
+        const int cnt = r.ctr->touched;
         for (long long t = tid; t < cnt; t += nth) {
-            const int v = touched[t];
-            cells[v] = 0.f;
-            occ[v] = 0;
+            const int v = r.touched[t];
+            r.cells[v] = 0.f;
+            r.occ[v] = 0;
         }
     }
-    if (last_block(ctr)) {   // commit
-        ctr->touched = 0;
-        ctr->pending = 0;
-        ctr->overflow = 0;
-        ctr->dirty = 1;
+    if (last_block(r.ctr)) {   // commit
+        r.ctr->touched = 0;
+        r.ctr->pending = 0;
+        r.ctr->overflow = 0;
+        r.ctr->dirty = 1;
     }
+}
+
+__global__ void k_reset(ResetArgs r) {
+    reset_body(r, (long long)blockIdx.x * blockDim.x + threadIdx.x, (long long)gridDim.x * blockDim.x);
+}
+
+// the camera tick's resets in one launch: blockIdx.y picks the grid (each
+// commits in its own last block); block (0, 0) also zeroes up to three small
+// buffers (slice flags, per-link OOB counters, insert stats) that would
+// otherwise be memset nodes of their own
+__global__ void k_reset2(ResetArgs a, ResetArgs b, ZeroSpan z0, ZeroSpan z1, ZeroSpan z2) {
+    if (blockIdx.x == 0 && blockIdx.y == 0) {
+        for (const ZeroSpan &z : {z0, z1, z2})
+            for (size_t i = threadIdx.x; i < z.bytes; i += blockDim.x) static_cast<unsigned char *>(z.p)[i] = 0;
+    }
+    reset_body(blockIdx.y ? b : a, (long long)blockIdx.x * blockDim.x + threadIdx.x,
+               (long long)gridDim.x * blockDim.x);
 }
 
 // clip untouched voxels (only needed after host writes put cells out of
@@ -312,7 +325,15 @@ cudaError_t launch_reset(float *cells, uint8_t *occ, int32_t *touched, DevCounte
     // the sparse count is only known on the device: size for the dense case
     // when asked, otherwise for a persistent grid-stride sweep
     const unsigned g = dense ? grid_for(n / 4 + 1, 256) : (unsigned)(num_sms() * 4);
-    k_reset<<<g, 256, 0, st>>>(cells, occ, touched, ctr, n, dense ? 1 : 0);   // commits in its last block
+    k_reset<<<g, 256, 0, st>>>(ResetArgs{cells, occ, touched, ctr, n, dense ? 1 : 0});   // commits in its last block
+    return cudaGetLastError();
+}
+
+cudaError_t launch_reset2(const ResetArgs &a, const ResetArgs &b, ZeroSpan z0, ZeroSpan z1, ZeroSpan z2,
+                          cudaStream_t st) {
+    const long long work = std::max(a.dense ? a.n / 4 + 1 : 0LL, b.dense ? b.n / 4 + 1 : 0LL);
+    const unsigned g = work ? std::max(grid_for(work, 256), (unsigned)(num_sms() * 2)) : (unsigned)(num_sms() * 2);
+    k_reset2<<<dim3(g, 2), 256, 0, st>>>(a, b, z0, z1, z2);
     return cudaGetLastError();
 }
 
