@@ -845,8 +845,6 @@ extern "C" int vx_edt_pass3_device(vx_ctx *c, const void *d_s2, int nx, int ny, 
     return VX_OK;
 }
 
-__global__ void k_set_count(long long *dst, long long v) { *dst = v; }
-
 // ---- camera-tick pipeline (engine.py:233-280) ----------------------------------------
 struct vx_cycle {
     vx_ctx *ctx = nullptr;
@@ -885,6 +883,12 @@ struct vx_cycle {
     // EDT, gather); the cloud size is read from d_npts on the device
     bool use_graph = true;
     long long *d_npts = nullptr, *h_npts = nullptr;  // device / pinned host point count
+    // per-step arguments staged in one H2D copy: {npts, cloud pointer | pad |
+    // link frames (nlinks x 4x4) | sphere centres}; two pinned host slots
+    unsigned char *d_stage = nullptr, *h_stage[2] = {nullptr, nullptr};
+    cudaEvent_t ev_stage[2] = {nullptr, nullptr};
+    size_t stage_bytes = 0;
+    int stage_slot = 0;
     // occupied-slice count of the last env EDT (host-mapped, written by the
     // device) -> which pass-3 kernels the next tick launches
     int *h_m = nullptr, *d_m = nullptr;
@@ -987,8 +991,19 @@ extern "C" int vx_cycle_create(vx_ctx *c, int nx, int ny, int nz, double vs, con
     if (e == cudaSuccess) e = cudaMalloc(&cy->d_lin, 2 * S * 4);
     if (e == cudaSuccess) e = cudaMalloc(&cy->d_world, 2 * S * 24);
     if (e == cudaSuccess) e = cudaMalloc(&cy->d_dist, 2 * S * 8);
-    if (e == cudaSuccess) e = cudaMalloc(&cy->d_npts, sizeof(long long));
     if (e == cudaSuccess) e = cudaHostAlloc(&cy->h_npts, sizeof(long long), cudaHostAllocPortable);
+    cy->stage_bytes = 64 + (size_t)nlinks * 128 + S * 24;
+    if (e == cudaSuccess) e = cudaMalloc(&cy->d_stage, cy->stage_bytes);
+    for (int b = 0; b < 2 && e == cudaSuccess; ++b) {
+        e = cudaHostAlloc(&cy->h_stage[b], cy->stage_bytes, cudaHostAllocPortable);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&cy->ev_stage[b], cudaEventDisableTiming);
+    }
+    if (e == cudaSuccess) {   // the graph reads frames, centres and the count from the staged block
+        cy->d_npts = reinterpret_cast<long long *>(cy->d_stage);
+        cy->T_all = reinterpret_cast<double *>(cy->d_stage + 64);
+        cudaFree(cy->d_centers);
+        cy->d_centers = reinterpret_cast<double *>(cy->d_stage + 64 + (size_t)nlinks * 128);
+    }
     if (e == cudaSuccess) e = cudaHostAlloc(&cy->h_m, sizeof(int), cudaHostAllocMapped | cudaHostAllocPortable);
     if (e == cudaSuccess)
         e = cudaHostAlloc(&cy->h_out, 64 + 8 + S * 2 * 36, cudaHostAllocMapped | cudaHostAllocPortable);
@@ -1029,12 +1044,16 @@ extern "C" int vx_cycle_destroy(vx_cycle *cy) {
     vx_grid_destroy(cy->mask);
     cudaFree(cy->tab);
     cudaFree(cy->d_pts);
-    cudaFree(cy->d_centers);
+    if (!cy->d_stage) cudaFree(cy->d_centers);   // else it lives in d_stage
+    cudaFree(cy->d_stage);
+    for (int b = 0; b < 2; ++b) {
+        if (cy->h_stage[b]) cudaFreeHost(cy->h_stage[b]);
+        if (cy->ev_stage[b]) cudaEventDestroy(cy->ev_stage[b]);
+    }
     cudaFree(cy->d_lin);
     cudaFree(cy->d_world);
     cudaFree(cy->d_dist);
     av_free(cy);
-    cudaFree(cy->d_npts);
     if (cy->h_npts) cudaFreeHost(cy->h_npts);
     if (cy->h_m) cudaFreeHost(cy->h_m);
     if (cy->h_out) cudaFreeHost(cy->h_out);
@@ -1187,13 +1206,26 @@ static int cycle_step(vx_cycle *cy, const double *pts, const double *d_pts_in, i
         cy->pf_host[pf_slot] = nullptr;   // consumed
         cy->pf_n[pf_slot] = -1;
     }
-    // H2D: FK frames of every link, the self subset, the cloud, the centres
-    if (cy->nlinks) VX_CUDA(cudaMemcpyAsync(cy->T_all, link_T, 128 * cy->nlinks, cudaMemcpyHostToDevice, st));
+    // H2D: the cloud (unless staged by prefetch or already on the device),
+    // then one copy of the per-step block {count, cloud pointer, frames, centres}
     std::vector<double> Ts(16 * cy->nself);
     for (int q = 0; q < cy->nself; ++q) std::memcpy(&Ts[16 * q], link_T + 16 * cy->self_links[q], 128);
     const double *d_pts = d_pts_in ? d_pts_in : cy->d_pts;
     if (npts && !d_pts_in) VX_CUDA(cudaMemcpyAsync(cy->d_pts, pts, (size_t)npts * 24, cudaMemcpyHostToDevice, st));
-    if (s) VX_CUDA(cudaMemcpyAsync(cy->d_centers, centers, (size_t)s * 24, cudaMemcpyHostToDevice, st));
+    {
+        const int b = cy->stage_slot;
+        cy->stage_slot ^= 1;
+        VX_CUDA(cudaEventSynchronize(cy->ev_stage[b]));   // its previous copy has been read
+        unsigned char *h = cy->h_stage[b];
+        const long long n64 = npts;
+        std::memcpy(h, &n64, 8);
+        std::memcpy(h + 8, &d_pts, sizeof(d_pts));
+        if (cy->nlinks) std::memcpy(h + 64, link_T, (size_t)128 * cy->nlinks);
+        if (s) std::memcpy(h + 64 + (size_t)128 * cy->nlinks, centers, (size_t)s * 24);
+        const size_t bytes = 64 + (size_t)128 * cy->nlinks + (size_t)s * 24;
+        VX_CUDA(cudaMemcpyAsync(cy->d_stage, h, bytes, cudaMemcpyHostToDevice, st));
+        VX_CUDA(cudaEventRecord(cy->ev_stage[b], st));
+    }
     if (cy->av_s && s == cy->av_s)
         VX_CUDA(cudaMemcpyAsync(cy->d_frames, cy->h_frames, (size_t)cy->av_nj * 48, cudaMemcpyHostToDevice, st));
     cy->mark(1);
@@ -1215,19 +1247,14 @@ static int cycle_step(vx_cycle *cy, const double *pts, const double *d_pts_in, i
     }
     cy->mark(2);
     if (cy->use_graph && !cy->profiling) {
-        // cloud into the fixed buffer the graph reads; its size via d_npts
-        if (npts && d_pts_in)
-            VX_CUDA(cudaMemcpyAsync(cy->d_pts, d_pts_in, (size_t)npts * 24, cudaMemcpyDeviceToDevice, st));
-        // by-value kernel argument: a later step cannot overwrite it before it runs
-        k_set_count<<<1, 1, 0, st>>>(cy->d_npts, npts);
-        VX_CUDA(cudaGetLastError());
+        // the graph reads the cloud pointer and its size from the staged block
         cy->p3_mode = pass3_mode_hint(cy->plan, *(volatile int *)cy->h_m);
         if (!cy->gexec || cy->g_s != s || cy->g_hit != hit || cy->g_thr != thr || cy->g_mode != cy->p3_mode) {
             if (cy->gexec) cudaGraphExecDestroy(cy->gexec);
             cy->gexec = nullptr;
             const long long l0 = c->launches;
             VX_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed));
-            rc = cycle_main_seq(cy, cy->d_pts, cy->max_points, cy->d_npts, hit, thr, s, false);
+            rc = cycle_main_seq(cy, nullptr, cy->max_points, cy->d_npts, hit, thr, s, false);
             cudaGraph_t graph = nullptr;
             cudaError_t ce = cudaStreamEndCapture(st, &graph);
             if (rc) {
@@ -1245,9 +1272,9 @@ static int cycle_step(vx_cycle *cy, const double *pts, const double *d_pts_in, i
             cy->g_hit = hit;
             cy->g_thr = thr;
         }
-        if (pf_slot >= 0) VX_CUDA(cudaEventRecord(cy->ev_used[pf_slot], st));   // slot copied out
         VX_CUDA(cudaGraphLaunch(cy->gexec, st));
         c->launches += cy->g_kernels;
+        if (pf_slot >= 0) VX_CUDA(cudaEventRecord(cy->ev_used[pf_slot], st));   // the tick read the slot
     } else {
         cy->p3_mode = pass3_mode_hint(cy->plan, *(volatile int *)cy->h_m);
         if ((rc = cycle_main_seq(cy, d_pts, npts, nullptr, hit, thr, s, true))) return rc;

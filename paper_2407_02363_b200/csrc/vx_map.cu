@@ -130,6 +130,9 @@ __global__ void k_scatter(const double *__restrict__ pts, long long npts,
                           uint32_t *__restrict__ counts, int32_t *__restrict__ touched,
                           DevCounters *__restrict__ ctr, int capacity, const uint8_t *__restrict__ keep) {
     const long long n = npts_dev ? *npts_dev : npts;
+    // pts == nullptr: npts_dev heads a device block {count, cloud pointer}
+    // (the camera tick's staged arguments, so its graph needs no cloud copy)
+    if (!pts) pts = *reinterpret_cast<const double *const *>(npts_dev + 1);
     const int base = ctr->touched;
     __shared__ int s_cnt, s_base;
     if (threadIdx.x == 0) s_cnt = 0;
