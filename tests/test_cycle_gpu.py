@@ -143,3 +143,33 @@ def test_prefetch_matches_plain_step():
     cyc.step(clouds[0].array, frames, centers)
     r = cyc.wait()
     assert r["inserted"] == want[0][0]
+
+
+@pytest.mark.parametrize("dims", [(96, 80, 72), (130, 64, 36), (64, 128, 30)],
+                         ids=lambda d: "x".join(map(str, d)))
+def test_cycle_odd_dims_matches_plain_calls(dims):
+    """The fused tick on grids whose extents are not multiples of 32 (ragged
+    k tiles; nz % 4 != 0 takes the non-TMA column kernels): its env field and
+    gather equal a plain EDT of its occupancy and site_world on it."""
+    from paper_2407_02363_b200 import pba_edt
+    from paper_2407_02363_b200.engine import site_world
+    vs = 0.02
+    origin = np.array([-0.5, -0.6, -0.1])
+    d = desk7()
+    cyc = MapCycle(dims, vs, origin, d["links"], vs, d["o_links"], max_points=20000, max_spheres=16)
+    rng = np.random.default_rng(sum(dims))
+    ext = np.array(dims) * vs
+    frames = d["frames"][1]
+    for t in range(3):
+        pts = origin + rng.random((20000, 3)) * ext * np.array([1.0, 1.0, 0.6])
+        centers = origin + rng.random((16, 3)) * ext
+        cyc.step(pts, frames, centers)
+        res = cyc.wait()
+        env, _, _ = cyc.grids()
+        fe, _ = cyc.fields()
+        want = pba_edt(env.occupancy_mask())
+        assert np.array_equal(fe.site, want.site), t
+        lin, world, dist = site_world(want, origin, vs, centers)
+        assert np.array_equal(res["env"][0], lin)
+        assert np.array_equal(res["env"][1], world)
+        assert np.allclose(res["env"][2], dist, rtol=1e-12, equal_nan=True)
