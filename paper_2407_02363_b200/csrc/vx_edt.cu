@@ -868,7 +868,7 @@ inline long long stream_min_tiles() {
     return v;
 }
 
-template <typename FT>
+template <typename FT, int C512>
 __global__ void __launch_bounds__(kWarpCtaThreads, 1) k_pass3_stream(const uint32_t *__restrict__ in,
                                                                      int32_t *__restrict__ out,
                                                                      uint32_t *__restrict__ ovf, const ColParams P) {
@@ -889,19 +889,21 @@ __global__ void __launch_bounds__(kWarpCtaThreads, 1) k_pass3_stream(const uint3
         if (i < kStreamCap) sst[i * 32] = e;
         else gst[(long long)i * 32] = e;
     };
-    // entry: (x << yzb) | s2 code (y << zb | z); F = x^2 + (j - y)^2 + (k - z)^2
-    const uint32_t eb = (uint32_t)P.yzb;
-    const uint32_t zb = (uint32_t)P.zb, zmask = P.zmask, ymask = P.ymask;
-    const long long plane = P.plane, splane = P.splane;
-    const int nz = P.nz, L = P.L;
+    // entry: (x << yzb) | s2 code (y << zb | z); F = x^2 + (j - y)^2 + (k - z)^2.
+    // C512: the 512^3 single-scene grid, whose strides and shifts are constants
+    const uint32_t eb = C512 ? 18u : (uint32_t)P.yzb;
+    const uint32_t zb = C512 ? 9u : (uint32_t)P.zb, zmask = C512 ? 511u : P.zmask, ymask = C512 ? 511u : P.ymask;
+    const long long plane = C512 ? 262144LL : P.plane, splane = C512 ? 262144LL : P.splane;
+    const int nz = C512 ? 512 : P.nz, L = C512 ? 512 : P.L;
     constexpr FT kNever = sizeof(FT) == 4 ? (FT)0x7fffffff : (FT)0x7fffffffffffffffLL;
     const long long step = (long long)gridDim.x * nw;
+    const int nkt = C512 ? 16 : P.nkt;
     for (long long tile = gw; tile < P.ntiles; tile += step) {
-        const int kt = (int)(tile % P.nkt);
-        const long long outer = tile / P.nkt;
-        const int scene = (int)(outer / P.nyl);
+        const int kt = (int)(tile % nkt);
+        const long long outer = tile / nkt;
+        const int scene = C512 ? 0 : (int)(outer / P.nyl);
         const int jl = (int)(outer - (long long)scene * P.nyl);
-        const int jq = P.j0 + jl;
+        const int jq = C512 ? jl : P.j0 + jl;
         const int k = kt * 32 + lane;
         if (k >= nz) continue;   // lanes only; no warp-wide sync below
         const long long base = (long long)scene * P.nvox + (long long)jl * nz + k;
@@ -1166,7 +1168,9 @@ cudaError_t launch_col(const void *in, void *out, void *gstack, const EdtPlan &p
                         spill <= (long long)p.s1_bytes && P.ntiles >= (long long)stream_min_tiles() && ssm <= kSmemLimit) {
                         const char *sm = getenv("VX_STREAM_MAX");
                         P.stream_max = mode == 1 ? 0x7fffffff : sm ? atoi(sm) : std::min(kStreamMaxRows, P.L / 2);
-                        auto kern = k_pass3_stream<typename C::FT>;
+                        const bool c512 = !p.fwide && p.nx == 512 && p.ny == 512 && p.nz == 512 && nyl == 512 &&
+                                          j0 == 0 && nouter == 512;
+                        auto kern = c512 ? k_pass3_stream<typename C::FT, 1> : k_pass3_stream<typename C::FT, 0>;
                         cudaError_t e = allow_smem(kern);
                         if (e != cudaSuccess) return e;
                         const unsigned grid = (unsigned)std::min<long long>((P.ntiles + VX_STREAM_WARPS - 1) / VX_STREAM_WARPS, num_sms());

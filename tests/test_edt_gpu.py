@@ -297,3 +297,21 @@ def test_cycle_pass3_kernel_choice(monkeypatch):
         occ = env.occupancy_mask()
         monkeypatch.setenv("VX_STREAM_MAX", "-1")
         assert np.array_equal(fe.site, pba_edt(occ).site), t
+
+
+def test_pass3_one_warp_kernel_512_specialisation(monkeypatch):
+    """The 512^3 specialisation of the one-warp pass 3 (constant strides) on a
+    scene-like grid (90 occupied slices, clustered sites, some deep hulls)
+    equals the banded kernel, which the 512^3 reference digests pin."""
+    rng = np.random.default_rng(512)
+    occ = np.zeros((512, 512, 512), np.uint8)
+    xs = np.sort(rng.choice(512, 90, replace=False))
+    pts = rng.integers(0, 512, size=(60, 2))
+    for n, x in enumerate(xs):
+        sl = occ[x]
+        sl[rng.random((512, 512)) < 2e-4] = 1
+        if n % 3 == 0:   # shared sites across slices: hulls keep every candidate
+            sl[pts[:, 0], pts[:, 1]] = 1
+    got = pba_edt(occ).site
+    monkeypatch.setenv("VX_STREAM_MAX", "-1")
+    assert np.array_equal(got, pba_edt(occ).site)
