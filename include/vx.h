@@ -199,8 +199,9 @@ int vx_cycle_destroy(vx_cycle *c);
 int vx_cycle_step(vx_cycle *c, const double *pts, int64_t npts, const double *link_T,
                   float hit_logodds, double occupancy_threshold, const double *centers,
                   int s, int sync);
-/* same tick with the cloud already in device memory (d_pts, npts points);
- * frames and centres are host arrays (a few hundred bytes) */
+/* same tick with the cloud already in device memory (d_pts, npts points;
+ * it must stay valid until the tick has run); frames and centres are host
+ * arrays (a few hundred bytes), copied into a pinned staging block at the call */
 int vx_cycle_step_device(vx_cycle *c, const double *d_pts, int64_t npts, const double *link_T,
                          float hit_logodds, double occupancy_threshold, const double *centers,
                          int s, int sync);
@@ -209,6 +210,8 @@ int vx_cycle_step_device(vx_cycle *c, const double *d_pts, int64_t npts, const d
  * the same pointer and count reads the staged copy instead of uploading it.
  * Two slots; the host buffer must stay unchanged until that step. */
 int vx_cycle_prefetch(vx_cycle *c, const double *pts, int64_t npts);
+/* wait for the last step and copy its results (the tick already packed them
+ * into host-mapped memory); any output may be NULL */
 int vx_cycle_wait(vx_cycle *c, vx_cycle_result *res, int32_t *site_lin /* 2*s */,
                   double *site_world /* 2*s*3 */, double *dist /* 2*s */);
 /* Per-phase CUDA-event timing of vx_cycle_step (bench evidence).  Phases:
