@@ -514,8 +514,11 @@ __device__ __forceinline__ void column_tile(const typename Col<PASS, S2W, EW, FW
     // of occupied slices (slot t = row xs[t]), split evenly over the bands
     int alo = lo, ahi = hi;
     int G = P.B;   // groups that build band hulls (and then merge: log2 G rounds)
+    // CMP: this scene's occupied-slice list (one list per scene of a batch)
+    const long long cscene = PASS == 3 ? outer / P.nyl : 0;
+    const int *cxs = CMP ? P.xs + cscene * P.nx : nullptr;
     if constexpr (CMP) {
-        const int m = __ldg(P.hdr);
+        const int m = __ldg(P.hdr + cscene);
         if (m < P.L) {
             // few occupied slices: longer groups, fewer merge rounds
             G = 1;
@@ -551,7 +554,7 @@ __device__ __forceinline__ void column_tile(const typename Col<PASS, S2W, EW, FW
         if constexpr (STAGED) {
             const InT *tin = reinterpret_cast<const InT *>(stk);
             if constexpr (CMP) {
-                for (int t = alo; t < ahi; ++t) consume(tin[(size_t)t * 32 + kk], __ldg(P.xs + t));
+                for (int t = alo; t < ahi; ++t) consume(tin[(size_t)t * 32 + kk], __ldg(cxs + t));
             } else {
 #pragma unroll 4
                 for (int y = lo; y < hi; ++y) consume(tin[(size_t)y * 32 + kk], y);
@@ -778,12 +781,13 @@ __global__ void __launch_bounds__(MAXT, MAXT >= 1024 ? 1 : kColMinBlocks) k_colu
     if constexpr (CMP) {
         // rows of occupied slices only (slot t <- row xs[t]); when every slice
         // is occupied the plain box loads below are used instead
-        const int m = __ldg(P.hdr);
+        const int scene = (int)(outer / P.nyl);
+        const int m = __ldg(P.hdr + scene);
         if (m <= P.stream_max) return;   // k_pass3_stream did this pass
         all_rows = m == P.L;
         if (!all_rows) {
-            const int scene = (int)(outer / P.nyl);
             const int jl = (int)(outer - (long long)scene * P.nyl);
+            const int *xsl = P.xs + (long long)scene * P.nx;
             if (threadIdx.x == 0 && threadIdx.y == 0) {
                 mbar_init(bar, 1);
                 mbar_expect_tx(bar, (uint32_t)m * 32u * (uint32_t)sizeof(EntT));
@@ -792,7 +796,7 @@ __global__ void __launch_bounds__(MAXT, MAXT >= 1024 ? 1 : kColMinBlocks) k_colu
             // one 32-column x 1-row box per occupied row, issued by all threads
             const int tid = threadIdx.y * 32 + threadIdx.x, nth = blockDim.x * blockDim.y;
             for (int t = tid; t < m; t += nth)
-                tma_load_4d(stk + (size_t)t * 32, &tmap1, bar, kt * 32, jl, __ldg(P.xs + t), scene);
+                tma_load_4d(stk + (size_t)t * 32, &tmap1, bar, kt * 32, jl, __ldg(xsl + t), scene);
         }
     }
     if (all_rows) {
@@ -1140,8 +1144,12 @@ cudaError_t launch_col(const void *in, void *out, void *gstack, const EdtPlan &p
     ColParams P = col_params(p, PASS, nouter, nyl, j0);
     if (sp) {   // the caller only passes one when both column passes are TMA-staged
         if (PASS == 2) P.sflag = sp->sflag;
-        P.xs = sp->xs;
-        P.hdr = sp->hdr;
+        // pass 2 maps CTAs through the list only for a single scene (a batch
+        // skips its empty slices by flag); pass 3 reads each scene's own list
+        if (PASS == 3 || nouter == p.nx) {
+            P.xs = sp->xs;
+            P.hdr = sp->hdr;
+        }
     }
     if (P.ntiles == 0) return cudaSuccess;
     const dim3 block(32, P.B);
@@ -1164,7 +1172,7 @@ cudaError_t launch_col(const void *in, void *out, void *gstack, const EdtPlan &p
                     // its tile alone, so small grids keep the banded kernel
                     const int mode = sp ? sp->p3_mode : 0;
                     const size_t ssm = (size_t)VX_STREAM_WARPS * kStreamCap * 32 * 4 + (size_t)P.L * 4;   // stacks + row list
-                    if (mode != 2 && cmp && gstack && p.xb + p.yb + p.zb <= 32 &&
+                    if (mode != 2 && cmp && gstack && nouter == nyl && p.xb + p.yb + p.zb <= 32 &&
                         spill <= (long long)p.s1_bytes && P.ntiles >= (long long)stream_min_tiles() && ssm <= kSmemLimit) {
                         const char *sm = getenv("VX_STREAM_MAX");
                         P.stream_max = mode == 1 ? 0x7fffffff : sm ? atoi(sm) : std::min(kStreamMaxRows, P.L / 2);
@@ -1388,6 +1396,11 @@ __global__ void __launch_bounds__(256) k_slice_flags(const uint8_t *__restrict__
 __global__ void __launch_bounds__(1024) k_slice_list(const uint8_t *__restrict__ sflag, int nslices,
                                                      int *__restrict__ xs, int *__restrict__ hdr,
                                                      int *__restrict__ m_mirror) {
+    // one CTA per scene of a batch: its flags, list and count
+    sflag += (size_t)blockIdx.x * nslices;
+    xs += (size_t)blockIdx.x * nslices;
+    hdr += blockIdx.x;
+    if (blockIdx.x) m_mirror = nullptr;
     __shared__ int wsum[32];
     __shared__ int base_s;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1473,9 +1486,11 @@ cudaError_t launch_slice_list_only(const EdtPlan &p, const SparseRows &sp, cudaS
     return cudaGetLastError();
 }
 
-cudaError_t launch_slice_list(const uint8_t *occ, const EdtPlan &p, const SparseRows &sp, cudaStream_t st) {
-    k_slice_flags<<<(unsigned)p.nx, 256, 0, st>>>(occ, (long long)p.ny * p.nz, const_cast<uint8_t *>(sp.sflag));
-    k_slice_list<<<1, 1024, 0, st>>>(sp.sflag, p.nx, const_cast<int *>(sp.xs), const_cast<int *>(sp.hdr),
+cudaError_t launch_slice_list(const uint8_t *occ, const EdtPlan &p, const SparseRows &sp, cudaStream_t st,
+                              int nscenes) {
+    k_slice_flags<<<(unsigned)(p.nx * nscenes), 256, 0, st>>>(occ, (long long)p.ny * p.nz,
+                                                             const_cast<uint8_t *>(sp.sflag));
+    k_slice_list<<<(unsigned)nscenes, 1024, 0, st>>>(sp.sflag, p.nx, const_cast<int *>(sp.xs), const_cast<int *>(sp.hdr),
                                      sp.m_mirror);
     return cudaGetLastError();
 }
@@ -1498,28 +1513,30 @@ int pass3_mode_hint(const EdtPlan &p, int m) {
     return m <= smax ? 1 : 2;
 }
 
-size_t sparse_bytes(const EdtPlan &p) {
-    return ((size_t)p.nx + 255) / 256 * 256 + ((size_t)p.nx * 4 + 255) / 256 * 256 + 256;
+size_t sparse_bytes(const EdtPlan &p, int nscenes) {
+    const size_t sx = (size_t)p.nx * nscenes;
+    return (sx + 255) / 256 * 256 + (sx * 4 + 255) / 256 * 256 + ((size_t)nscenes * 4 + 255) / 256 * 256;
 }
 
 size_t scratch_bytes_for(const EdtPlan &p, int nscenes) {
     const size_t n = (size_t)p.nx * p.ny * p.nz * nscenes;
     const size_t s1b = (n * 4 + 255) & ~(size_t)255;
     const size_t s2b = (n * (p.s2_wide ? 8 : 4) + 255) & ~(size_t)255;
-    return s1b + s2b + p.gstack_bytes + sparse_bytes(p);
+    return s1b + s2b + p.gstack_bytes + sparse_bytes(p, nscenes);
 }
 
 bool sparse_ok(const EdtPlan &p, int nscenes) {
     const char *ns = getenv("VX_NO_SPARSE");
-    return nscenes == 1 && p.tma2 && p.tma3 && !(ns && atoi(ns));
+    return nscenes >= 1 && p.tma2 && p.tma3 && !(ns && atoi(ns));
 }
 
-SparseRows sparse_rows_at(void *where, const EdtPlan &p) {
+SparseRows sparse_rows_at(void *where, const EdtPlan &p, int nscenes) {
     unsigned char *b = static_cast<unsigned char *>(where);
+    const size_t sx = (size_t)p.nx * nscenes;
     SparseRows sp;
     sp.sflag = b;
-    sp.xs = reinterpret_cast<int *>(b + ((size_t)p.nx + 255) / 256 * 256);
-    sp.hdr = reinterpret_cast<int *>(b + ((size_t)p.nx + 255) / 256 * 256 + ((size_t)p.nx * 4 + 255) / 256 * 256);
+    sp.xs = reinterpret_cast<int *>(b + (sx + 255) / 256 * 256);
+    sp.hdr = reinterpret_cast<int *>(b + (sx + 255) / 256 * 256 + (sx * 4 + 255) / 256 * 256);
     return sp;
 }
 
@@ -1535,13 +1552,18 @@ cudaError_t edt_device_batched(const uint8_t *occ, int32_t *site, void *scratch,
     void *gs = base + s1b + s2b;
     cudaError_t e;
     if (sparse_ok(p, nscenes)) {
-        const SparseRows sp = sparse_rows_at(base + s1b + s2b + p.gstack_bytes, p);
-        e = launch_slice_list(occ, p, sp, st);
-        if (e == cudaSuccess) e = launch_pass1(occ, s1, p.nx, p.ny, p.nz, st, &sp);
-        if (e == cudaSuccess) e = launch_pass2(s1, s2, gs, p, p.nx, st, &sp);
+        const SparseRows sp = sparse_rows_at(base + s1b + s2b + p.gstack_bytes, p, nscenes);
+        e = launch_slice_list(occ, p, sp, st, nscenes);
+        // a batch skips its empty slices by flag in passes 1-2 (the list remap
+        // is per scene); pass 3 stages each scene's occupied rows
+        SparseRows spf = sp;
+        if (nscenes > 1) spf.xs = nullptr, spf.hdr = nullptr;
+        const long long nsl = (long long)p.nx * nscenes;
+        if (e == cudaSuccess) e = launch_pass1(occ, s1, nsl, p.ny, p.nz, st, &spf);
+        if (e == cudaSuccess) e = launch_pass2(s1, s2, gs, p, nsl, st, &sp);
         // pass 3 of the sparse path: s1 is dead by now and serves as the
-        // spill slab of the per-warp column stacks
-        if (e == cudaSuccess) e = launch_pass3(s2, site, s1, p, 1, 0, p.ny, st, &sp);
+        // spill slab of the per-warp column stacks (single scene)
+        if (e == cudaSuccess) e = launch_pass3(s2, site, s1, p, nscenes, 0, p.ny, st, &sp);
         return e;
     }
     e = launch_pass1(occ, s1, (long long)p.nx * nscenes, p.ny, p.nz, st);

@@ -63,8 +63,9 @@ cudaError_t launch_pass3(const void *s2, int32_t *site, void *gstack, const EdtP
                          int nscenes, int j0, int nyl, cudaStream_t st, const SparseRows *sp = nullptr);
 // occupied-slice list: flags + compacted list (2 launches)
 bool sparse_ok(const EdtPlan &p, int nscenes);
-SparseRows sparse_rows_at(void *where, const EdtPlan &p);
-cudaError_t launch_slice_list(const uint8_t *occ, const EdtPlan &p, const SparseRows &sp, cudaStream_t st);
+SparseRows sparse_rows_at(void *where, const EdtPlan &p, int nscenes = 1);
+cudaError_t launch_slice_list(const uint8_t *occ, const EdtPlan &p, const SparseRows &sp, cudaStream_t st,
+                              int nscenes = 1);
 cudaError_t launch_slice_list_only(const EdtPlan &p, const SparseRows &sp, cudaStream_t st);
 int pass3_mode_hint(const EdtPlan &p, int m);   // SparseRows::p3_mode from a predicted count
 struct DevCounters;
