@@ -884,11 +884,13 @@ struct vx_cycle {
     bool use_graph = true;
     long long *d_npts = nullptr, *h_npts = nullptr;  // device / pinned host point count
     // per-step arguments staged in one H2D copy: {npts, cloud pointer | pad |
-    // link frames (nlinks x 4x4) | sphere centres}; two pinned host slots
-    unsigned char *d_stage = nullptr, *h_stage[2] = {nullptr, nullptr};
-    cudaEvent_t ev_stage[2] = {nullptr, nullptr};
+    // link frames (nlinks x 4x4) | sphere centres}; kStage pinned host slots
+    // let the host run up to kStage ticks ahead of the device
+    static constexpr int kStage = 8;
+    unsigned char *d_stage = nullptr, *h_stage[kStage] = {};
+    cudaEvent_t ev_stage[kStage] = {};
     size_t stage_bytes = 0;
-    int stage_slot = 0;
+    int stage_slot = 0, nstage = kStage;
     // occupied-slice count of the last env EDT (host-mapped, written by the
     // device) -> which pass-3 kernels the next tick launches
     int *h_m = nullptr, *d_m = nullptr;
@@ -994,7 +996,8 @@ extern "C" int vx_cycle_create(vx_ctx *c, int nx, int ny, int nz, double vs, con
     if (e == cudaSuccess) e = cudaHostAlloc(&cy->h_npts, sizeof(long long), cudaHostAllocPortable);
     cy->stage_bytes = 64 + (size_t)nlinks * 128 + S * 24;
     if (e == cudaSuccess) e = cudaMalloc(&cy->d_stage, cy->stage_bytes);
-    for (int b = 0; b < 2 && e == cudaSuccess; ++b) {
+    if (const char *ev = getenv("VX_STAGE_SLOTS")) cy->nstage = std::max(1, std::min(vx_cycle::kStage, atoi(ev)));
+    for (int b = 0; b < vx_cycle::kStage && e == cudaSuccess; ++b) {
         e = cudaHostAlloc(&cy->h_stage[b], cy->stage_bytes, cudaHostAllocPortable);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&cy->ev_stage[b], cudaEventDisableTiming);
     }
@@ -1046,7 +1049,7 @@ extern "C" int vx_cycle_destroy(vx_cycle *cy) {
     cudaFree(cy->d_pts);
     if (!cy->d_stage) cudaFree(cy->d_centers);   // else it lives in d_stage
     cudaFree(cy->d_stage);
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < vx_cycle::kStage; ++b) {
         if (cy->h_stage[b]) cudaFreeHost(cy->h_stage[b]);
         if (cy->ev_stage[b]) cudaEventDestroy(cy->ev_stage[b]);
     }
@@ -1214,7 +1217,7 @@ static int cycle_step(vx_cycle *cy, const double *pts, const double *d_pts_in, i
     if (npts && !d_pts_in) VX_CUDA(cudaMemcpyAsync(cy->d_pts, pts, (size_t)npts * 24, cudaMemcpyHostToDevice, st));
     {
         const int b = cy->stage_slot;
-        cy->stage_slot ^= 1;
+        cy->stage_slot = (b + 1) % cy->nstage;
         VX_CUDA(cudaEventSynchronize(cy->ev_stage[b]));   // its previous copy has been read
         unsigned char *h = cy->h_stage[b];
         const long long n64 = npts;
