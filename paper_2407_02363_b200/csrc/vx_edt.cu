@@ -282,12 +282,15 @@ struct ColParams {
     int stream_max;        // pass 3: k_pass3_stream takes m <= stream_max (-1: never)
 };
 
-template <int PASS, bool S2W, bool EW, bool FW>
+template <int PASS, bool S2W, bool EW, int FW>
 struct Col {
     using S2T = typename std::conditional<S2W, unsigned long long, uint32_t>::type;
     // pass 2: the stack entry is the s2 code itself; pass 3: (x, sy, sz)
     using EntT = typename std::conditional<PASS == 2 ? S2W : EW, unsigned long long, uint32_t>::type;
-    using FT = typename std::conditional<FW, long long, int>::type;
+    // FW: 0 = int32 weights and products; 1 = int32 weights, int64 products
+    // in the hull test; 2 = int64 weights
+    using FT = typename std::conditional<FW == 2, long long, int>::type;
+    using PT = typename std::conditional<FW >= 1, long long, int>::type;
     using InT = typename std::conditional<PASS == 2, int32_t, S2T>::type;
     using OutT = typename std::conditional<PASS == 2, S2T, int32_t>::type;
 
@@ -383,9 +386,10 @@ struct Col {
 };
 
 // b on or above segment a-c  ==> pop b   (edt.py:267-268, written with F=w+y^2)
-template <typename FT>
+// (PT: the product type; int32 weights with int64 products are one IMAD.WIDE each)
+template <typename FT, typename PT = FT>
 __device__ __forceinline__ bool dominated(int ya, FT Fa, int yb, FT Fb, int yc, FT Fc) {
-    return (Fb - Fa) * (FT)(yc - yb) >= (Fc - Fb) * (FT)(yb - ya);
+    return (PT)(Fb - Fa) * (PT)(yc - yb) >= (PT)(Fc - Fb) * (PT)(yb - ya);
 }
 
 // succ strictly closer than cur at query row y (edt.py:311 strict <)
@@ -471,7 +475,7 @@ struct RowOut {
     }
 };
 
-template <int PASS, bool S2W, bool EW, bool FW, bool STAGED, bool SCAT = false, bool CMP = false>
+template <int PASS, bool S2W, bool EW, int FW, bool STAGED, bool SCAT = false, bool CMP = false>
 __device__ __forceinline__ void column_tile(const typename Col<PASS, S2W, EW, FW>::InT *__restrict__ in,
                                             typename Col<PASS, S2W, EW, FW>::OutT *__restrict__ out,
                                             typename Col<PASS, S2W, EW, FW>::EntT *stk, int *meta,
@@ -480,6 +484,7 @@ __device__ __forceinline__ void column_tile(const typename Col<PASS, S2W, EW, FW
     using C = Col<PASS, S2W, EW, FW>;
     using EntT = typename C::EntT;
     using FT = typename C::FT;
+    using PT = typename C::PT;
     using InT = typename C::InT;
     using OutT = typename C::OutT;
 
@@ -536,7 +541,7 @@ __device__ __forceinline__ void column_tile(const typename Col<PASS, S2W, EW, FW
             if (!C::valid(v)) return;
             const EntT ec = C::make(P, v, yc, jq, k);
             const FT Fc = C::F(P, ec, jq, k);
-            while (n >= 2 && dominated<FT>(ya, Fa, yb, Fb, yc, Fc)) {
+            while (n >= 2 && dominated<FT, PT>(ya, Fa, yb, Fb, yc, Fc)) {
                 --n;
                 yb = ya;
                 Fb = Fa;
@@ -607,7 +612,7 @@ __device__ __forceinline__ void column_tile(const typename Col<PASS, S2W, EW, FW
                         e = stk[(size_t)pl2 * 32 + kk];
                         const int yl2 = C::row(P, e);
                         const FT Fl2 = C::F(P, e, jq, k);
-                        if (!dominated<FT>(yl2, Fl2, yl1, Fl1, yr0, Fr0)) break;
+                        if (!dominated<FT, PT>(yl2, Fl2, yl1, Fl1, yr0, Fr0)) break;
                         be[bl * 32 + kk] = pl1;
                         bl = bl2; pl1 = pl2; yl1 = yl2; Fl1 = Fl2;
                     }
@@ -623,7 +628,7 @@ __device__ __forceinline__ void column_tile(const typename Col<PASS, S2W, EW, FW
                         e = stk[(size_t)pr1 * 32 + kk];
                         const int yr1 = C::row(P, e);
                         const FT Fr1 = C::F(P, e, jq, k);
-                        if (!dominated<FT>(yl1, Fl1, yr0, Fr0, yr1, Fr1)) break;
+                        if (!dominated<FT, PT>(yl1, Fl1, yr0, Fr0, yr1, Fr1)) break;
                         bs[br * 32 + kk] = pr0 + 1;
                         br = br2; pr0 = pr1; yr0 = yr1; Fr0 = Fr1;
                         popped = true;
@@ -738,7 +743,7 @@ __device__ __forceinline__ void column_tile(const typename Col<PASS, S2W, EW, FW
     }
 }
 
-template <int PASS, bool S2W, bool EW, bool FW, bool SCAT>
+template <int PASS, bool S2W, bool EW, int FW, bool SCAT>
 __global__ void __launch_bounds__(kColThreads, kColMinBlocks) k_column_smem(const typename Col<PASS, S2W, EW, FW>::InT *__restrict__ in,
                                                       typename Col<PASS, S2W, EW, FW>::OutT *__restrict__ out,
                                                       const ColParams P, const __grid_constant__ ScatterTab sc) {
@@ -752,7 +757,7 @@ __global__ void __launch_bounds__(kColThreads, kColMinBlocks) k_column_smem(cons
 // TMA-staged variant (narrow 32-bit codes, nz % 4 == 0): one elected thread
 // issues the bulk tensor loads of the whole 32-column tile into the stack
 // region; every row of the column is in flight at once.
-template <int PASS, bool FW, bool SCAT, bool CMP, int MAXT>
+template <int PASS, int FW, bool SCAT, bool CMP, int MAXT>
 __global__ void __launch_bounds__(MAXT, MAXT >= 1024 ? 1 : kColMinBlocks) k_column_tma(const __grid_constant__ CUtensorMap tmap,
                                                      const __grid_constant__ CUtensorMap tmap1,
                                                      const typename Col<PASS, false, false, FW>::InT *__restrict__ in,
@@ -828,7 +833,7 @@ __global__ void __launch_bounds__(MAXT, MAXT >= 1024 ? 1 : kColMinBlocks) k_colu
 
 // Columns too long for shared memory: per-CTA stack slab in global scratch,
 // persistent over tiles.
-template <int PASS, bool S2W, bool EW, bool FW, bool SCAT>
+template <int PASS, bool S2W, bool EW, int FW, bool SCAT>
 __global__ void __launch_bounds__(kColThreads, kColMinBlocks) k_column_gstack(const typename Col<PASS, S2W, EW, FW>::InT *__restrict__ in,
                                                         typename Col<PASS, S2W, EW, FW>::OutT *__restrict__ out,
                                                         typename Col<PASS, S2W, EW, FW>::EntT *gstack,
@@ -872,7 +877,7 @@ inline long long stream_min_tiles() {
     return v;
 }
 
-template <typename FT, int C512>
+template <typename FT, typename PT, int C512>
 __global__ void __launch_bounds__(kWarpCtaThreads, 1) k_pass3_stream(const uint32_t *__restrict__ in,
                                                                      int32_t *__restrict__ out,
                                                                      uint32_t *__restrict__ ovf, const ColParams P) {
@@ -929,7 +934,7 @@ __global__ void __launch_bounds__(kWarpCtaThreads, 1) k_pass3_stream(const uint3
             const FT wc = wof(v);
             const uint32_t ec = ((uint32_t)yc << eb) | v;
             const FT Fc = (FT)yc * (FT)yc + wc;
-            while (n >= 2 && dominated<FT>(ya, Fa, yb, Fb, yc, Fc)) {
+            while (n >= 2 && dominated<FT, PT>(ya, Fa, yb, Fb, yc, Fc)) {
                 --n;
                 yb = ya;
                 Fb = Fa;
@@ -1137,7 +1142,7 @@ bool make_tmap(CUtensorMap *m, const void *in, const EdtPlan &p, int pass, long 
     return r == CUDA_SUCCESS;
 }
 
-template <int PASS, bool S2W, bool EW, bool FW, bool SCAT>
+template <int PASS, bool S2W, bool EW, int FW, bool SCAT>
 cudaError_t launch_col(const void *in, void *out, void *gstack, const EdtPlan &p, long long nouter,
                        int nyl, int j0, const ScatterTab &sc, cudaStream_t st, const SparseRows *sp) {
     using C = Col<PASS, S2W, EW, FW>;
@@ -1176,9 +1181,10 @@ cudaError_t launch_col(const void *in, void *out, void *gstack, const EdtPlan &p
                         spill <= (long long)p.s1_bytes && P.ntiles >= (long long)stream_min_tiles() && ssm <= kSmemLimit) {
                         const char *sm = getenv("VX_STREAM_MAX");
                         P.stream_max = mode == 1 ? 0x7fffffff : sm ? atoi(sm) : std::min(kStreamMaxRows, P.L / 2);
-                        const bool c512 = !p.fwide && p.nx == 512 && p.ny == 512 && p.nz == 512 && nyl == 512 &&
+                        const bool c512 = !p.fwide && !p.pwide && p.nx == 512 && p.ny == 512 && p.nz == 512 && nyl == 512 &&
                                           j0 == 0 && nouter == 512;
-                        auto kern = c512 ? k_pass3_stream<typename C::FT, 1> : k_pass3_stream<typename C::FT, 0>;
+                        auto kern = c512 ? k_pass3_stream<typename C::FT, typename C::PT, 1>
+                                         : k_pass3_stream<typename C::FT, typename C::PT, 0>;
                         cudaError_t e = allow_smem(kern);
                         if (e != cudaSuccess) return e;
                         const unsigned grid = (unsigned)std::min<long long>((P.ntiles + VX_STREAM_WARPS - 1) / VX_STREAM_WARPS, num_sms());
@@ -1233,13 +1239,16 @@ cudaError_t dispatch_col(const void *in, void *out, void *gstack, const EdtPlan 
                          int nyl, int j0, const ScatterTab &sc, cudaStream_t st,
                          const SparseRows *sp = nullptr) {
     // narrow: u32 s2, u32 entries, int weights (the 512^3 path)
+    if (!p.s2_wide && !p.e3_wide && !p.fwide && !p.pwide)
+        return launch_col<PASS, false, false, 0, SCAT>(in, out, gstack, p, nouter, nyl, j0, sc, st, sp);
+    // int32 weights, int64 hull-test products (the 1024^3 path)
     if (!p.s2_wide && !p.e3_wide && !p.fwide)
-        return launch_col<PASS, false, false, false, SCAT>(in, out, gstack, p, nouter, nyl, j0, sc, st, sp);
-    if (!p.s2_wide && !p.e3_wide && p.fwide)
-        return launch_col<PASS, false, false, true, SCAT>(in, out, gstack, p, nouter, nyl, j0, sc, st, sp);
-    if (!p.s2_wide && p.e3_wide)
-        return launch_col<PASS, false, true, true, SCAT>(in, out, gstack, p, nouter, nyl, j0, sc, st, sp);
-    return launch_col<PASS, true, true, true, SCAT>(in, out, gstack, p, nouter, nyl, j0, sc, st, sp);
+        return launch_col<PASS, false, false, 1, SCAT>(in, out, gstack, p, nouter, nyl, j0, sc, st, sp);
+    if (!p.s2_wide && !p.e3_wide)
+        return launch_col<PASS, false, false, 2, SCAT>(in, out, gstack, p, nouter, nyl, j0, sc, st, sp);
+    if (!p.s2_wide)
+        return launch_col<PASS, false, true, 2, SCAT>(in, out, gstack, p, nouter, nyl, j0, sc, st, sp);
+    return launch_col<PASS, true, true, 2, SCAT>(in, out, gstack, p, nouter, nyl, j0, sc, st, sp);
 }
 
 }  // namespace
@@ -1263,7 +1272,8 @@ bool make_plan(int nx, int ny, int nz, EdtPlan *p, int force_global_stack) {
     q.yb = bits_of(ny - 1);
     q.zb = bits_of(nz - 1);
     // test hooks: VX_FORCE_WIDE=1|2|3 selects the wider code paths on small
-    // grids (1: int64 weights, 2: +u64 pass-3 entries, 3: +u64 s2 codes);
+    // grids (1: int64 weights, 2: +u64 pass-3 entries, 3: +u64 s2 codes,
+    // 4: int32 weights with int64 hull-test products);
     // VX_FORCE_GSTACK=1 puts the column stacks in global memory
     const char *fw = getenv("VX_FORCE_WIDE");
     const int force_wide = fw ? atoi(fw) : 0;
@@ -1276,8 +1286,12 @@ bool make_plan(int nx, int ny, int nz, EdtPlan *p, int force_global_stack) {
     const double fmax = (double)(nx - 1) * (nx - 1) + (double)(ny - 1) * (ny - 1) +
                         (double)(nz - 1) * (nz - 1);
     const double lmax = (double)std::max(nx, ny);
-    q.fwide = q.e3_wide || force_wide >= 1 || (2.0 * fmax * lmax >= 2147483647.0) ||
+    // int64 weights when F, or the walk's 2*L*L right-hand side, leaves int32
+    // (or a test hook asks); otherwise int32 weights, and int64 products in the
+    // hull test only when F*L can leave int32 (the 1024^3 grids)
+    q.fwide = q.e3_wide || (force_wide >= 1 && force_wide <= 3) || fmax >= 2147483647.0 ||
               (2.0 * lmax * lmax >= 2147483647.0);
+    q.pwide = !q.fwide && (2.0 * fmax * lmax >= 2147483647.0 || force_wide == 4);
     auto bands = [](int L, int &B, int &W) {
         B = std::min(kMaxBands, pow2ceil((L + VX_BAND_ROWS - 1) / VX_BAND_ROWS));
         W = (L + B - 1) / B;

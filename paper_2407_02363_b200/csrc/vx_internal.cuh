@@ -16,7 +16,8 @@ struct EdtPlan {
     int wb;                // bits of the largest pass-3 weight (ny-1)^2 + (nz-1)^2
     bool s2_wide;          // pass-2 output as u64 (y<<32 | z) instead of u32 (y<<zb | z)
     bool e3_wide;          // pass-3 stack entries as u64
-    bool fwide;            // int64 weights/products (extents beyond ~700)
+    bool fwide;            // int64 weights (F or 2*L^2 beyond int32; and the VX_FORCE_WIDE hooks)
+    bool pwide;            // int32 weights, int64 hull-test products (2*F*L beyond int32: ~700-26k)
     int B2, W2;            // pass 2: bands per column, rows per band
     int B3, W3;            // pass 3
     bool gstack2, gstack3; // stack in global scratch (column longer than smem allows)

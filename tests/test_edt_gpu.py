@@ -100,14 +100,14 @@ print("ok")
 """
 
 
-@pytest.mark.parametrize("env", [{"VX_FORCE_WIDE": "1"}, {"VX_FORCE_WIDE": "2"},
+@pytest.mark.parametrize("env", [{"VX_FORCE_WIDE": "1"}, {"VX_FORCE_WIDE": "2"}, {"VX_FORCE_WIDE": "4"},
                                  {"VX_FORCE_WIDE": "3"}, {"VX_FORCE_GSTACK": "1"},
                                  {"VX_FORCE_WIDE": "3", "VX_FORCE_GSTACK": "1"},
                                  {"VX_NO_TMA": "1"}, {"VX_NO_SPARSE": "1"}],
                          ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
 def test_wide_and_gstack_variants(env):
-    """Every template variant (int64 weights, u64 entries / codes, global
-    stacks) on small grids, in a subprocess so the env knob is seen."""
+    """Every template variant (int64 weights, int64 hull-test products only,
+    u64 entries / codes, global stacks) on small grids, in a subprocess so the env knob is seen."""
     r = subprocess.run([sys.executable, "-c", _SUB.format(root=ROOT)], env={**os.environ, **env},
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
