@@ -866,6 +866,10 @@ constexpr int kWarpCtaThreads = 32 * VX_STREAM_WARPS;   // k_pass3_stream CTA: o
 // Runs when m <= P.stream_max; otherwise it exits and the banded
 // k_column_tma (launched right after it) does the pass.
 constexpr int kStreamCap = VX_STREAM_CAP;
+#ifndef VX_WALK_UNROLL
+#define VX_WALK_UNROLL 4
+#endif
+constexpr int kWalkUnroll = VX_WALK_UNROLL;   // query-walk rows per loop trip
 
 // the one-warp pass 3 needs enough tiles to keep its warps busy: each walks its
 // tile alone (VX_STREAM_MIN_TILES overrides; default 16 per SM)
@@ -1004,6 +1008,7 @@ __global__ void __launch_bounds__(kWarpCtaThreads, 1) k_pass3_stream(const uint3
             FT dN = has ? Fs - Fc : kNever;
             FT tt = has ? (FT)2 * (FT)(ys - yc) : (FT)0;
             FT rhs = 0;
+#pragma unroll kWalkUnroll
             for (int y = 0; y < L; ++y) {
                 if (dN < rhs) {   // successor strictly closer at row y (edt.py:311)
                     do {
