@@ -269,6 +269,9 @@ def cpu_baseline_sample(d):
 # ----------------------------------------------------------------------------
 def run_gpu(args, world, rank, local):
     import torch
+    # one GPU per rank; the modulo only matters when a box has fewer GPUs than
+    # ranks (a 2-rank smoke of this code path on a 1-GPU box, gloo backend)
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     os.environ["VX_DEVICE"] = str(local)
     from paper_2407_02363_b200 import _lib
