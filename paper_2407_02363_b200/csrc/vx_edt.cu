@@ -417,6 +417,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
         "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
         "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)), "r"(phase) : "memory");
 }
+__device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+        ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
 __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1,
                                             int c2) {
     asm volatile(
@@ -475,7 +481,7 @@ struct RowOut {
     }
 };
 
-template <int PASS, bool S2W, bool EW, int FW, bool STAGED, bool SCAT = false, bool CMP = false>
+template <int PASS, bool S2W, bool EW, int FW, bool STAGED, bool SCAT = false, bool CMP = false, int TW = 32>
 __device__ __forceinline__ void column_tile(const typename Col<PASS, S2W, EW, FW>::InT *__restrict__ in,
                                             typename Col<PASS, S2W, EW, FW>::OutT *__restrict__ out,
                                             typename Col<PASS, S2W, EW, FW>::EntT *stk, int *meta,
@@ -492,7 +498,7 @@ __device__ __forceinline__ void column_tile(const typename Col<PASS, S2W, EW, FW
     const int b = threadIdx.y;
     const int kt = (int)(tile % P.nkt);
     const long long outer = tile / P.nkt;
-    const int k = kt * 32 + kk;
+    const int k = kt * TW + kk;
     const bool colok = k < P.nz;
     long long base, stride;
     int jq = 0;
@@ -507,9 +513,9 @@ __device__ __forceinline__ void column_tile(const typename Col<PASS, S2W, EW, FW
         stride = P.splane;
     }
     int *bs = meta;
-    int *be = bs + P.B * 32;
-    int *nbl = be + P.B * 32;
-    int *ncnt = nbl + P.B * 32;
+    int *be = bs + P.B * TW;
+    int *nbl = be + P.B * TW;
+    int *ncnt = nbl + P.B * TW;
     const int lo = min(P.L, b * P.W);
     const int hi = min(P.L, lo + P.W);
 
@@ -546,12 +552,12 @@ __device__ __forceinline__ void column_tile(const typename Col<PASS, S2W, EW, FW
                 yb = ya;
                 Fb = Fa;
                 if (n >= 2) {
-                    const EntT t = stk[(size_t)(alo + n - 2) * 32 + kk];
+                    const EntT t = stk[(size_t)(alo + n - 2) * TW + kk];
                     ya = C::row(P, t);
                     Fa = C::F(P, t, jq, k);
                 }
             }
-            stk[(size_t)(alo + n) * 32 + kk] = ec;
+            stk[(size_t)(alo + n) * TW + kk] = ec;
             ya = yb; Fa = Fb;
             yb = yc; Fb = Fc;
             ++n;
@@ -559,10 +565,10 @@ __device__ __forceinline__ void column_tile(const typename Col<PASS, S2W, EW, FW
         if constexpr (STAGED) {
             const InT *tin = reinterpret_cast<const InT *>(stk);
             if constexpr (CMP) {
-                for (int t = alo; t < ahi; ++t) consume(tin[(size_t)t * 32 + kk], __ldg(cxs + t));
+                for (int t = alo; t < ahi; ++t) consume(tin[(size_t)t * TW + kk], __ldg(cxs + t));
             } else {
 #pragma unroll 4
-                for (int y = lo; y < hi; ++y) consume(tin[(size_t)y * 32 + kk], y);
+                for (int y = lo; y < hi; ++y) consume(tin[(size_t)y * TW + kk], y);
             }
         } else {
             const InT *src = in + base + (long long)lo * stride;
@@ -578,8 +584,8 @@ __device__ __forceinline__ void column_tile(const typename Col<PASS, S2W, EW, FW
             }
         }
     }
-    bs[b * 32 + kk] = alo;
-    be[b * 32 + kk] = alo + n;
+    bs[b * TW + kk] = alo;
+    be[b * TW + kk] = alo + n;
     __syncthreads();
     VX_PT(2);
 
@@ -588,48 +594,48 @@ __device__ __forceinline__ void column_tile(const typename Col<PASS, S2W, EW, FW
         if (colok && (b & (2 * r - 1)) == r) {
             const int gl = b - r, gm = b, ge = min(P.B, b + r);
             int bl = gm - 1;
-            while (bl >= gl && bs[bl * 32 + kk] == be[bl * 32 + kk]) --bl;
+            while (bl >= gl && bs[bl * TW + kk] == be[bl * TW + kk]) --bl;
             int br = gm;
-            while (br < ge && bs[br * 32 + kk] == be[br * 32 + kk]) ++br;
+            while (br < ge && bs[br * TW + kk] == be[br * TW + kk]) ++br;
             if (bl >= gl && br < ge) {
-                int pl1 = be[bl * 32 + kk] - 1;
-                EntT e = stk[(size_t)pl1 * 32 + kk];
+                int pl1 = be[bl * TW + kk] - 1;
+                EntT e = stk[(size_t)pl1 * TW + kk];
                 int yl1 = C::row(P, e);
                 FT Fl1 = C::F(P, e, jq, k);
-                int pr0 = bs[br * 32 + kk];
-                e = stk[(size_t)pr0 * 32 + kk];
+                int pr0 = bs[br * TW + kk];
+                e = stk[(size_t)pr0 * TW + kk];
                 int yr0 = C::row(P, e);
                 FT Fr0 = C::F(P, e, jq, k);
                 while (true) {
                     while (true) {  // pop the left tail while dominated
                         int bl2 = bl, pl2 = pl1 - 1;
-                        if (pl2 < bs[bl * 32 + kk]) {
+                        if (pl2 < bs[bl * TW + kk]) {
                             bl2 = bl - 1;
-                            while (bl2 >= gl && bs[bl2 * 32 + kk] == be[bl2 * 32 + kk]) --bl2;
+                            while (bl2 >= gl && bs[bl2 * TW + kk] == be[bl2 * TW + kk]) --bl2;
                             if (bl2 < gl) break;
-                            pl2 = be[bl2 * 32 + kk] - 1;
+                            pl2 = be[bl2 * TW + kk] - 1;
                         }
-                        e = stk[(size_t)pl2 * 32 + kk];
+                        e = stk[(size_t)pl2 * TW + kk];
                         const int yl2 = C::row(P, e);
                         const FT Fl2 = C::F(P, e, jq, k);
                         if (!dominated<FT, PT>(yl2, Fl2, yl1, Fl1, yr0, Fr0)) break;
-                        be[bl * 32 + kk] = pl1;
+                        be[bl * TW + kk] = pl1;
                         bl = bl2; pl1 = pl2; yl1 = yl2; Fl1 = Fl2;
                     }
                     bool popped = false;
                     while (true) {  // pop the right head while dominated
                         int br2 = br, pr1 = pr0 + 1;
-                        if (pr1 >= be[br * 32 + kk]) {
+                        if (pr1 >= be[br * TW + kk]) {
                             br2 = br + 1;
-                            while (br2 < ge && bs[br2 * 32 + kk] == be[br2 * 32 + kk]) ++br2;
+                            while (br2 < ge && bs[br2 * TW + kk] == be[br2 * TW + kk]) ++br2;
                             if (br2 >= ge) break;
-                            pr1 = bs[br2 * 32 + kk];
+                            pr1 = bs[br2 * TW + kk];
                         }
-                        e = stk[(size_t)pr1 * 32 + kk];
+                        e = stk[(size_t)pr1 * TW + kk];
                         const int yr1 = C::row(P, e);
                         const FT Fr1 = C::F(P, e, jq, k);
                         if (!dominated<FT, PT>(yl1, Fl1, yr0, Fr0, yr1, Fr1)) break;
-                        bs[br * 32 + kk] = pr0 + 1;
+                        bs[br * TW + kk] = pr0 + 1;
                         br = br2; pr0 = pr1; yr0 = yr1; Fr0 = Fr1;
                         popped = true;
                     }
@@ -645,7 +651,7 @@ __device__ __forceinline__ void column_tile(const typename Col<PASS, S2W, EW, FW
     if (b == 0) {
         int c = 0;
         for (int q = 0; q < P.B; ++q)
-            if (bs[q * 32 + kk] < be[q * 32 + kk]) nbl[(c++) * 32 + kk] = q;
+            if (bs[q * TW + kk] < be[q * TW + kk]) nbl[(c++) * TW + kk] = q;
         ncnt[kk] = c;
     }
     __syncthreads();
@@ -664,30 +670,30 @@ __device__ __forceinline__ void column_tile(const typename Col<PASS, S2W, EW, FW
             int mlo = 0, mhi = cnt - 1;
             while (mlo < mhi) {
                 const int mid = (mlo + mhi) >> 1;
-                const int bm = nbl[mid * 32 + kk], bn = nbl[(mid + 1) * 32 + kk];
-                const EntT a = stk[(size_t)(be[bm * 32 + kk] - 1) * 32 + kk];
-                const EntT s = stk[(size_t)bs[bn * 32 + kk] * 32 + kk];
+                const int bm = nbl[mid * TW + kk], bn = nbl[(mid + 1) * TW + kk];
+                const EntT a = stk[(size_t)(be[bm * TW + kk] - 1) * TW + kk];
+                const EntT s = stk[(size_t)bs[bn * TW + kk] * TW + kk];
                 if (better<FT>(C::row(P, s), C::F(P, s, jq, k), C::row(P, a), C::F(P, a, jq, k), y0))
                     mlo = mid + 1;
                 else
                     mhi = mid;
             }
             int m = mlo;
-            int bm = nbl[m * 32 + kk];
+            int bm = nbl[m * TW + kk];
             // ... then inside the band
-            int ilo = bs[bm * 32 + kk], ihi = be[bm * 32 + kk] - 1;
+            int ilo = bs[bm * TW + kk], ihi = be[bm * TW + kk] - 1;
             while (ilo < ihi) {
                 const int mid = (ilo + ihi) >> 1;
-                const EntT a = stk[(size_t)mid * 32 + kk];
-                const EntT s = stk[(size_t)(mid + 1) * 32 + kk];
+                const EntT a = stk[(size_t)mid * TW + kk];
+                const EntT s = stk[(size_t)(mid + 1) * TW + kk];
                 if (better<FT>(C::row(P, s), C::F(P, s, jq, k), C::row(P, a), C::F(P, a, jq, k), y0))
                     ilo = mid + 1;
                 else
                     ihi = mid;
             }
             int pos = ilo;
-            int epos = be[bm * 32 + kk];
-            EntT cur = stk[(size_t)pos * 32 + kk];
+            int epos = be[bm * TW + kk];
+            EntT cur = stk[(size_t)pos * TW + kk];
             int yc = C::row(P, cur);
             FT Fc = C::F(P, cur, jq, k);
             const InT *src = in + base;
@@ -699,13 +705,13 @@ __device__ __forceinline__ void column_tile(const typename Col<PASS, S2W, EW, FW
             // successor
             int spos = -1, sm = m;
             if (pos + 1 < epos) spos = pos + 1;
-            else if (m + 1 < cnt) { sm = m + 1; spos = bs[nbl[sm * 32 + kk] * 32 + kk]; }
+            else if (m + 1 < cnt) { sm = m + 1; spos = bs[nbl[sm * TW + kk] * TW + kk]; }
             EntT sent = 0;
             int ys = 0;
             FT Fs = 0;
             InT scode = InT(0);   // the successor's site code, prefetched
             if (spos >= 0) {
-                sent = stk[(size_t)spos * 32 + kk];
+                sent = stk[(size_t)spos * TW + kk];
                 ys = C::row(P, sent);
                 Fs = C::F(P, sent, jq, k);
                 scode = code_of(ys);
@@ -721,12 +727,12 @@ __device__ __forceinline__ void column_tile(const typename Col<PASS, S2W, EW, FW
                     InT ccode = scode;
                     do {
                         cur = sent; yc = ys; Fc = Fs; pos = spos; ccode = scode;
-                        if (sm != m) { m = sm; epos = be[nbl[m * 32 + kk] * 32 + kk]; }
+                        if (sm != m) { m = sm; epos = be[nbl[m * TW + kk] * TW + kk]; }
                         if (pos + 1 < epos) spos = pos + 1;
-                        else if (m + 1 < cnt) { sm = m + 1; spos = bs[nbl[sm * 32 + kk] * 32 + kk]; }
+                        else if (m + 1 < cnt) { sm = m + 1; spos = bs[nbl[sm * TW + kk] * TW + kk]; }
                         else spos = -1;
                         if (spos >= 0) {
-                            sent = stk[(size_t)spos * 32 + kk];
+                            sent = stk[(size_t)spos * TW + kk];
                             ys = C::row(P, sent);
                             Fs = C::F(P, sent, jq, k);
                             scode = code_of(ys);
@@ -757,7 +763,7 @@ __global__ void __launch_bounds__(kColThreads, kColMinBlocks) k_column_smem(cons
 // TMA-staged variant (narrow 32-bit codes, nz % 4 == 0): one elected thread
 // issues the bulk tensor loads of the whole 32-column tile into the stack
 // region; every row of the column is in flight at once.
-template <int PASS, int FW, bool SCAT, bool CMP, int MAXT>
+template <int PASS, int FW, bool SCAT, bool CMP, int MAXT, int TW = 32>
 __global__ void __launch_bounds__(MAXT, MAXT >= 1024 ? 1 : kColMinBlocks) k_column_tma(const __grid_constant__ CUtensorMap tmap,
                                                      const __grid_constant__ CUtensorMap tmap1,
                                                      const typename Col<PASS, false, false, FW>::InT *__restrict__ in,
@@ -766,8 +772,8 @@ __global__ void __launch_bounds__(MAXT, MAXT >= 1024 ? 1 : kColMinBlocks) k_colu
     extern __shared__ __align__(128) unsigned char smem[];
     using EntT = typename Col<PASS, false, false, FW>::EntT;
     EntT *stk = reinterpret_cast<EntT *>(smem);
-    int *meta = reinterpret_cast<int *>(smem + (size_t)P.rows_alloc * 32 * sizeof(EntT));
-    uint64_t *bar = reinterpret_cast<uint64_t *>(meta + 3 * P.B * 32 + 32);
+    int *meta = reinterpret_cast<int *>(smem + (size_t)P.rows_alloc * TW * sizeof(EntT));
+    uint64_t *bar = reinterpret_cast<uint64_t *>(meta + 3 * P.B * TW + TW);
     long long tile = blockIdx.x;
     const int kt = (int)(tile % P.nkt);
     long long outer = tile / P.nkt;
@@ -793,37 +799,48 @@ __global__ void __launch_bounds__(MAXT, MAXT >= 1024 ? 1 : kColMinBlocks) k_colu
         if (!all_rows) {
             const int jl = (int)(outer - (long long)scene * P.nyl);
             const int *xsl = P.xs + (long long)scene * P.nx;
+            // 16-column rows are 64 B, below the 128-B smem alignment of tensor
+            // boxes: plain bulk copies of the row's in-range columns instead
+            const uint32_t rbytes = TW == 32 ? 0u : (uint32_t)min(TW, P.nz - kt * TW) * (uint32_t)sizeof(EntT);
             if (threadIdx.x == 0 && threadIdx.y == 0) {
                 mbar_init(bar, 1);
-                mbar_expect_tx(bar, (uint32_t)m * 32u * (uint32_t)sizeof(EntT));
+                mbar_expect_tx(bar, TW == 32 ? (uint32_t)m * (uint32_t)TW * (uint32_t)sizeof(EntT)
+                                             : (uint32_t)m * rbytes);
             }
             __syncthreads();
-            // one 32-column x 1-row box per occupied row, issued by all threads
-            const int tid = threadIdx.y * 32 + threadIdx.x, nth = blockDim.x * blockDim.y;
-            for (int t = tid; t < m; t += nth)
-                tma_load_4d(stk + (size_t)t * 32, &tmap1, bar, kt * 32, jl, __ldg(xsl + t), scene);
+            // one TW-column x 1-row load per occupied row, issued by all threads
+            const int tid = threadIdx.y * TW + threadIdx.x, nth = blockDim.x * blockDim.y;
+            if constexpr (TW == 32) {
+                for (int t = tid; t < m; t += nth)
+                    tma_load_4d(stk + (size_t)t * TW, &tmap1, bar, kt * TW, jl, __ldg(xsl + t), scene);
+            } else {
+                const EntT *row0 = reinterpret_cast<const EntT *>(in) + (long long)scene * P.nvox +
+                                   (long long)jl * P.nz + kt * TW;
+                for (int t = tid; t < m; t += nth)
+                    bulk_load(stk + (size_t)t * TW, row0 + (long long)__ldg(xsl + t) * P.splane, rbytes, bar);
+            }
         }
     }
     if (all_rows) {
         if (threadIdx.x == 0 && threadIdx.y == 0) {
             mbar_init(bar, 1);
             const int nbox = P.rows_alloc / P.boxh;
-            mbar_expect_tx(bar, (uint32_t)(P.rows_alloc * 32 * sizeof(EntT)));
+            mbar_expect_tx(bar, (uint32_t)(P.rows_alloc * TW * sizeof(EntT)));
             for (int q = 0; q < nbox; ++q) {
-                void *dst = stk + (size_t)q * P.boxh * 32;
+                void *dst = stk + (size_t)q * P.boxh * TW;
                 if constexpr (PASS == 2) {
-                    tma_load_3d(dst, &tmap, bar, kt * 32, q * P.boxh, (int)outer);
+                    tma_load_3d(dst, &tmap, bar, kt * TW, q * P.boxh, (int)outer);
                 } else {
                     const int scene = (int)(outer / P.nyl);
                     const int jl = (int)(outer - (long long)scene * P.nyl);
-                    tma_load_4d(dst, &tmap, bar, kt * 32, jl, q * P.boxh, scene);
+                    tma_load_4d(dst, &tmap, bar, kt * TW, jl, q * P.boxh, scene);
                 }
             }
         }
     }
     __syncthreads();
     mbar_wait(bar, 0);
-    column_tile<PASS, false, false, FW, true, SCAT, CMP>(in, out, stk, meta, P, tile, &sc);
+    column_tile<PASS, false, false, FW, true, SCAT, CMP, TW>(in, out, stk, meta, P, tile, &sc);
 #ifdef VX_PHASE_TIMING
     VX_PT(5);
     __syncthreads();
@@ -1122,7 +1139,7 @@ PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
 // TMA view of a column pass input: 3D (k, y, slice) for pass 2, 4D
 // (k, j, x, scene) for pass 3; box = 32 columns x boxh rows.
 bool make_tmap(CUtensorMap *m, const void *in, const EdtPlan &p, int pass, long long nouter, int nyl,
-               int boxh) {
+               int boxh, int boxw = 32) {
     auto enc = tmap_encoder();
     if (!enc) return false;
     cuuint64_t dims[4], strides[3];
@@ -1132,14 +1149,14 @@ bool make_tmap(CUtensorMap *m, const void *in, const EdtPlan &p, int pass, long 
         rank = 3;
         dims[0] = p.nz; dims[1] = p.ny; dims[2] = (cuuint64_t)nouter;
         strides[0] = (cuuint64_t)p.nz * 4; strides[1] = (cuuint64_t)p.ny * p.nz * 4;
-        box[0] = 32; box[1] = boxh; box[2] = 1;
+        box[0] = (cuuint32_t)boxw; box[1] = boxh; box[2] = 1;
     } else {
         rank = 4;
         const long long nscenes = nouter / nyl;
         dims[0] = p.nz; dims[1] = nyl; dims[2] = p.nx; dims[3] = (cuuint64_t)nscenes;
         strides[0] = (cuuint64_t)p.nz * 4; strides[1] = (cuuint64_t)nyl * p.nz * 4;
         strides[2] = (cuuint64_t)p.nx * nyl * p.nz * 4;
-        box[0] = 32; box[1] = 1; box[2] = boxh; box[3] = 1;
+        box[0] = (cuuint32_t)boxw; box[1] = 1; box[2] = boxh; box[3] = 1;
     }
     CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, rank, const_cast<void *>(in), dims, strides, box, estr,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -1169,8 +1186,11 @@ cudaError_t launch_col(const void *in, void *out, void *gstack, const EdtPlan &p
         if (staged && !gs) {
             CUtensorMap m, m1;
             const bool cmp = PASS == 3 && P.xs != nullptr;
-            if (make_tmap(&m, in, p, PASS, nouter, nyl, P.boxh) &&
-                (!cmp || make_tmap(&m1, in, p, PASS, nouter, nyl, 1))) {
+            // long columns (L > 512): 16-column tiles, so a 1024-row tile is
+            // 64 KB and three CTAs share an SM (make_plan: tw2 / tw3)
+            const int tw = PASS == 2 ? p.tw2 : p.tw3;
+            if (make_tmap(&m, in, p, PASS, nouter, nyl, P.boxh, tw) &&
+                (!cmp || make_tmap(&m1, in, p, PASS, nouter, nyl, 1, tw))) {
                 if (!cmp) m1 = m;
                 if constexpr (PASS == 3 && !SCAT) {
                     // few occupied slices: one warp per tile (k_pass3_stream) when
@@ -1203,8 +1223,21 @@ cudaError_t launch_col(const void *in, void *out, void *gstack, const EdtPlan &p
                     }
                 }
                 const size_t smem = PASS == 2 ? p.smem2 : p.smem3;
-                // long columns (L > 512) take 32 bands = 1024 threads: their tile
-                // already fills an SM's shared memory, so one CTA per SM anyway
+                if (tw == 16) {
+                    // 32 bands x 16 columns = 512 threads (two bands per warp)
+                    P.nkt = (p.nz + 15) / 16;
+                    P.ntiles = (long long)P.nkt * nouter;
+                    auto kern = cmp ? k_column_tma<PASS, FW, SCAT, true, kColThreads, 16>
+                                    : k_column_tma<PASS, FW, SCAT, false, kColThreads, 16>;
+                    cudaError_t e = allow_smem(kern);
+                    if (e != cudaSuccess) return e;
+                    kern<<<(unsigned)P.ntiles, dim3(16, P.B), smem, st>>>(
+                        m, m1, reinterpret_cast<const typename C::InT *>(in),
+                        reinterpret_cast<typename C::OutT *>(out), P, sc);
+                    return cudaGetLastError();
+                }
+                // long columns (L > 512) with 32-column tiles take 32 bands =
+                // 1024 threads: one CTA per SM (VX_NARROW_TILES=0)
                 auto kern = P.B > kMaxBands
                                 ? (cmp ? k_column_tma<PASS, FW, SCAT, true, 1024> : k_column_tma<PASS, FW, SCAT, false, 1024>)
                                 : (cmp ? k_column_tma<PASS, FW, SCAT, true, kColThreads>
@@ -1316,27 +1349,38 @@ bool make_plan(int nx, int ny, int nz, EdtPlan *p, int force_global_stack) {
     // the box-rounded tile (+ mbarrier) must fit; VX_NO_TMA=1 disables it
     const char *nt = getenv("VX_NO_TMA");
     const bool tma_ok = !(nt && atoi(nt)) && nz % 4 == 0;
-    auto staged_bytes = [](int L, int B) {
+    auto staged_bytes = [](int L, int B, int tw = 32) {
         const int boxh = std::min(L, 256);
         const size_t rows = (size_t)(L + boxh - 1) / boxh * boxh;
-        return rows * 32 * 4 + (size_t)(3 * B * 32 + 32) * 4 + 16;
+        return rows * tw * 4 + (size_t)(3 * B * tw + tw) * 4 + 16;
     };
     const size_t sb2 = staged_bytes(ny, q.B2), sb3 = staged_bytes(nx, q.B3);
     q.tma2 = tma_ok && !q.s2_wide && !q.gstack2 && sb2 <= kSmemLimit;
     q.tma3 = tma_ok && !q.s2_wide && !q.e3_wide && !q.gstack3 && sb3 <= kSmemLimit;
-    // TMA-staged long columns: up to 32 bands (the 1024-thread kernel)
-    auto widen = [&](int L, bool tma, int &B, int &W, size_t &smem) {
+    // TMA-staged long columns: up to 32 bands, as 16-column tiles (32 x 16 =
+    // 512 threads; a 1024-row tile is 64 KB, three CTAs per SM) or, with
+    // VX_NARROW_TILES=0, 32-column tiles (1024 threads, one CTA per SM)
+    const char *ntl = getenv("VX_NARROW_TILES");
+    const bool narrow_ok = !(ntl && atoi(ntl) == 0);
+    q.tw2 = q.tw3 = 32;
+    // (16-column tiles for L <= 512 measured: +1-3 %, 6 CTAs/SM buy nothing there)
+    auto widen = [&](int L, bool tma, int &B, int &W, size_t &smem, int &tw) {
         if (!tma || L <= 512) return;
         const int B32 = std::min(32, pow2ceil((L + VX_BAND_ROWS - 1) / VX_BAND_ROWS));
-        if (B32 <= B || staged_bytes(L, B32) > kSmemLimit) return;
+        if (B32 <= B) return;
+        if (narrow_ok && B32 * 16 <= kColThreads && 3 * staged_bytes(L, B32, 16) <= kSmemLimit) {
+            tw = 16;
+        } else if (staged_bytes(L, B32) > kSmemLimit) {
+            return;
+        }
         B = B32;
         W = (L + B - 1) / B;
-        smem = staged_bytes(L, B);
+        smem = staged_bytes(L, B, tw);
     };
     if (q.tma2) q.smem2 = sb2;
     if (q.tma3) q.smem3 = sb3;
-    widen(ny, q.tma2, q.B2, q.W2, q.smem2);
-    widen(nx, q.tma3, q.B3, q.W3, q.smem3);
+    widen(ny, q.tma2, q.B2, q.W2, q.smem2, q.tw2);
+    widen(nx, q.tma3, q.B3, q.W3, q.smem3, q.tw3);
     q.gstack_ctas = 2 * num_sms();
     size_t gs = 0;
     if (q.gstack2) gs = std::max(gs, (size_t)q.gstack_ctas * st2);

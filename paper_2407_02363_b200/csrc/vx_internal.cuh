@@ -22,6 +22,7 @@ struct EdtPlan {
     int B3, W3;            // pass 3
     bool gstack2, gstack3; // stack in global scratch (column longer than smem allows)
     bool tma2, tma3;       // input tile staged into shared memory by TMA
+    int tw2, tw3;          // columns per TMA-staged tile (32; 16 for columns longer than 512)
     size_t smem2, smem3;   // dynamic smem bytes per CTA
     size_t s1_bytes, s2_bytes, gstack_bytes;  // scratch layout
     int gstack_ctas;       // persistent CTAs when a global stack is used

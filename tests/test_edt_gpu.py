@@ -315,3 +315,20 @@ def test_pass3_one_warp_kernel_512_specialisation(monkeypatch):
     got = pba_edt(occ).site
     monkeypatch.setenv("VX_STREAM_MAX", "-1")
     assert np.array_equal(got, pba_edt(occ).site)
+
+
+@pytest.mark.parametrize("narrow", ["1", "0"], ids=["16col-tiles", "32col-tiles"])
+def test_long_columns_vs_oracle(narrow, monkeypatch):
+    """Columns longer than 512 rows (32 bands): 16-column tiles at three CTAs
+    per SM, or 32-column tiles of 1024 threads (VX_NARROW_TILES=0); dense,
+    ragged nz, and few occupied i-slices (the compact pass-3 row staging)."""
+    monkeypatch.setenv("VX_NARROW_TILES", narrow)
+    rng = np.random.default_rng(31)
+    cases = [((700, 48, 64), 0.02), ((40, 1024, 36), 0.01), ((1024, 24, 20), 0.003)]
+    for dims, p in cases:
+        occ = (rng.random(dims) < p).astype(np.uint8)
+        assert np.array_equal(pba_edt(occ).site, O.pba_edt_site(occ)), dims
+    occ = np.zeros((900, 40, 48), np.uint8)
+    for x in rng.choice(900, 25, replace=False):
+        occ[x][rng.random((40, 48)) < 0.01] = 1
+    assert np.array_equal(pba_edt(occ).site, O.pba_edt_site(occ))
