@@ -75,6 +75,12 @@ constexpr bool kP3XW = VX_P3_XW != 0;
 #ifndef VX_CMP_GROUP_ROWS
 #define VX_CMP_GROUP_ROWS 24   // target candidates per group in compact pass 3
 #endif
+#ifndef VX_P2_REVERSE
+#define VX_P2_REVERSE 1
+#endif
+#ifndef VX_P2_EVICT_FIRST
+#define VX_P2_EVICT_FIRST 0
+#endif
 #ifndef VX_STREAM_CAP
 #define VX_STREAM_CAP 55   // shared-memory stack entries per column (k_pass3_stream; 32 warps x 55 x 128 B)
 #endif
@@ -430,6 +436,15 @@ __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, u
         ::"r"(smem_u32(dst)), "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
         : "memory");
 }
+__device__ __forceinline__ void tma_load_3d_ef(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1,
+                                               int c2) {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3, %4}], [%5], %6;"
+        ::"r"(smem_u32(dst)), "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
 __device__ __forceinline__ void tma_load_4d(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1,
                                             int c2, int c3) {
     asm volatile(
@@ -780,8 +795,12 @@ __global__ void __launch_bounds__(MAXT, MAXT >= 1024 ? 1 : kColMinBlocks) k_colu
     if constexpr (PASS == 2) {
         if (P.xs) {   // occupied-slice list: CTA rows map to occupied slices, the
                       // surplus CTAs (empty slices) all sit at the end of the grid
-            if (outer >= __ldg(P.hdr)) return;
-            outer = __ldg(P.xs + outer);
+            const int m = __ldg(P.hdr);
+            if (outer >= m) return;
+            // VX_P2_REVERSE: last occupied slice first -- pass 1 wrote the
+            // slices in ascending order, so the newest s1 lines, still in L2,
+            // are read first
+            outer = __ldg(P.xs + (VX_P2_REVERSE ? m - 1 - outer : outer));
             tile = outer * P.nkt + kt;
         } else if (P.sflag && !P.sflag[outer]) {
             return;   // empty slice: pass 3 never reads it
@@ -829,7 +848,10 @@ __global__ void __launch_bounds__(MAXT, MAXT >= 1024 ? 1 : kColMinBlocks) k_colu
             for (int q = 0; q < nbox; ++q) {
                 void *dst = stk + (size_t)q * P.boxh * TW;
                 if constexpr (PASS == 2) {
-                    tma_load_3d(dst, &tmap, bar, kt * TW, q * P.boxh, (int)outer);
+                    if constexpr (VX_P2_EVICT_FIRST)   // s1 is read once: keep s2 in L2 for pass 3
+                        tma_load_3d_ef(dst, &tmap, bar, kt * TW, q * P.boxh, (int)outer);
+                    else
+                        tma_load_3d(dst, &tmap, bar, kt * TW, q * P.boxh, (int)outer);
                 } else {
                     const int scene = (int)(outer / P.nyl);
                     const int jl = (int)(outer - (long long)scene * P.nyl);
@@ -886,6 +908,9 @@ constexpr int kStreamCap = VX_STREAM_CAP;
 #ifndef VX_WALK_UNROLL
 #define VX_WALK_UNROLL 4
 #endif
+#ifndef VX_STREAM_STCS
+#define VX_STREAM_STCS 1
+#endif
 constexpr int kWalkUnroll = VX_WALK_UNROLL;   // query-walk rows per loop trip
 
 // the one-warp pass 3 needs enough tiles to keep its warps busy: each walks its
@@ -896,6 +921,18 @@ inline long long stream_min_tiles() {
         return e ? atoll(e) : 16LL * num_sms();
     }();
     return v;
+}
+
+#ifndef VX_STREAM_LDCS
+#define VX_STREAM_LDCS 1
+#endif
+// candidate rows are read once per pass
+__device__ __forceinline__ uint32_t cand_load(const uint32_t *p) {
+#if VX_STREAM_LDCS
+    return __ldcs(p);
+#else
+    return __ldg(p);
+#endif
 }
 
 template <typename FT, typename PT, int C512>
@@ -981,14 +1018,14 @@ __global__ void __launch_bounds__(kWarpCtaThreads, 1) k_pass3_stream(const uint3
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 yr[u] = rows_s[t0 + u];
-                v[u] = __ldg(src + (uint32_t)yr[u] * ssp);
+                v[u] = cand_load(src + (uint32_t)yr[u] * ssp);
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) consume(v[u], yr[u]);
         }
         for (; t0 < m; ++t0) {
             const int yr = rows_s[t0];
-            consume(__ldg(src + (uint32_t)yr * ssp), yr);
+            consume(cand_load(src + (uint32_t)yr * ssp), yr);
         }
 #ifdef VX_PHASE_TIMING
         {   // hull size (max over the warp's columns) for tools/phase_timing
@@ -1045,7 +1082,11 @@ __global__ void __launch_bounds__(kWarpCtaThreads, 1) k_pass3_stream(const uint3
                     tt = has ? (FT)2 * (FT)(ys - yc) : (FT)0;
                     rhs = (FT)y * tt;
                 }
+#if VX_STREAM_STCS
+                __stcs(dst, ocur);   // evict-first: the sites are not re-read by this pass
+#else
                 *dst = ocur;
+#endif
                 dst += splane;
                 rhs += tt;
             }
