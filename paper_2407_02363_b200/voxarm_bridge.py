@@ -14,9 +14,10 @@ controller.py, engine.py:282-318) run unchanged on the host.
     with voxarm_bridge.installed():      # or voxarm_bridge.install()
         log = voxarm.engine.run_scenario(sc)
 
-The engine's outlier filter default (k_neighbors=8) has no GPU version yet
-(grids.insert_point_cloud raises NotImplementedError): use scenarios with
-``CloudConfig(k_neighbors=0)``.
+The engine's default statistical outlier filter (k_neighbors=8,
+grids.py:224-240) runs on the device too (vx_outlier.cu), so the shipped
+scenarios run unmodified; tests/test_acceptance_gpu.py checks their CSV logs
+against the CPU engine's.
 """
 
 from __future__ import annotations
