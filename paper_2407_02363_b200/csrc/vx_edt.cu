@@ -97,6 +97,10 @@ constexpr int kStreamMaxRows = VX_STREAM_MAX_ROWS;
 #ifndef VX_COL_MIN_BLOCKS
 #define VX_COL_MIN_BLOCKS 2
 #endif
+#ifndef VX_COL_WALK_UNROLL
+#define VX_COL_WALK_UNROLL 4   // phase-D rows per loop trip in the banded column kernels
+#endif
+constexpr int kColWalkUnroll = VX_COL_WALK_UNROLL;
 constexpr int kColMinBlocks = VX_COL_MIN_BLOCKS;
 
 // bit e (e = 0..3) set iff byte e of w is non-zero
@@ -737,6 +741,7 @@ __device__ __forceinline__ void column_tile(const typename Col<PASS, S2W, EW, FW
             FT dN = spos >= 0 ? Fs - Fc : kNever;
             FT t = spos >= 0 ? (FT)2 * (FT)(ys - yc) : (FT)0;
             FT rhs = (FT)lo * t;
+#pragma unroll kColWalkUnroll
             for (int y = lo; y < hi; ++y, rhs += t) {
                 if (dN < rhs) {
                     InT ccode = scode;
