@@ -270,6 +270,25 @@ def test_pass3_one_warp_kernel_vs_oracle(deep, monkeypatch):
     assert np.array_equal(pba_edt(occ).site, want)
 
 
+@pytest.mark.parametrize("deep", [False, True], ids=["shallow", "deep-spill"])
+def test_pass3_one_warp_kernel_multi_tile(deep, monkeypatch):
+    """k_pass3_stream with more tiles than warps (6400 tiles > 148 x 32): warps
+    walk a second tile after their first, re-using their stacks (deep: the
+    global spill slab too); equal to the oracle and to the banded kernel."""
+    rng = np.random.default_rng(11)
+    occ = np.zeros((160, 1536, 128), np.uint8)
+    xs = np.sort(rng.choice(160, 80 if deep else 50, replace=False))
+    pts = rng.integers(0, [1536, 128], size=(50, 2))
+    for x in xs:
+        occ[x][rng.random((1536, 128)) < 0.001] = 1
+        if deep:
+            occ[x, pts[:, 0], pts[:, 1]] = 1
+    want = O.pba_edt_site(occ)
+    assert np.array_equal(pba_edt(occ).site, want)
+    monkeypatch.setenv("VX_STREAM_MAX", "-1")   # banded kernel only
+    assert np.array_equal(pba_edt(occ).site, want)
+
+
 def test_cycle_pass3_kernel_choice(monkeypatch):
     """The camera tick picks its pass-3 kernel from the previous tick's
     occupied-slice count (host-mapped hint); every choice, and every switch
