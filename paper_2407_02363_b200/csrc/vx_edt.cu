@@ -94,6 +94,12 @@ constexpr int kStreamMaxRows = VX_STREAM_MAX_ROWS;
 #ifndef VX_BAND_ROWS
 #define VX_BAND_ROWS 32   // target rows per band
 #endif
+#ifndef VX_P1_WAVES
+#define VX_P1_WAVES 1   // pass 1 over occupied slices: persistent CTAs per SM / 8
+#endif
+#ifndef VX_P1_LPW512
+#define VX_P1_LPW512 1  // lines per warp iteration for nz <= 512 (occupied-slice path)
+#endif
 #ifndef VX_COL_MIN_BLOCKS
 #define VX_COL_MIN_BLOCKS 2
 #endif
@@ -188,19 +194,24 @@ __global__ void __launch_bounds__(256) k_pass1_v4(const uint8_t *__restrict__ oc
                                                   const uint8_t *__restrict__ sflag, int ny,
                                                   const int *__restrict__ xs, const int *__restrict__ hdr) {
     const int lane = threadIdx.x & 31;
-    const long long line0 = ((long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * LPW;
     const int nq = nz >> 2;
     uint32_t nib[LPW][CMAX];
     bool act[LPW];
     long long lines[LPW];
     const int m = xs ? __ldg(hdr) : 0;
+    // the occupied-slice path runs a persistent grid over the m * ny lines
+    // (m is read here); the dense path's grid covers every line once
+    const long long total = xs ? (long long)m * ny : nlines;
+    const long long wstep = (long long)gridDim.x * (blockDim.x >> 5) * LPW;
+    for (long long line0 = ((long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * LPW; line0 < total;
+         line0 += wstep) {
 #pragma unroll
     for (int l = 0; l < LPW; ++l) {
         long long line = line0 + l;
         // warp-uniform; empty slices are skipped (nothing downstream reads them)
-        if (xs) {   // lines of occupied slices first (slot-major), the surplus idles
+        if (xs) {   // lines of occupied slices, slot-major
             const uint32_t slot = (uint32_t)line / (uint32_t)ny;
-            act[l] = (int)slot < m;
+            act[l] = line < total;
             if (act[l]) line = (long long)__ldg(xs + slot) * ny + (line - (long long)slot * ny);
         } else {
             act[l] = line < nlines && (!sflag || sflag[(uint32_t)line / (uint32_t)ny]);
@@ -229,6 +240,7 @@ __global__ void __launch_bounds__(256) k_pass1_v4(const uint8_t *__restrict__ oc
             continue;
         }
         pass1_line<CMAX>(nib[l], dst, nq, lane);
+    }
     }
 }
 
@@ -1446,11 +1458,16 @@ cudaError_t launch_pass1(const uint8_t *occ, int32_t *s1, long long nslices, int
     if (nlines == 0) return cudaSuccess;
     const uint8_t *sflag = sp ? sp->sflag : nullptr;
     const int *xs = sp ? sp->xs : nullptr, *hdr = sp ? sp->hdr : nullptr;
-    const unsigned grid = (unsigned)((nlines + 7) / 8);
-    const unsigned grid2 = (unsigned)((nlines + 15) / 16);
+    unsigned grid = (unsigned)((nlines + 7) / 8);
+    unsigned grid2 = (unsigned)((nlines + 15) / 16);
+    if (xs) {   // persistent: VX_P1_WAVES x 8 CTAs of 256 threads per SM
+        grid = (unsigned)std::min<long long>(grid, (long long)num_sms() * 8 * VX_P1_WAVES);
+        grid2 = (unsigned)std::min<long long>(grid2, (long long)num_sms() * 8 * VX_P1_WAVES);
+    }
     const bool vec = (nz % 4 == 0) && ((uintptr_t)occ % 16 == 0) && ((uintptr_t)s1 % 16 == 0);
     if (vec && nz <= 128) k_pass1_v4<1, 2><<<grid2, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny, xs, hdr);
     else if (vec && nz <= 256) k_pass1_v4<2, 2><<<grid2, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny, xs, hdr);
+    else if (vec && nz <= 512 && xs && VX_P1_LPW512 == 2) k_pass1_v4<4, 2><<<grid2, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny, xs, hdr);
     else if (vec && nz <= 512) k_pass1_v4<4, 1><<<grid, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny, xs, hdr);
     else if (vec && nz <= 1024) k_pass1_v4<8, 1><<<grid, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny, xs, hdr);
     else if (vec && nz <= 2048) k_pass1_v4<16, 1><<<grid, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny, xs, hdr);
