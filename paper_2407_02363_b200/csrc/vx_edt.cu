@@ -807,13 +807,15 @@ __global__ void __launch_bounds__(MAXT, MAXT >= 1024 ? 1 : kColMinBlocks) k_colu
     int *meta = reinterpret_cast<int *>(smem + (size_t)P.rows_alloc * TW * sizeof(EntT));
     uint64_t *bar = reinterpret_cast<uint64_t *>(meta + 3 * P.B * TW + TW);
     long long tile = blockIdx.x;
+    if constexpr (PASS == 2) {   // surplus CTAs leave before any index math
+        if (P.xs && (long long)blockIdx.x >= (long long)__ldg(P.hdr) * P.nkt) return;
+    }
     const int kt = (int)(tile % P.nkt);
     long long outer = tile / P.nkt;
     if constexpr (PASS == 2) {
         if (P.xs) {   // occupied-slice list: CTA rows map to occupied slices, the
                       // surplus CTAs (empty slices) all sit at the end of the grid
             const int m = __ldg(P.hdr);
-            if (outer >= m) return;
             // VX_P2_REVERSE: last occupied slice first -- pass 1 wrote the
             // slices in ascending order, so the newest s1 lines, still in L2,
             // are read first
