@@ -905,6 +905,16 @@ struct vx_cycle {
     long long pf_n[2] = {-1, -1};
     int pf_next = 0;
     cudaGraphExec_t gexec = nullptr;
+    cudaGraph_t graph = nullptr;   // kept while gexec lives (its reset node is updated per tick)
+    // the graph's reset node copies the per-step block from the host-mapped
+    // staging slot of the tick: its CopySpan source is set before each launch
+    cudaGraphNode_t g_reset = nullptr;
+    cudaKernelNodeParams g_reset_kp = {};
+    ResetArgs g_ra = {}, g_rb = {};
+    ZeroSpan g_z[3] = {};
+    CopySpan g_cp = {};
+    unsigned char *d_hstage[kStage] = {};   // device views of h_stage (mapped)
+    bool capturing = false;
     int g_s = -1;
     float g_hit = 0.f;
     double g_thr = 0.0;
@@ -919,6 +929,7 @@ struct vx_cycle {
         if (profiling && ring_n < kRing) cudaEventRecord(ev[ring_n][phase], ctx->stream);
     }
 };
+static void drop_graph(vx_cycle *cy);
 
 static void av_free(vx_cycle *cy);
 
@@ -994,11 +1005,12 @@ extern "C" int vx_cycle_create(vx_ctx *c, int nx, int ny, int nz, double vs, con
     if (e == cudaSuccess) e = cudaMalloc(&cy->d_world, 2 * S * 24);
     if (e == cudaSuccess) e = cudaMalloc(&cy->d_dist, 2 * S * 8);
     if (e == cudaSuccess) e = cudaHostAlloc(&cy->h_npts, sizeof(long long), cudaHostAllocPortable);
-    cy->stage_bytes = 64 + (size_t)nlinks * 128 + S * 24;
+    cy->stage_bytes = (64 + (size_t)nlinks * 128 + S * 24 + 15) & ~(size_t)15;
     if (e == cudaSuccess) e = cudaMalloc(&cy->d_stage, cy->stage_bytes);
     if (const char *ev = getenv("VX_STAGE_SLOTS")) cy->nstage = std::max(1, std::min(vx_cycle::kStage, atoi(ev)));
     for (int b = 0; b < vx_cycle::kStage && e == cudaSuccess; ++b) {
-        e = cudaHostAlloc(&cy->h_stage[b], cy->stage_bytes, cudaHostAllocPortable);
+        e = cudaHostAlloc(&cy->h_stage[b], cy->stage_bytes, cudaHostAllocMapped | cudaHostAllocPortable);
+        if (e == cudaSuccess) e = cudaHostGetDevicePointer((void **)&cy->d_hstage[b], cy->h_stage[b], 0);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&cy->ev_stage[b], cudaEventDisableTiming);
     }
     if (e == cudaSuccess) {   // the graph reads frames, centres and the count from the staged block
@@ -1066,7 +1078,7 @@ extern "C" int vx_cycle_destroy(vx_cycle *cy) {
         if (cy->ev_used[b]) cudaEventDestroy(cy->ev_used[b]);
     }
     if (cy->cst) cudaStreamDestroy(cy->cst);
-    if (cy->gexec) cudaGraphExecDestroy(cy->gexec);
+    drop_graph(cy);
     cudaFree(cy->env_f.site);
     cudaFree(cy->self_f.site);
     cudaFree(cy->scratch);
@@ -1123,6 +1135,14 @@ static cudaError_t edt_passes(vx_cycle *cy, const vx_grid *src, int32_t *site, b
 // engine.py:236-254 and 272-280: mask <- all links; env <- cloud minus mask;
 // EDT of env; the per-sphere gather on both fields.  n_dev (graph mode): the
 // point count is read on the device and npts only sizes the launch.
+static void drop_graph(vx_cycle *cy) {
+    if (cy->gexec) cudaGraphExecDestroy(cy->gexec);
+    if (cy->graph) cudaGraphDestroy(cy->graph);
+    cy->gexec = nullptr;
+    cy->graph = nullptr;
+    cy->g_reset = nullptr;
+}
+
 static int cycle_main_seq(vx_cycle *cy, const double *d_pts, long long npts, const long long *n_dev,
                           float hit, double thr, int s, bool marks) {
     vx_ctx *c = cy->ctx;
@@ -1145,10 +1165,28 @@ static int cycle_main_seq(vx_cycle *cy, const double *d_pts, long long npts, con
                            cy->mask->sparse_ok ? 0 : 1};
         const ResetArgs rb{cy->env->cells, cy->env->occ, cy->env->touched, cy->env->ctr, cy->env->n,
                            cy->env->sparse_ok ? 0 : 1};
-        cudaError_t e = launch_reset2(ra, rb, ZeroSpan{sflag, sflag ? (size_t)cy->plan.nx : 0},
-                                      ZeroSpan{cy->mask->set_oob, cy->nlinks ? (size_t)cy->nlinks * 8 : 0},
-                                      ZeroSpan{cy->env->ctr, 3 * sizeof(unsigned long long)}, st);
+        const ZeroSpan z0{sflag, sflag ? (size_t)cy->plan.nx : 0},
+            z1{cy->mask->set_oob, cy->nlinks ? (size_t)cy->nlinks * 8 : 0},
+            z2{cy->env->ctr, 3 * sizeof(unsigned long long)};
+        // captured into the graph: the node also fetches the staged block
+        // (source slot set per tick by cycle_step)
+        const CopySpan cp = cy->capturing ? CopySpan{cy->d_stage, cy->d_hstage[0], cy->stage_bytes}
+                                          : CopySpan{nullptr, nullptr, 0};
+        cudaError_t e = launch_reset2(ra, rb, z0, z1, z2, st, cp);
         if (e != cudaSuccess) return cuda_fail(e, "reset");
+        if (cy->capturing) {   // the node just added: the capture's only dependency now
+            cudaStreamCaptureStatus cs;
+            const cudaGraphNode_t *deps = nullptr;
+            size_t ndeps = 0;
+            e = cudaStreamGetCaptureInfo(st, &cs, nullptr, nullptr, &deps, &ndeps);
+            if (e != cudaSuccess || ndeps != 1) return cuda_fail(e != cudaSuccess ? e : cudaErrorUnknown, "capture info");
+            cy->g_reset = deps[0];
+            e = cudaGraphKernelNodeGetParams(cy->g_reset, &cy->g_reset_kp);
+            if (e != cudaSuccess) return cuda_fail(e, "reset node params");
+            cy->g_ra = ra; cy->g_rb = rb;
+            cy->g_z[0] = z0; cy->g_z[1] = z1; cy->g_z[2] = z2;
+            cy->g_cp = cp;
+        }
         c->launches += 1;
         for (vx_grid *g : {cy->mask, cy->env}) {   // as grid_clear_async
             g->sparse_ok = true;
@@ -1215,8 +1253,11 @@ static int cycle_step(vx_cycle *cy, const double *pts, const double *d_pts_in, i
     for (int q = 0; q < cy->nself; ++q) std::memcpy(&Ts[16 * q], link_T + 16 * cy->self_links[q], 128);
     const double *d_pts = d_pts_in ? d_pts_in : cy->d_pts;
     if (npts && !d_pts_in) VX_CUDA(cudaMemcpyAsync(cy->d_pts, pts, (size_t)npts * 24, cudaMemcpyHostToDevice, st));
+    const bool graph_path = cy->use_graph && !cy->profiling;
+    int stage_b = 0;
     {
         const int b = cy->stage_slot;
+        stage_b = b;
         cy->stage_slot = (b + 1) % cy->nstage;
         VX_CUDA(cudaEventSynchronize(cy->ev_stage[b]));   // its previous copy has been read
         unsigned char *h = cy->h_stage[b];
@@ -1226,8 +1267,10 @@ static int cycle_step(vx_cycle *cy, const double *pts, const double *d_pts_in, i
         if (cy->nlinks) std::memcpy(h + 64, link_T, (size_t)128 * cy->nlinks);
         if (s) std::memcpy(h + 64 + (size_t)128 * cy->nlinks, centers, (size_t)s * 24);
         const size_t bytes = 64 + (size_t)128 * cy->nlinks + (size_t)s * 24;
-        VX_CUDA(cudaMemcpyAsync(cy->d_stage, h, bytes, cudaMemcpyHostToDevice, st));
-        VX_CUDA(cudaEventRecord(cy->ev_stage[b], st));
+        if (!graph_path) {   // the graph's reset node reads the mapped slot itself
+            VX_CUDA(cudaMemcpyAsync(cy->d_stage, h, bytes, cudaMemcpyHostToDevice, st));
+            VX_CUDA(cudaEventRecord(cy->ev_stage[b], st));
+        }
     }
     if (cy->av_s && s == cy->av_s)
         VX_CUDA(cudaMemcpyAsync(cy->d_frames, cy->h_frames, (size_t)cy->av_nj * 48, cudaMemcpyHostToDevice, st));
@@ -1249,15 +1292,16 @@ static int cycle_step(vx_cycle *cy, const double *pts, const double *d_pts_in, i
         cy->self_recomputed = 1;
     }
     cy->mark(2);
-    if (cy->use_graph && !cy->profiling) {
+    if (graph_path) {
         // the graph reads the cloud pointer and its size from the staged block
         cy->p3_mode = pass3_mode_hint(cy->plan, *(volatile int *)cy->h_m);
         if (!cy->gexec || cy->g_s != s || cy->g_hit != hit || cy->g_thr != thr || cy->g_mode != cy->p3_mode) {
-            if (cy->gexec) cudaGraphExecDestroy(cy->gexec);
-            cy->gexec = nullptr;
+            drop_graph(cy);
             const long long l0 = c->launches;
             VX_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed));
+            cy->capturing = true;
             rc = cycle_main_seq(cy, nullptr, cy->max_points, cy->d_npts, hit, thr, s, false);
+            cy->capturing = false;
             cudaGraph_t graph = nullptr;
             cudaError_t ce = cudaStreamEndCapture(st, &graph);
             if (rc) {
@@ -1266,8 +1310,11 @@ static int cycle_step(vx_cycle *cy, const double *pts, const double *d_pts_in, i
             }
             if (ce != cudaSuccess) return cuda_fail(ce, "cudaStreamEndCapture");
             ce = cudaGraphInstantiate(&cy->gexec, graph, 0);
-            cudaGraphDestroy(graph);
-            if (ce != cudaSuccess) return cuda_fail(ce, "cudaGraphInstantiate");
+            cy->graph = graph;
+            if (ce != cudaSuccess) {
+                drop_graph(cy);
+                return cuda_fail(ce, "cudaGraphInstantiate");
+            }
             cy->g_kernels = c->launches - l0;
             c->launches = l0;
             cy->g_s = s;
@@ -1275,7 +1322,17 @@ static int cycle_step(vx_cycle *cy, const double *pts, const double *d_pts_in, i
             cy->g_hit = hit;
             cy->g_thr = thr;
         }
+        {   // this tick's staging slot -> the reset node's copy source
+            CopySpan cp = cy->g_cp;
+            cp.src = cy->d_hstage[stage_b];
+            void *args[] = {&cy->g_ra, &cy->g_rb, &cy->g_z[0], &cy->g_z[1], &cy->g_z[2], &cp};
+            cudaKernelNodeParams kp = cy->g_reset_kp;
+            kp.kernelParams = args;
+            kp.extra = nullptr;
+            VX_CUDA(cudaGraphExecKernelNodeSetParams(cy->gexec, cy->g_reset, &kp));
+        }
         VX_CUDA(cudaGraphLaunch(cy->gexec, st));
+        VX_CUDA(cudaEventRecord(cy->ev_stage[stage_b], st));   // the graph read the slot
         c->launches += cy->g_kernels;
         if (pf_slot >= 0) VX_CUDA(cudaEventRecord(cy->ev_used[pf_slot], st));   // the tick read the slot
     } else {
@@ -1396,8 +1453,7 @@ extern "C" int vx_cycle_set_avoidance(vx_cycle *cy, int s, const double *radius,
     cudaStream_t st = cy->ctx->stream;
     VX_CUDA(cudaStreamSynchronize(st));
     av_free(cy);
-    if (cy->gexec) cudaGraphExecDestroy(cy->gexec);
-    cy->gexec = nullptr;
+    drop_graph(cy);
     if (!s) return VX_OK;
     const int nj = n_joints > 0 ? n_joints : 1;
     cudaError_t e = cudaMalloc(&cy->d_av_par, (size_t)2 * s * 8);

@@ -110,8 +110,13 @@ struct ZeroSpan {
     void *p;
     size_t bytes;
 };
+struct CopySpan {   // a small block copied by the reset launch (16-byte units)
+    void *dst;
+    const void *src;   // may be host-mapped pinned memory
+    size_t bytes;
+};
 cudaError_t launch_reset2(const ResetArgs &a, const ResetArgs &b, ZeroSpan z0, ZeroSpan z1, ZeroSpan z2,
-                          cudaStream_t st);
+                          cudaStream_t st, CopySpan cp = CopySpan{nullptr, nullptr, 0});
 cudaError_t launch_reset(float *cells, uint8_t *occ, int32_t *touched, DevCounters *ctr,
                          int64_t n, int capacity, bool dense, cudaStream_t st);
 cudaError_t launch_dense_clip(float *cells, const uint32_t *counts, int64_t n,

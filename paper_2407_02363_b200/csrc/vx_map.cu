@@ -105,10 +105,18 @@ __global__ void k_reset(ResetArgs r) {
 // commits in its own last block); block (0, 0) also zeroes up to three small
 // buffers (slice flags, per-link OOB counters, insert stats) that would
 // otherwise be memset nodes of their own
-__global__ void k_reset2(ResetArgs a, ResetArgs b, ZeroSpan z0, ZeroSpan z1, ZeroSpan z2) {
+// Block (0, 1) also copies `cp` (the camera tick's per-step arguments, read
+// straight from the host-mapped staging slot, so the tick needs no H2D copy
+// of its own; the graph node's source pointer is updated per tick).
+__global__ void k_reset2(ResetArgs a, ResetArgs b, ZeroSpan z0, ZeroSpan z1, ZeroSpan z2, CopySpan cp) {
     if (blockIdx.x == 0 && blockIdx.y == 0) {
         for (const ZeroSpan &z : {z0, z1, z2})
             for (size_t i = threadIdx.x; i < z.bytes; i += blockDim.x) static_cast<unsigned char *>(z.p)[i] = 0;
+    }
+    if (blockIdx.x == 0 && blockIdx.y == 1 && cp.bytes) {
+        const uint4 *src = static_cast<const uint4 *>(cp.src);
+        uint4 *dst = static_cast<uint4 *>(cp.dst);
+        for (size_t i = threadIdx.x; i < cp.bytes / 16; i += blockDim.x) dst[i] = src[i];
     }
     reset_body(blockIdx.y ? b : a, (long long)blockIdx.x * blockDim.x + threadIdx.x,
                (long long)gridDim.x * blockDim.x);
@@ -333,10 +341,10 @@ cudaError_t launch_reset(float *cells, uint8_t *occ, int32_t *touched, DevCounte
 }
 
 cudaError_t launch_reset2(const ResetArgs &a, const ResetArgs &b, ZeroSpan z0, ZeroSpan z1, ZeroSpan z2,
-                          cudaStream_t st) {
+                          cudaStream_t st, CopySpan cp) {
     const long long work = std::max(a.dense ? a.n / 4 + 1 : 0LL, b.dense ? b.n / 4 + 1 : 0LL);
     const unsigned g = work ? std::max(grid_for(work, 256), (unsigned)(num_sms() * 2)) : (unsigned)(num_sms() * 2);
-    k_reset2<<<dim3(g, 2), 256, 0, st>>>(a, b, z0, z1, z2);
+    k_reset2<<<dim3(g, 2), 256, 0, st>>>(a, b, z0, z1, z2, cp);
     return cudaGetLastError();
 }
 
