@@ -249,7 +249,8 @@ static bool same_geometry(const vx_grid *a, const vx_grid *b) {  // grids.py:214
 // flags the occupied i-slices for the EDT; *flags_done says whether it did
 static int insert_device(vx_grid *g, const double *d_xyz, long long n, const long long *n_dev,
                          float hit, double thr, const vx_grid *mask, const uint8_t *keep = nullptr,
-                         uint8_t *sflag = nullptr, bool *flags_done = nullptr, bool stats_zeroed = false) {
+                         uint8_t *sflag = nullptr, bool *flags_done = nullptr, bool stats_zeroed = false,
+                         const SparseRows *list = nullptr) {
     if (mask && !same_geometry(g, mask))
         return fail(VX_EINVAL, "robot_mask geometry does not match this grid");
     cudaStream_t st = g->ctx->stream;
@@ -270,8 +271,11 @@ static int insert_device(vx_grid *g, const double *d_xyz, long long n, const lon
         g->ctx->launches += 1;
     }
     uint8_t *fl = fresh ? sflag : nullptr;
+    // list (with the flags): finalize's last block also builds the occupied-slice list
     e = launch_finalize(g->cells, g->occ, counts, g->touched, g->ctr, g->n, g->capacity,
-                        n > 0 ? n : 1, hit, kOccThr, st, fresh, fl, (long long)g->g.ny * g->g.nz, g->g.nx);
+                        n > 0 ? n : 1, hit, kOccThr, st, fresh, fl, (long long)g->g.ny * g->g.nz, g->g.nx,
+                        list ? const_cast<int *>(list->xs) : nullptr, list ? const_cast<int *>(list->hdr) : nullptr,
+                        list ? list->m_mirror : nullptr);
     if (flags_done) *flags_done = fl != nullptr;
     if (e != cudaSuccess) return cuda_fail(e, "finalize");
     g->ctx->launches += 1;
@@ -1093,7 +1097,7 @@ extern "C" int vx_cycle_destroy(vx_cycle *cy) {
 // occupied voxel the slice flags come from that list
 // flags_ready: the occupied-slice flags were set by the insert's finalize
 static cudaError_t edt_passes(vx_cycle *cy, const vx_grid *src, int32_t *site, bool marks,
-                              bool flags_ready = false) {
+                              bool flags_ready = false, bool list_ready = false) {
     const uint8_t *occ = src->occ;
     unsigned char *base = static_cast<unsigned char *>(cy->scratch);
     const EdtPlan &p = cy->plan;
@@ -1112,7 +1116,9 @@ static cudaError_t edt_passes(vx_cycle *cy, const vx_grid *src, int32_t *site, b
             sp.m_mirror = cy->d_m;
             sp.p3_mode = cy->p3_mode;
         }
-        if (flags_ready) {
+        if (list_ready) {
+            // the insert's finalize built the list (and the host-mapped hint)
+        } else if (flags_ready) {
             e = launch_slice_list_only(p, sp, st);
             cy->ctx->launches += 1;
         } else {
@@ -1149,13 +1155,16 @@ static int cycle_main_seq(vx_cycle *cy, const double *d_pts, long long npts, con
     cudaStream_t st = c->stream;
     int rc;
     // the env EDT's occupied-slice flags come out of the (fresh-grid) finalize
+    // (and, from its last block, the occupied-slice list and the host-mapped hint)
     uint8_t *sflag = nullptr;
+    SparseRows sp_env{};
     if (sparse_ok(cy->plan, 1)) {
         const EdtPlan &p = cy->plan;
         const size_t nv = (size_t)p.nx * p.ny * p.nz;
         const size_t s1b = (nv * 4 + 255) & ~(size_t)255, s2b = (nv * (p.s2_wide ? 8 : 4) + 255) & ~(size_t)255;
-        sflag = const_cast<uint8_t *>(
-            sparse_rows_at(static_cast<unsigned char *>(cy->scratch) + s1b + s2b + p.gstack_bytes, p).sflag);
+        sp_env = sparse_rows_at(static_cast<unsigned char *>(cy->scratch) + s1b + s2b + p.gstack_bytes, p);
+        sp_env.m_mirror = cy->d_m;
+        sflag = const_cast<uint8_t *>(sp_env.sflag);
     }
     // one launch resets the mask and env grids and zeroes the slice flags, the
     // mask's per-link OOB counters and the env insert stats
@@ -1199,11 +1208,13 @@ static int cycle_main_seq(vx_cycle *cy, const double *d_pts, long long npts, con
         return rc;
     if (marks) cy->mark(3);
     bool flags_ready = sflag != nullptr;   // no points: the zeroed flags are right
+    bool list_ready = false;
     if ((npts || n_dev) && (rc = insert_device(cy->env, d_pts, npts, n_dev, hit, thr, cy->mask, nullptr, sflag,
-                                               &flags_ready, true)))
+                                               &flags_ready, true, sflag ? &sp_env : nullptr)))
         return rc;
+    if (npts || n_dev) list_ready = flags_ready;
     if (marks) cy->mark(4);
-    cudaError_t e = edt_passes(cy, cy->env, cy->env_f.site, marks, flags_ready);
+    cudaError_t e = edt_passes(cy, cy->env, cy->env_f.site, marks, flags_ready, list_ready);
     if (e != cudaSuccess) return cuda_fail(e, "edt(env)");
     const GridGeom g = cy->env->g;
     e = launch_gather_pack(cy->env_f.site, cy->self_f.site, g, cy->d_centers, s, cy->d_lin, cy->d_world,

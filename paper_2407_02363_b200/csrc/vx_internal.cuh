@@ -128,7 +128,8 @@ cudaError_t launch_scatter(const double *pts, int64_t npts, const int64_t *npts_
 cudaError_t launch_finalize(float *cells, uint8_t *occ, uint32_t *counts, int32_t *touched,
                             DevCounters *ctr, int64_t n, int capacity, int64_t max_new,
                             float hit, float occ_thr, cudaStream_t st, bool fresh = false,
-                            uint8_t *sflag = nullptr, long long plane = 0, int nx = 0);
+                            uint8_t *sflag = nullptr, long long plane = 0, int nx = 0,
+                            int *xs = nullptr, int *hdr = nullptr, int *m_mirror = nullptr);
 cudaError_t launch_stamp(const int32_t *ijk, const int64_t *offsets, int nsets,
                          const double *set_origin, const double *set_vs, const double *T,
                          GridGeom g, float *cells, uint8_t *occ, float value, float occ_thr,

@@ -216,7 +216,8 @@ __global__ void k_finalize(float *__restrict__ cells, uint8_t *__restrict__ occ,
                            uint32_t *__restrict__ counts, const int32_t *__restrict__ touched,
                            DevCounters *__restrict__ ctr, long long n, float hit,
                            float occ_thr, int capacity, int fresh, uint8_t *__restrict__ sflag,
-                           long long plane, int nx) {
+                           long long plane, int nx, int *__restrict__ xs, int *__restrict__ hdr,
+                           int *__restrict__ m_mirror) {
     // sflag (fresh grids only): every occupied voxel is one of this insert's,
     // so the EDT's occupied-slice flags are set here (per-CTA bitmap, one
     // store per slice and CTA) and need no pass over the touched list
@@ -248,11 +249,51 @@ __global__ void k_finalize(float *__restrict__ cells, uint8_t *__restrict__ occ,
         for (int w = threadIdx.x; w < (nx + 31) / 32; w += blockDim.x)
             for (unsigned b = bits[w]; b; b &= b - 1) sflag[w * 32 + __ffs(b) - 1] = 1;
     }
-    if (last_block(ctr)) {   // commit
+    // last block: commit; with xs it also builds the EDT's occupied-slice list
+    // from the finished flags (what k_slice_list would do in a launch of its own)
+    __shared__ bool is_last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        is_last = atomicAdd(&ctr->done, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!is_last) return;
+    if (threadIdx.x == 0) {   // commit
+        ctr->done = 0u;
+        __threadfence();
         const long long t = (long long)ctr->touched + ctr->pending;
         ctr->touched = t > capacity ? capacity : (int)t;
         ctr->pending = 0;
         if (ctr->inserted) ctr->dirty = 1;
+    }
+    if (!xs) return;
+    __threadfence();
+    __shared__ int wsum[32];
+    __shared__ int base_s;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    if (threadIdx.x == 0) base_s = 0;
+    __syncthreads();
+    for (int c0 = 0; c0 < nx; c0 += blockDim.x) {   // ascending slice indices
+        const int x = c0 + threadIdx.x;
+        const int f = (x < nx && __ldcg(sflag + x)) ? 1 : 0;
+        const unsigned fm = __ballot_sync(VX_FULL_MASK, f);
+        if (lane == 0) wsum[warp] = __popc(fm);
+        __syncthreads();
+        int wbase = 0, tot = 0;
+        for (int q = 0; q < nwarps; ++q) {
+            if (q < warp) wbase += wsum[q];
+            tot += wsum[q];
+        }
+        const int base = base_s;
+        if (f) xs[base + wbase + __popc(fm & ((1u << lane) - 1u))] = x;
+        __syncthreads();
+        if (threadIdx.x == 0) base_s = base + tot;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        hdr[0] = base_s;
+        if (m_mirror) *(volatile int *)m_mirror = base_s;   // host-mapped hint
     }
 }
 
@@ -366,13 +407,13 @@ cudaError_t launch_scatter(const double *pts, int64_t npts, const int64_t *npts_
 cudaError_t launch_finalize(float *cells, uint8_t *occ, uint32_t *counts, int32_t *touched,
                             DevCounters *ctr, int64_t n, int capacity, int64_t max_new, float hit,
                             float occ_thr, cudaStream_t st, bool fresh, uint8_t *sflag, long long plane,
-                            int nx) {
+                            int nx, int *xs, int *hdr, int *m_mirror) {
     // grid-stride over the new touched entries (<= max_new; a dense overflow
     // sweep loops): few blocks, so the last-block commit's atomic is cheap
     const long long work = n < max_new ? n : max_new;
     const unsigned gf = (unsigned)std::min<long long>(grid_for(work, 256), 2LL * num_sms());
     k_finalize<<<gf, 256, 0, st>>>(cells, occ, counts, touched, ctr, n, hit, occ_thr, capacity, fresh ? 1 : 0,
-                                   sflag, plane, nx);
+                                   sflag, plane, nx, sflag ? xs : nullptr, hdr, m_mirror);
     return cudaGetLastError();
 }
 
