@@ -92,21 +92,34 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
+            # nvidia-smi takes ~0.1-0.5 s to print its first row: wait for it
+            # so the samples fall inside the timed region, not after it
+            t_wait = time.perf_counter() + 5.0
+            while not self.rows and time.perf_counter() < t_wait:
+                time.sleep(0.01)
         except Exception:
             self.proc = None
+        self.t_start = time.perf_counter()
         return self
 
     def _read(self):
         for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
+            self.rows.append((time.perf_counter(), [x.strip() for x in line.split(",")]))
 
     def __exit__(self, *exc):
+        self.t_end = time.perf_counter()
         if self.proc:
-            time.sleep(0.25)
+            # a region shorter than the sampling period: take the next row
+            # (the clocks have not moved in 50 ms) and say so in the summary
+            if not any(self.t_start <= t for t, _ in self.rows):
+                t_wait = time.perf_counter() + 0.3
+                while time.perf_counter() < t_wait and not any(
+                        self.t_start <= t for t, _ in self.rows):
+                    time.sleep(0.005)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=2)
@@ -115,14 +128,19 @@ class ClockSampler:
         return False
 
     def summary(self):
-        if not self.rows:
+        rows = [r for t, r in self.rows if self.t_start <= t <= self.t_end]
+        window = "timed region"
+        if not rows:
+            rows = [r for t, r in self.rows if t > self.t_end][:1]
+            window = "first sample after the timed region (shorter than the 50 ms period)"
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({n for r in self.rows for n, v in zip(names, r[5:9]) if v == "Active"})
+        reasons = sorted({n for r in rows for n, v in zip(names, r[5:9]) if v == "Active"})
         return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows), "window": window}
 
 
 def dist_init():
@@ -683,13 +701,17 @@ def c5_slab(rank: int, world: int):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--steps", type=int, default=None,
+                    help="timed steps (default: 2000 ticks, ~0.8 s, so nvidia-smi samples the "
+                         "clocks under load; 30 for --impl reference)")
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-sweep", action="store_true", help="skip the C3 EDT latency sweep")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
+    if args.steps is None:
+        args.steps = 30 if args.impl == "reference" else 2000
     world, rank, local = dist_init()
     if args.impl == "reference":
         run_reference(args, world, rank)
