@@ -224,7 +224,9 @@ def run_reference(args, world, rank):
         return
     from oracle import oracle as O
     O.build()
-    threads = O.max_threads()
+    # every host core: torchrun exports OMP_NUM_THREADS=1 to each rank, but
+    # only rank 0 runs the CPU path, so the OpenMP default would undercount
+    threads = max(O.max_threads(), len(os.sched_getaffinity(0)))
     d = desk7()
     n = float(np.prod(DIMS))
     pts, frames, centers = scene_inputs(0, 0, d)
@@ -267,7 +269,9 @@ def cpu_baseline_sample(d):
     """Bounded CPU sample (~10-30 s): two full 512^3 ticks after one warm-up."""
     from oracle import oracle as O
     O.build()
-    threads = O.max_threads()
+    # every host core: torchrun exports OMP_NUM_THREADS=1 to each rank, but
+    # only rank 0 runs the CPU path, so the OpenMP default would undercount
+    threads = max(O.max_threads(), len(os.sched_getaffinity(0)))
     pts, frames, centers = scene_inputs(0, 0, d)
     cpu_cycle(pts, frames, centers, d, threads)
     ts = []
