@@ -44,6 +44,11 @@ __device__ __forceinline__ long long discretize(double px, double py, double pz,
 }
 
 // warp-aggregated counter add (one atomic per warp)
+__device__ __forceinline__ void warp_sum(unsigned long long *dst, int v) {
+    const int t = __reduce_add_sync(VX_FULL_MASK, (unsigned)v);
+    if ((threadIdx.x & 31) == 0 && t) atomicAdd(dst, (unsigned long long)t);
+}
+
 __device__ __forceinline__ void warp_count(unsigned long long *dst, bool pred) {
     const unsigned m = __ballot_sync(VX_FULL_MASK, pred);
     if ((threadIdx.x & 31) == 0 && m) atomicAdd(dst, (unsigned long long)__popc(m));
@@ -132,11 +137,20 @@ __global__ void k_dense_clip(float *__restrict__ cells, const uint32_t *__restri
         if (counts[v] == 0) cells[v] = clip_logodds(__fadd_rn(cells[v], 0.0f));
 }
 
-__global__ void k_scatter(const double *__restrict__ pts, long long npts,
-                          const long long *__restrict__ npts_dev, GridGeom g,
-                          const float *__restrict__ mask_cells, float thr,
-                          uint32_t *__restrict__ counts, int32_t *__restrict__ touched,
-                          DevCounters *__restrict__ ctr, int capacity, const uint8_t *__restrict__ keep) {
+// VX_SCATTER_U points per thread per trip, their loads, mask lookups and
+// count atomics issued back to back: the per-point chain (point load ->
+// mask load -> returning atomic) is latency-bound, and one wave of CTAs with
+// U independent chains per thread beats two waves of single chains
+#ifndef VX_SCATTER_U
+#define VX_SCATTER_U 2
+#endif
+__global__ void __launch_bounds__(256, 4)
+k_scatter(const double *__restrict__ pts, long long npts,
+          const long long *__restrict__ npts_dev, GridGeom g,
+          const float *__restrict__ mask_cells, float thr,
+          uint32_t *__restrict__ counts, int32_t *__restrict__ touched,
+          DevCounters *__restrict__ ctr, int capacity, const uint8_t *__restrict__ keep) {
+    constexpr int U = VX_SCATTER_U;
     const long long n = npts_dev ? *npts_dev : npts;
     // pts == nullptr: npts_dev heads a device block {count, cloud pointer}
     // (the camera tick's staged arguments, so its graph needs no cloud copy)
@@ -147,46 +161,68 @@ __global__ void k_scatter(const double *__restrict__ pts, long long npts,
     __syncthreads();
     const long long nth = (long long)gridDim.x * blockDim.x;
     const long long start = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
     // uniform trip count so the warp-aggregated counters see full warps
-    const long long trips = (n + nth - 1) / nth;
+    const long long trips = (n + nth * U - 1) / (nth * U);
     for (long long it = 0; it < trips; ++it) {
-        const long long p = start + it * nth;
-        bool oob = false, skip = false, ins = false, first = false;
-        long long lin = -1;
-        if (p < n && (!keep || keep[p])) {   // outliers were removed before discretising (grids.py:166-170)
-            const double x = pts[3 * p], y = pts[3 * p + 1], z = pts[3 * p + 2];
-            lin = discretize(x, y, z, g);
-            if (lin < 0) {
-                oob = true;                                          // grids.py:171
-            } else if (mask_cells && mask_cells[lin] > thr) {
-                skip = true;                                         // grids.py:178-182
+        bool oob[U], skip[U], ins[U], first[U];
+        long long lin[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const long long p = start + (it * U + u) * nth;
+            oob[u] = skip[u] = ins[u] = first[u] = false;
+            lin[u] = -2;
+            if (p < n && (!keep || keep[p])) {   // outliers were removed before discretising (grids.py:166-170)
+                const double x = pts[3 * p], y = pts[3 * p + 1], z = pts[3 * p + 2];
+                lin[u] = discretize(x, y, z, g);
+                oob[u] = lin[u] < 0;                                 // grids.py:171
+            }
+        }
+        float mv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            mv[u] = (mask_cells && lin[u] >= 0) ? mask_cells[lin[u]] : 0.0f;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (lin[u] < 0) continue;
+            if (mask_cells && mv[u] > thr) {
+                skip[u] = true;                                      // grids.py:178-182
             } else {
-                ins = true;
-                first = atomicAdd(&counts[lin], 1u) == 0u;          // first touch
+                ins[u] = true;
+                first[u] = atomicAdd(&counts[lin[u]], 1u) == 0u;     // first touch
             }
         }
         // first touches join the touched list with one global atomic per block
         // (a per-warp atomic on the one counter serialised ~10k requests)
-        const unsigned fm = __ballot_sync(VX_FULL_MASK, first);
-        const int lane = threadIdx.x & 31;
-        int wofs = 0;
-        if (lane == 0 && fm) wofs = atomicAdd(&s_cnt, __popc(fm));
-        wofs = __shfl_sync(VX_FULL_MASK, wofs, 0);
+        unsigned fm[U];
+        int wofs[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            fm[u] = __ballot_sync(VX_FULL_MASK, first[u]);
+            wofs[u] = 0;
+            if (lane == 0 && fm[u]) wofs[u] = atomicAdd(&s_cnt, __popc(fm[u]));
+            wofs[u] = __shfl_sync(VX_FULL_MASK, wofs[u], 0);
+        }
         __syncthreads();
         if (threadIdx.x == 0) {
             s_base = s_cnt ? atomicAdd(&ctr->pending, s_cnt) : 0;
             s_cnt = 0;
         }
         __syncthreads();
-        if (first) {
-            const int slot = base + s_base + wofs + __popc(fm & ((1u << lane) - 1u));
-            if (slot < capacity) touched[slot] = (int32_t)lin;
-            else ctr->overflow = 1;
+        int ns = 0, nk = 0, ni = 0;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (first[u]) {
+                const int slot = base + s_base + wofs[u] + __popc(fm[u] & ((1u << lane) - 1u));
+                if (slot < capacity) touched[slot] = (int32_t)lin[u];
+                else ctr->overflow = 1;
+            }
+            ns += oob[u]; nk += skip[u]; ni += ins[u];
         }
         __syncthreads();   // s_base is rewritten next iteration
-        warp_count(&ctr->oob, oob);
-        warp_count(&ctr->skipped, skip);
-        warp_count(&ctr->inserted, ins);
+        warp_sum(&ctr->oob, ns);
+        warp_sum(&ctr->skipped, nk);
+        warp_sum(&ctr->inserted, ni);
     }
 }
 
@@ -399,7 +435,7 @@ cudaError_t launch_scatter(const double *pts, int64_t npts, const int64_t *npts_
                            const float *mask_cells, float thr, uint32_t *counts, int32_t *touched,
                            DevCounters *ctr, int capacity, cudaStream_t st, const uint8_t *keep) {
     if (npts <= 0 && !npts_dev) return cudaSuccess;
-    k_scatter<<<grid_for(npts, 256), 256, 0, st>>>(pts, npts, (const long long *)npts_dev, g,
+    k_scatter<<<grid_for((npts + VX_SCATTER_U - 1) / VX_SCATTER_U, 256), 256, 0, st>>>(pts, npts, (const long long *)npts_dev, g,
                                                    mask_cells, thr, counts, touched, ctr, capacity, keep);
     return cudaGetLastError();
 }
