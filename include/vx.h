@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define VX_ABI_VERSION 1
+#define VX_ABI_VERSION 2
 
 enum {
     VX_OK = 0,
@@ -205,15 +205,27 @@ int vx_cycle_step(vx_cycle *c, const double *pts, int64_t npts, const double *li
 int vx_cycle_step_device(vx_cycle *c, const double *d_pts, int64_t npts, const double *link_T,
                          float hit_logodds, double occupancy_threshold, const double *centers,
                          int s, int sync);
-/* Stage the NEXT tick's cloud (pinned host memory, npts points) on a copy
- * stream while the current tick computes: the next vx_cycle_step called with
- * the same pointer and count reads the staged copy instead of uploading it.
- * Two slots; the host buffer must stay unchanged until that step. */
-int vx_cycle_prefetch(vx_cycle *c, const double *pts, int64_t npts);
+/* Stage a later tick's cloud (pinned host memory, npts points) on a copy
+ * stream while the current tick computes, and return a ticket (> 0) naming
+ * the staged copy.  vx_cycle_step_staged(ticket) runs a tick on exactly that
+ * copy; the host buffer may be rewritten once that tick has completed
+ * (vx_cycle_wait), since the upload itself is asynchronous.  Two
+ * slots: a third prefetch overwrites the oldest unconsumed slot, and a
+ * consumed or overwritten ticket fails with VX_EINVAL (never a stale cloud).
+ * vx_cycle_step never reads a staged copy. */
+int vx_cycle_prefetch(vx_cycle *c, const double *pts, int64_t npts, uint64_t *ticket);
+int vx_cycle_step_staged(vx_cycle *c, uint64_t ticket, const double *link_T, float hit_logodds,
+                         double occupancy_threshold, const double *centers, int s, int sync);
 /* wait for the last step and copy its results (the tick already packed them
  * into host-mapped memory); any output may be NULL */
 int vx_cycle_wait(vx_cycle *c, vx_cycle_result *res, int32_t *site_lin /* 2*s */,
                   double *site_world /* 2*s*3 */, double *dist /* 2*s */);
+/* How the last tick ran (tests and bench evidence), after waiting for it:
+ * info[0] pass-3 kernel choice (0 both launched, the device picks; 1 the
+ * one-warp streaming kernel; 2 the banded kernel), info[1] 1 if it replayed
+ * the CUDA graph, info[2] graph captures so far, info[3] the env map's
+ * occupied i-slice count written by that tick (-1 before the first). */
+int vx_cycle_info(vx_cycle *c, int32_t info[4]);
 /* Per-phase CUDA-event timing of vx_cycle_step (bench evidence).  Phases:
  * 0 H2D, 1 self map (stamp + EDT, only when it changed), 2 mask stamp +
  * env/mask reset, 3 scatter + finalize, 4 EDT pass 1, 5 pass 2, 6 pass 3,

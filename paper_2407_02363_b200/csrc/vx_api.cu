@@ -258,7 +258,10 @@ static int insert_device(vx_grid *g, const double *d_xyz, long long n, const lon
     const float thr32 = (float)logit(thr);  // numpy compares in float32
     // a fresh grid counts hits in its own (zero) cells: finalize then reads one
     // array per touched voxel instead of two and has no counts to clear
-    const bool fresh = g->fresh && !g->maybe_oor;
+    // (not when the grid is its own robot mask: the scatter would read the
+    // partly incremented counts as mask cells, grids.py:178-182 reads the
+    // pre-insert cells)
+    const bool fresh = g->fresh && !g->maybe_oor && mask != g;
     uint32_t *counts = fresh ? reinterpret_cast<uint32_t *>(g->cells) : g->counts;
     g->fresh = false;
     cudaError_t e = launch_scatter(d_xyz, n, (const int64_t *)n_dev, g->g, mask ? mask->cells : nullptr,
@@ -899,14 +902,16 @@ struct vx_cycle {
     // device) -> which pass-3 kernels the next tick launches
     int *h_m = nullptr, *d_m = nullptr;
     int p3_mode = 0, g_mode = -1;
+    int captures = 0, last_graph = 0;   // vx_cycle_info
     unsigned char *h_out = nullptr, *d_out = nullptr;   // packed results (host-mapped)
     // vx_cycle_prefetch: the next cloud is uploaded on a copy stream into one
     // of two device slots while the current tick computes
     cudaStream_t cst = nullptr;
     double *d_pb[2] = {nullptr, nullptr};
     cudaEvent_t ev_up[2] = {nullptr, nullptr}, ev_used[2] = {nullptr, nullptr};
-    const double *pf_host[2] = {nullptr, nullptr};
+    unsigned long long pf_ticket[2] = {0, 0};   // 0 = slot empty or consumed
     long long pf_n[2] = {-1, -1};
+    unsigned long long pf_issued = 0;
     int pf_next = 0;
     cudaGraphExec_t gexec = nullptr;
     cudaGraph_t graph = nullptr;   // kept while gexec lives (its reset node is updated per tick)
@@ -1234,9 +1239,20 @@ static int cycle_main_seq(vx_cycle *cy, const double *d_pts, long long npts, con
 }
 
 static int cycle_step(vx_cycle *cy, const double *pts, const double *d_pts_in, int64_t npts,
-                      const double *link_T, float hit, double thr, const double *centers, int s, int sync) {
+                      const double *link_T, float hit, double thr, const double *centers, int s, int sync,
+                      unsigned long long ticket = 0) {
+    // a cloud staged by vx_cycle_prefetch: the tick reads that device slot
+    int pf_slot = -1;
+    if (cy && ticket) {
+        for (int b = 0; b < 2; ++b)
+            if (cy->pf_ticket[b] == ticket) pf_slot = b;
+        if (pf_slot < 0)
+            return fail(VX_EINVAL, "prefetch ticket %llu is not staged (already consumed or overwritten)",
+                        ticket);
+        npts = cy->pf_n[pf_slot];
+    }
     if (!cy || npts < 0 || npts > cy->max_points || s < 0 || s > cy->max_spheres ||
-        (npts && !pts && !d_pts_in) || (s && !centers) || (cy->nlinks && !link_T))
+        (npts && !pts && !d_pts_in && pf_slot < 0) || (s && !centers) || (cy->nlinks && !link_T))
         return fail(VX_EINVAL, "bad argument (npts %lld of max %lld, spheres %d of max %d)",
                     (long long)npts, (long long)cy->max_points, s, cy->max_spheres);
     vx_ctx *c = cy->ctx;
@@ -1247,15 +1263,10 @@ static int cycle_step(vx_cycle *cy, const double *pts, const double *d_pts_in, i
         cy->ring_used = cy->ring_n + 1;
     }
     cy->mark(0);
-    // a cloud staged by vx_cycle_prefetch: the tick reads that device slot
-    int pf_slot = -1;
-    if (npts && pts && !d_pts_in)
-        for (int b = 0; b < 2; ++b)
-            if (cy->pf_host[b] == pts && cy->pf_n[b] == npts) pf_slot = b;
     if (pf_slot >= 0) {
         VX_CUDA(cudaStreamWaitEvent(st, cy->ev_up[pf_slot], 0));
         d_pts_in = cy->d_pb[pf_slot];
-        cy->pf_host[pf_slot] = nullptr;   // consumed
+        cy->pf_ticket[pf_slot] = 0;   // consumed
         cy->pf_n[pf_slot] = -1;
     }
     // H2D: the cloud (unless staged by prefetch or already on the device),
@@ -1306,6 +1317,9 @@ static int cycle_step(vx_cycle *cy, const double *pts, const double *d_pts_in, i
     if (graph_path) {
         // the graph reads the cloud pointer and its size from the staged block
         cy->p3_mode = pass3_mode_hint(cy->plan, *(volatile int *)cy->h_m);
+        // reset modes from the grids' state before this tick (a capture below
+        // runs cycle_main_seq, which already marks the grids as reset)
+        const int dense_mask = cy->mask->sparse_ok ? 0 : 1, dense_env = cy->env->sparse_ok ? 0 : 1;
         if (!cy->gexec || cy->g_s != s || cy->g_hit != hit || cy->g_thr != thr || cy->g_mode != cy->p3_mode) {
             drop_graph(cy);
             const long long l0 = c->launches;
@@ -1326,6 +1340,7 @@ static int cycle_step(vx_cycle *cy, const double *pts, const double *d_pts_in, i
                 drop_graph(cy);
                 return cuda_fail(ce, "cudaGraphInstantiate");
             }
+            cy->captures += 1;
             cy->g_kernels = c->launches - l0;
             c->launches = l0;
             cy->g_s = s;
@@ -1333,7 +1348,13 @@ static int cycle_step(vx_cycle *cy, const double *pts, const double *d_pts_in, i
             cy->g_hit = hit;
             cy->g_thr = thr;
         }
-        {   // this tick's staging slot -> the reset node's copy source
+        {   // this tick's staging slot -> the reset node's copy source.  The
+            // reset mode follows the grids' current state: host writes since
+            // the last tick (vx_grid_write_cells on cycle grids) leave cells
+            // outside the touched list, so that tick's reset must be dense (it
+            // also makes the captured fresh-grid insert valid again).
+            cy->g_ra.dense = dense_mask;
+            cy->g_rb.dense = dense_env;
             CopySpan cp = cy->g_cp;
             cp.src = cy->d_hstage[stage_b];
             void *args[] = {&cy->g_ra, &cy->g_rb, &cy->g_z[0], &cy->g_z[1], &cy->g_z[2], &cp};
@@ -1343,6 +1364,11 @@ static int cycle_step(vx_cycle *cy, const double *pts, const double *d_pts_in, i
             VX_CUDA(cudaGraphExecKernelNodeSetParams(cy->gexec, cy->g_reset, &kp));
         }
         VX_CUDA(cudaGraphLaunch(cy->gexec, st));
+        for (vx_grid *g : {cy->mask, cy->env}) {   // host state after the replayed tick (as cycle_main_seq)
+            g->sparse_ok = true;
+            g->maybe_oor = false;
+            g->fresh = false;
+        }
         VX_CUDA(cudaEventRecord(cy->ev_stage[stage_b], st));   // the graph read the slot
         c->launches += cy->g_kernels;
         if (pf_slot >= 0) VX_CUDA(cudaEventRecord(cy->ev_used[pf_slot], st));   // the tick read the slot
@@ -1353,6 +1379,7 @@ static int cycle_step(vx_cycle *cy, const double *pts, const double *d_pts_in, i
     }
     if (cy->profiling && cy->ring_n < vx_cycle::kRing) cy->ring_n++;
     cy->last_s = s;
+    cy->last_graph = graph_path ? 1 : 0;
     if (sync) VX_CUDA(cudaStreamSynchronize(st));
     return VX_OK;
 }
@@ -1367,22 +1394,30 @@ extern "C" int vx_cycle_step_device(vx_cycle *cy, const double *d_pts, int64_t n
     return cycle_step(cy, nullptr, d_pts, npts, link_T, hit, thr, centers, s, sync);
 }
 
-// Stage the next tick's cloud (pinned host memory) on a copy stream while the
-// current tick computes; the next vx_cycle_step with the same pointer and
-// count reads the staged copy.  The host buffer must not change until then.
-extern "C" int vx_cycle_prefetch(vx_cycle *cy, const double *pts, int64_t npts) {
-    if (!cy || npts < 0 || npts > cy->max_points || (npts && !pts))
+// Stage a later tick's cloud (pinned host memory) on a copy stream while the
+// current tick computes.  The upload is asynchronous: the host buffer must
+// stay unchanged until the tick that consumes the ticket (vx_cycle_step_staged)
+// has completed.  Two slots: a third prefetch
+// overwrites the oldest unconsumed one, whose ticket then fails loudly.
+extern "C" int vx_cycle_prefetch(vx_cycle *cy, const double *pts, int64_t npts, uint64_t *ticket) {
+    if (!cy || !ticket || npts < 0 || npts > cy->max_points || (npts && !pts))
         return fail(VX_EINVAL, "bad argument (npts %lld of max %lld)", (long long)npts,
                     (long long)(cy ? cy->max_points : 0));
-    if (!npts) return VX_OK;
     const int b = cy->pf_next;
     cy->pf_next ^= 1;
     VX_CUDA(cudaStreamWaitEvent(cy->cst, cy->ev_used[b], 0));   // the tick that read slot b is past it
-    VX_CUDA(cudaMemcpyAsync(cy->d_pb[b], pts, (size_t)npts * 24, cudaMemcpyHostToDevice, cy->cst));
+    if (npts) VX_CUDA(cudaMemcpyAsync(cy->d_pb[b], pts, (size_t)npts * 24, cudaMemcpyHostToDevice, cy->cst));
     VX_CUDA(cudaEventRecord(cy->ev_up[b], cy->cst));
-    cy->pf_host[b] = pts;
+    cy->pf_ticket[b] = ++cy->pf_issued;
     cy->pf_n[b] = npts;
+    *ticket = cy->pf_ticket[b];
     return VX_OK;
+}
+
+extern "C" int vx_cycle_step_staged(vx_cycle *cy, uint64_t ticket, const double *link_T, float hit, double thr,
+                                    const double *centers, int s, int sync) {
+    if (!ticket) return fail(VX_EINVAL, "ticket 0 is never issued");
+    return cycle_step(cy, nullptr, nullptr, 0, link_T, hit, thr, centers, s, sync, ticket);
 }
 
 extern "C" int vx_cycle_use_graph(vx_cycle *cy, int enable) {
@@ -1513,6 +1548,16 @@ extern "C" int vx_cycle_rows(vx_cycle *cy, double *J, double *act, double *ref, 
     if (val) VX_CUDA(cudaMemcpyAsync(val, cy->d_val, r * 8, cudaMemcpyDeviceToHost, st));
     if (flag) VX_CUDA(cudaMemcpyAsync(flag, cy->d_flag, r * 4, cudaMemcpyDeviceToHost, st));
     VX_CUDA(cudaStreamSynchronize(st));
+    return VX_OK;
+}
+
+extern "C" int vx_cycle_info(vx_cycle *cy, int32_t info[4]) {
+    if (!cy || !info) return fail(VX_EINVAL, "NULL argument");
+    VX_CUDA(cudaStreamSynchronize(cy->ctx->stream));
+    info[0] = cy->p3_mode;
+    info[1] = cy->last_graph;
+    info[2] = cy->captures;
+    info[3] = *(volatile int *)cy->h_m;
     return VX_OK;
 }
 

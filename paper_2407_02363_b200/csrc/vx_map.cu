@@ -367,17 +367,24 @@ __global__ void k_stamp(const int32_t *__restrict__ ijk, const long long *__rest
             atomicAdd(&oob_per_set[s], 1ull);
             continue;
         }
-        cells[lin] = value;                                           // grids.py:202
+        // grids.py:202.  Only a voxel whose cell was +0.0f joins the touched
+        // list: any other value is already on it (a grid whose list is
+        // incomplete resets densely anyway), so repeated stamps of one voxel
+        // (several link voxels per cell, links overlapping) append it once.
+        const float old = atomicExch(&cells[lin], value);
         occ[lin] = value > occ_thr ? 1 : 0;
         // one touched-list atomic per warp (lanes that took `continue` are inactive)
         const unsigned am = __activemask();
+        const unsigned fm = __ballot_sync(am, __float_as_uint(old) == 0u);
         const int lane = threadIdx.x & 31, leader = __ffs(am) - 1;
         int wbase = 0;
-        if (lane == leader) wbase = atomicAdd(&ctr->touched, __popc(am));
+        if (lane == leader && fm) wbase = atomicAdd(&ctr->touched, __popc(fm));
         wbase = __shfl_sync(am, wbase, leader);
-        const int slot = wbase + __popc(am & ((1u << lane) - 1u));
-        if (slot < capacity) touched[slot] = (int32_t)lin;
-        else ctr->overflow = 1;
+        if (fm & (1u << lane)) {
+            const int slot = wbase + __popc(fm & ((1u << lane) - 1u));
+            if (slot < capacity) touched[slot] = (int32_t)lin;
+            else ctr->overflow = 1;
+        }
     }
     if (last_block(ctr)) {   // commit
         if (ctr->touched > capacity) ctr->touched = capacity;

@@ -45,6 +45,15 @@ def site_world(field: DistanceField, origin, voxel_size: float, centers):
     return lin, world, dist
 
 
+class StagedCloud:
+    """Ticket of a cloud staged on the device by MapCycle.prefetch."""
+
+    __slots__ = ("cycle", "ticket", "array")
+
+    def __init__(self, cycle, ticket: int, array):
+        self.cycle, self.ticket, self.array = cycle, ticket, array
+
+
 class MapCycle:
     """Device-resident camera tick (engine.py:233-280) for one robot.
 
@@ -92,26 +101,40 @@ class MapCycle:
     def step(self, points, link_frames, centers, hit_logodds: float = 0.85,
              occupancy_threshold: float = 0.5, sync: bool = True):
         """Run one tick.  points: (P,3) float64 world points (pinned for an
-        async copy), link_frames: (nlinks,4,4) FK frames, centers: (S,3)."""
-        pts = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 3)
+        async copy) or a StagedCloud from prefetch(); link_frames:
+        (nlinks,4,4) FK frames, centers: (S,3)."""
         T = np.ascontiguousarray(link_frames, dtype=np.float64).reshape(-1, 16)
         c = np.ascontiguousarray(centers, dtype=np.float64).reshape(-1, 3)
         self._s = c.shape[0]
-        _lib.check(_lib.load().vx_cycle_step(self._h, _lib.ptr(pts), pts.shape[0], _lib.ptr(T),
-                                             float(np.float32(hit_logodds)),
-                                             float(occupancy_threshold), _lib.ptr(c), c.shape[0],
-                                             1 if sync else 0))
+        if isinstance(points, StagedCloud):
+            if points.cycle is not self:
+                raise ValueError("StagedCloud belongs to another MapCycle")
+            _lib.check(_lib.load().vx_cycle_step_staged(
+                self._h, points.ticket, _lib.ptr(T), float(np.float32(hit_logodds)),
+                float(occupancy_threshold), _lib.ptr(c), c.shape[0], 1 if sync else 0))
+            pts = points.array
+        else:
+            pts = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 3)
+            _lib.check(_lib.load().vx_cycle_step(self._h, _lib.ptr(pts), pts.shape[0], _lib.ptr(T),
+                                                 float(np.float32(hit_logodds)),
+                                                 float(occupancy_threshold), _lib.ptr(c),
+                                                 c.shape[0], 1 if sync else 0))
         self._keep = (pts, T, c)   # host buffers must outlive an async copy
         return self
 
-    def prefetch(self, points):
-        """Upload the NEXT tick's cloud while the current one computes
-        (vx_cycle_prefetch).  points must be the pinned array later passed to
-        step() unchanged; it is kept alive here until then."""
+    def prefetch(self, points) -> "StagedCloud":
+        """Upload a later tick's cloud while the current one computes
+        (vx_cycle_prefetch) and return its ticket; pass the ticket to step()
+        in place of the points.  The upload is asynchronous: leave the
+        (pinned) array unchanged until that tick has been waited for.  Two
+        slots -- a third prefetch invalidates the oldest unconsumed ticket,
+        and stepping with a consumed or invalidated ticket raises."""
         pts = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 3)
-        _lib.check(_lib.load().vx_cycle_prefetch(self._h, _lib.ptr(pts), pts.shape[0]))
-        self._pf = getattr(self, "_pf", [])[-1:] + [pts]
-        return self
+        t = ctypes.c_uint64()
+        _lib.check(_lib.load().vx_cycle_prefetch(self._h, _lib.ptr(pts), pts.shape[0],
+                                                 ctypes.byref(t)))
+        self._pf = getattr(self, "_pf", [])[-1:] + [pts]   # alive until the upload ran
+        return StagedCloud(self, int(t.value), pts)
 
     def wait(self):
         """Results of the last step: dict with stats and per-map (lin, world, dist)."""
@@ -126,6 +149,13 @@ class MapCycle:
         return {"inserted": st.inserted, "robot_skipped": st.robot_skipped,
                 "out_of_bounds": st.out_of_bounds, "self_recomputed": bool(res.self_recomputed),
                 "env": (lin[0], world[0], dist[0]), "self": (lin[1], world[1], dist[1])}
+
+    def info(self) -> dict:
+        """How the last tick ran (vx_cycle_info)."""
+        a = np.zeros(4, np.int32)
+        _lib.check(_lib.load().vx_cycle_info(self._h, _lib.ptr(a)))
+        return {"pass3_mode": int(a[0]), "graph": bool(a[1]), "captures": int(a[2]),
+                "occupied_slices": int(a[3])}
 
     def set_avoidance(self, radius, buffer, link_index, n_joints: int, kappa: float,
                       x_star_offset=None):
@@ -181,4 +211,4 @@ class MapCycle:
         return mk(e), mk(s), mk(m)
 
 
-__all__ = ["site_world", "MapCycle", "L_MAX"]
+__all__ = ["site_world", "MapCycle", "StagedCloud", "L_MAX"]

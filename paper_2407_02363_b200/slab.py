@@ -121,7 +121,8 @@ class SlabEDT:
         nx, ny, nz = self.dims
         maxl = max(self.j_starts[q + 1] - self.j_starts[q] for q in range(self.world))
         buf = symm_mem.empty(nx * maxl * nz, dtype=torch.int32, device=self.device)
-        hdl = symm_mem.rendezvous(buf, self.group)
+        import torch.distributed as dist
+        hdl = symm_mem.rendezvous(buf, self.group if self.group is not None else dist.group.WORLD)
         self._symm = (buf, hdl)
         self.recv = buf[: nx * self.nyl * nz].view(nx, self.nyl, nz)
         self.peer_ptrs = []
@@ -146,6 +147,13 @@ class SlabEDT:
             raise ValueError(f"rank {self.rank} expects a slab of shape "
                              f"{(self.nxl, self.dims[1], self.dims[2])}")
         ptrs, x_base = self.destinations()
+        if self.exchange == "p2p":
+            # every peer is done reading its receive buffer (the previous
+            # call's pass 3) before anyone's pass-2 epilogue writes into it;
+            # the barrier kernel runs on the library stream, so it is ordered
+            # after this rank's pass 3 and before its pass 2
+            with torch.cuda.stream(self.backend.stream()):
+                self._symm[1].barrier()
         self.backend.pass12_scatter(occ_slab, self.dims, ptrs, self.j_starts, x_base)
         if self.exchange == "nccl":
             self.backend.synchronize()
@@ -156,8 +164,11 @@ class SlabEDT:
                 self.recv.view(-1).copy_(self.send)
             self.backend.synchronize()
         else:
-            self.backend.synchronize()
-            self._symm[1].barrier()
+            # the peers' NVLink stores into this rank's buffer have landed
+            # once every rank's pass 2 is past this barrier; pass 3 is queued
+            # behind it on the same (library) stream
+            with torch.cuda.stream(self.backend.stream()):
+                self._symm[1].barrier()
         self.backend.pass3(self.recv, self.site, self.dims, self.j_starts[self.rank])
         self.backend.synchronize()
         return self.site

@@ -95,6 +95,26 @@ def oscillating_sphere_cloud(t: float, *, obstacle_id: int, radius: float, point
     return base + pos
 
 
+_DESK7 = {}
+
+
+def desk7_model() -> dict:
+    """The desk7 robot at 2 cm as the host-side producers make it
+    (robot.voxelize_link / forward_kinematics / build_spheres, robot.py:467-
+    620): link voxel sets ("links": [(ijk int32 (K,3), origin (3,))]), the
+    self-obstacle links "o_links", a trajectory of FK "frames" and the
+    sphere table.  Generated once by the reference (tests/golden/make_golden.py)
+    and shipped as package data: this repo does not rebuild the robot model."""
+    if not _DESK7:
+        import os
+        z = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "data", "desk7_2cm.npz"))
+        d = {k: z[k] for k in z.files}
+        n = d["frames"].shape[1]
+        d["links"] = [(d[f"link{li}_ijk"], d[f"link{li}_origin"]) for li in range(n)]
+        _DESK7.update(d)
+    return _DESK7
+
+
 # config C1 (SURVEY.md 8(d)): 128^3 @ 2 cm, desk7 at GUARD_Q, 50k-point sphere
 C1 = {"dims": (128, 128, 128), "voxel_size": 0.02, "origin": (-1.28, -1.28, -0.24),
       "points": 50_000, "seed": 0, "obstacle_radius": 0.15,

@@ -12,7 +12,8 @@ Outputs
   edt_cases.npz   small random grids: occupancy, pba_edt site, pass-1 s1
   golden.json     blake2b digests of reference outputs at larger sizes,
                   map-insert / stamp / site-world cases, the C1 cycle
-  desk7_2cm.npz   desk7 link voxel sets (robot.voxelize_link), sphere
+  ../../paper_2407_02363_b200/data/desk7_2cm.npz
+                  desk7 link voxel sets (robot.voxelize_link), sphere
                   link/centre table (build_spheres), FK frames for a q list
 """
 
@@ -147,7 +148,8 @@ def desk7():
     for li, vs in enumerate(links):
         arrays[f"link{li}_ijk"] = vs.indices
         arrays[f"link{li}_origin"] = vs.origin
-    np.savez_compressed(os.path.join(HERE, "desk7_2cm.npz"), **arrays)
+    np.savez_compressed(os.path.join(HERE, "..", "..", "paper_2407_02363_b200", "data", "desk7_2cm.npz"),
+                        **arrays)
     return chain, links
 
 
@@ -244,7 +246,36 @@ def edt_digests_1024():
     return out
 
 
+def bench512_tick0():
+    """bench.py's headline tick 0 (512^3, 300k-point depth camera, desk7 mask
+    at the step's frames) through voxarm's own grids and pba_edt."""
+    import bench
+    d = synth.desk7_model()
+    pts, frames, centers = bench.scene_inputs(0, 0, d)
+    dims, vs, origin = bench.DIMS, bench.VS, bench.ORIGIN
+    mask = VoxelGrid(dims, vs, origin)
+    for li, (ijk, org) in enumerate(d["links"]):
+        mask.insert_voxel_set(VoxelSet(np.asarray(org, np.float64), vs, ijk), frames[li])
+    env = VoxelGrid(dims, vs, origin)
+    st = env.insert_point_cloud(PointCloud(pts), FilterConfig(k_neighbors=0), robot_mask=mask)
+    occ = env.occupancy_mask()
+    fe = pba_edt(occ, voxel_size=vs)
+    eng = _FakeEngine(fe, origin, vs, dims)
+    return {"stats": [st.inserted, st.robot_skipped, st.out_of_bounds], "occ": digest(occ),
+            "site": digest(fe.site), "cloud": digest(pts),
+            "env_world": [None if w is None else [float(v) for v in w]
+                          for w in (SimEngine._site_world(eng, "env", c) for c in centers)]}
+
+
 def main():
+    if "--bench512" in sys.argv:   # only the headline digest, merged into golden.json
+        path = os.path.join(HERE, "golden.json")
+        with open(path) as fh:
+            gold = json.load(fh)
+        gold["bench512_tick0"] = bench512_tick0()
+        with open(path, "w") as fh:
+            json.dump(gold, fh, indent=1)
+        return
     if "--big" in sys.argv:   # only the 1024^3 digests, merged into golden.json
         path = os.path.join(HERE, "golden.json")
         with open(path) as fh:
@@ -267,6 +298,8 @@ def main():
             prev = json.load(fh)
         if "edt_digests_1024" in prev:
             gold["edt_digests_1024"] = prev["edt_digests_1024"]
+        if "bench512_tick0" in prev:
+            gold["bench512_tick0"] = prev["bench512_tick0"]
     with open(os.path.join(HERE, "golden.json"), "w") as fh:
         json.dump(gold, fh, indent=1)
     print("wrote", HERE)

@@ -28,7 +28,7 @@ def test_library_loads_and_exports_every_symbol():
     L = _lib.load()
     for name in _declared():
         assert hasattr(L, name), name
-    assert L.vx_abi_version() == 1
+    assert L.vx_abi_version() == 2
 
 
 def test_library_is_sm100a_code():

@@ -108,6 +108,50 @@ def test_graph_and_direct_launch_agree():
     assert outs[0] == outs[1]
 
 
+@pytest.mark.parametrize("which", ["env", "mask"])
+def test_graph_tick_after_host_cell_writes(which):
+    """Host writes to a cycle grid between ticks (MapCycle.grids() hands out
+    writable grids) leave cells off the touched list and possibly out of
+    range: the next replayed graph tick must reset that grid densely, exactly
+    as the direct-launch tick does (the captured reset mode)."""
+    from paper_2407_02363_b200 import _lib
+    d = desk7()
+    s = synth.C1
+    rng = np.random.default_rng(5)
+    junk = rng.uniform(-4.0, 6.0, s["dims"]).astype(np.float32)   # includes out-of-range values
+    junk[rng.random(s["dims"]) < 0.5] = -0.0
+    outs = []
+    for graph in (1, 0):
+        cyc, _ = _c1_cycle()
+        _lib.check(_lib.load().vx_cycle_use_graph(cyc._h, graph))
+        res = []
+        for step in range(4):
+            frames = d["frames"][step]
+            centers = synth.sphere_centers(frames, d["sphere_link"], d["sphere_center"])
+            if step in (1, 3):   # after the graph exists: scribble on the grid
+                env, _, mask = cyc.grids()
+                (env if which == "env" else mask).cells = junk
+            cyc.step(synth.c1_cloud(step / 30.0), frames, centers)
+            r = cyc.wait()
+            env, _, mask = cyc.grids()
+            fe, _ = cyc.fields()
+            res.append((r["inserted"], r["robot_skipped"], digest(env.cells), digest(mask.cells),
+                        digest(fe.site), r["env"][2].tolist()))
+        outs.append(res)
+        cyc.close()
+    assert outs[0] == outs[1]
+    # and the tick after a write equals a tick on a never-written cycle
+    ref, _ = _c1_cycle()
+    frames = d["frames"][3]
+    ref.step(synth.c1_cloud(3 / 30.0), frames,
+             synth.sphere_centers(frames, d["sphere_link"], d["sphere_center"]))
+    r = ref.wait()
+    env, _, mask = ref.grids()
+    fe, _ = ref.fields()
+    assert outs[0][3][:5] == (r["inserted"], r["robot_skipped"], digest(env.cells),
+                              digest(mask.cells), digest(fe.site))
+
+
 def test_prefetch_matches_plain_step():
     """vx_cycle_prefetch: the staged cloud gives the same tick as a plain step
     (and a stale / mismatched prefetch is ignored, not used)."""
@@ -129,20 +173,34 @@ def test_prefetch_matches_plain_step():
         fe, _ = ref.fields()
         want.append((r["inserted"], digest(fe.site), r["env"][2].copy()))
     cyc, _ = _c1_cycle()
-    cyc.prefetch(clouds[0].array)
+    tk = cyc.prefetch(clouds[0].array)
     for q, pa in enumerate(clouds):
-        cyc.step(pa.array, frames, centers, sync=False)
+        cyc.step(tk, frames, centers, sync=False)
         if q + 1 < len(clouds):
-            cyc.prefetch(clouds[q + 1].array)
+            tk = cyc.prefetch(clouds[q + 1].array)
         r = cyc.wait()
         fe, _ = cyc.fields()
         assert (r["inserted"], digest(fe.site)) == want[q][:2], q
         assert np.array_equal(r["env"][2], want[q][2])
-    # a prefetch of a different buffer does not leak into a step
+    # a staged cloud never leaks into a plain step of another buffer
     cyc.prefetch(clouds[2].array)
     cyc.step(clouds[0].array, frames, centers)
     r = cyc.wait()
     assert r["inserted"] == want[0][0]
+    # a consumed ticket and an overwritten one fail loudly, never a stale cloud
+    used = cyc.prefetch(clouds[1].array)
+    cyc.step(used, frames, centers)
+    cyc.wait()
+    with pytest.raises(ValueError):
+        cyc.step(used, frames, centers)
+    old = cyc.prefetch(clouds[0].array)
+    cyc.prefetch(clouds[1].array)
+    cyc.prefetch(clouds[2].array)   # third prefetch: overwrites `old`'s slot
+    with pytest.raises(ValueError):
+        cyc.step(old, frames, centers)
+    tk = cyc.prefetch(clouds[1].array)   # a fresh ticket after the failures still works
+    cyc.step(tk, frames, centers)
+    assert cyc.wait()["inserted"] == want[1][0]
 
 
 @pytest.mark.parametrize("dims", [(96, 80, 72), (130, 64, 36), (64, 128, 30)],

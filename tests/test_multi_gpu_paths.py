@@ -78,3 +78,39 @@ def test_c5_1024_single_gpu_and_slab_vs_reference(rec):
     torch.cuda.empty_cache()
     got = emulate_ranks(d_occ, 8, "p2p").cpu().numpy()
     assert digest(got) == rec["site"]
+
+
+_P2P_SCRIPT = r"""
+import os, sys
+import numpy as np, torch, torch.distributed as dist
+sys.path.insert(0, os.environ["VX_ROOT"])
+from oracle import oracle as O
+from paper_2407_02363_b200 import synth
+from paper_2407_02363_b200.slab import SlabEDT
+torch.cuda.set_device(0)
+dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+for exchange in ("p2p", "nccl"):
+    for dims, p, seed in [((64, 48, 40), 0.03, 4), ((33, 20, 16), 0.2, 5)]:
+        slab = SlabEDT(dims, exchange=exchange)
+        for rep in range(3):   # repeated calls reuse the receive buffer
+            occ = synth.bernoulli_occupancy(dims, p, seed + rep)
+            site = slab(torch.from_numpy(occ).cuda()).cpu().numpy()
+            assert np.array_equal(site, O.pba_edt_site(occ)), (exchange, dims, rep)
+dist.destroy_process_group()
+print("P2P-WORLD1-OK")
+"""
+
+
+def test_slab_p2p_symmetric_memory_world1():
+    """SlabEDT(exchange="p2p") for real: a one-rank NCCL group sets up the
+    torch symmetric-memory receive buffer (rendezvous, peer pointer table),
+    and the pass-2 epilogue stores through the mapped peer pointer; the
+    barriers run on the library stream.  Repeated calls, vs the oracle."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, VX_ROOT=root, MASTER_ADDR="127.0.0.1", MASTER_PORT="29517")
+    r = subprocess.run([sys.executable, "-c", _P2P_SCRIPT], env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0 and "P2P-WORLD1-OK" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]

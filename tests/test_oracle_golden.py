@@ -167,3 +167,26 @@ def test_c1_cycle_vs_reference():
             assert (lin[q] == -1) if w is None else (world[q].tolist() == w)
     site = O.pba_edt_site(selfc > 0)
     assert digest(site) == g["self_site"]
+
+
+def test_bench512_tick0_vs_reference():
+    """The headline workload (bench.py tick 0 at 512^3) through the oracle
+    equals voxarm's own grids + pba_edt + _site_world on it."""
+    import bench
+    g = golden()["bench512_tick0"]
+    d = desk7()
+    pts, frames, centers = bench.scene_inputs(0, 0, d)
+    assert digest(pts) == g["cloud"]
+    mask = np.zeros(bench.DIMS, np.float32)
+    for li, (ijk, org) in enumerate(d["links"]):
+        O.stamp_voxels(mask, bench.VS, bench.ORIGIN, ijk, org, bench.VS, frames[li])
+    env = np.zeros(bench.DIMS, np.float32)
+    st = O.insert_points(env, bench.VS, bench.ORIGIN, pts, mask)
+    assert list(st) == g["stats"]
+    occ = env > 0
+    assert digest(occ) == g["occ"]
+    site = O.pba_edt_site(occ)
+    assert digest(site) == g["site"]
+    lin, world, _ = O.site_world(site, bench.VS, bench.ORIGIN, centers)
+    for q, w in enumerate(g["env_world"]):
+        assert (lin[q] == -1) if w is None else (world[q].tolist() == w)
