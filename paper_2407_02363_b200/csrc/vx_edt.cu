@@ -302,6 +302,16 @@ struct ColParams {
     const int *xs;         // occupied slice indices, ascending
     const int *hdr;        // hdr[0] = number of occupied slices (device-side)
     int stream_max;        // pass 3: k_pass3_stream takes m <= stream_max (-1: never)
+    // windowed search (k_column_ring) for dense scenes; the banded kernel then
+    // only takes the other scenes' tiles and the tiles the search gave up on
+    const int *mcount;     // per-scene occupied-slice counts (nullptr: treat every scene as dense)
+    const uint8_t *sflag3; // pass 3: per (scene, slice) flags (rows of empty slices hold no codes)
+    int ring_min;          // scenes with >= ring_min occupied slices take the windowed search
+    int *fails;            // [0] count, [1] spare, [2..] tiles handed back to the banded kernel
+    int rb;                // row bits of the search keys (w << rb | row)
+    int ring_cap;          // largest search radius before a tile is handed back
+    int ring_budget;       // mean window steps per 4-row block above which a tile is handed back
+    uint32_t kinv;         // key of a row without a candidate (stays above every reachable key)
 };
 
 template <int PASS, bool S2W, bool EW, int FW>
@@ -423,6 +433,11 @@ __device__ __forceinline__ bool better(int ys, FT Fs, int yp, FT Fp, int y) {
 // ---- TMA helpers (tile staging) ---------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ uint32_t lds_u32(int addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+    return v;
 }
 __device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
@@ -795,36 +810,16 @@ __global__ void __launch_bounds__(kColThreads, kColMinBlocks) k_column_smem(cons
 // TMA-staged variant (narrow 32-bit codes, nz % 4 == 0): one elected thread
 // issues the bulk tensor loads of the whole 32-column tile into the stack
 // region; every row of the column is in flight at once.
-template <int PASS, int FW, bool SCAT, bool CMP, int MAXT, int TW = 32>
-__global__ void __launch_bounds__(MAXT, MAXT >= 1024 ? 1 : kColMinBlocks) k_column_tma(const __grid_constant__ CUtensorMap tmap,
-                                                     const __grid_constant__ CUtensorMap tmap1,
-                                                     const typename Col<PASS, false, false, FW>::InT *__restrict__ in,
-                                                     typename Col<PASS, false, false, FW>::OutT *__restrict__ out,
-                                                     const ColParams P, const __grid_constant__ ScatterTab sc) {
-    extern __shared__ __align__(128) unsigned char smem[];
+template <int PASS, int FW, bool SCAT, bool CMP, int TW>
+__device__ __forceinline__ void col_tma_run(const CUtensorMap *tmap, const CUtensorMap *tmap1,
+                                            const typename Col<PASS, false, false, FW>::InT *__restrict__ in,
+                                            typename Col<PASS, false, false, FW>::OutT *__restrict__ out,
+                                            const ColParams &P, const ScatterTab *sc, unsigned char *smem,
+                                            long long tile, long long outer, int kt) {
     using EntT = typename Col<PASS, false, false, FW>::EntT;
     EntT *stk = reinterpret_cast<EntT *>(smem);
     int *meta = reinterpret_cast<int *>(smem + (size_t)P.rows_alloc * TW * sizeof(EntT));
     uint64_t *bar = reinterpret_cast<uint64_t *>(meta + 3 * P.B * TW + TW);
-    long long tile = blockIdx.x;
-    if constexpr (PASS == 2) {   // surplus CTAs leave before any index math
-        if (P.xs && (long long)blockIdx.x >= (long long)__ldg(P.hdr) * P.nkt) return;
-    }
-    const int kt = (int)(tile % P.nkt);
-    long long outer = tile / P.nkt;
-    if constexpr (PASS == 2) {
-        if (P.xs) {   // occupied-slice list: CTA rows map to occupied slices, the
-                      // surplus CTAs (empty slices) all sit at the end of the grid
-            const int m = __ldg(P.hdr);
-            // VX_P2_REVERSE: last occupied slice first -- pass 1 wrote the
-            // slices in ascending order, so the newest s1 lines, still in L2,
-            // are read first
-            outer = __ldg(P.xs + (VX_P2_REVERSE ? m - 1 - outer : outer));
-            tile = outer * P.nkt + kt;
-        } else if (P.sflag && !P.sflag[outer]) {
-            return;   // empty slice: pass 3 never reads it
-        }
-    }
     VX_PT(0);
     bool all_rows = true;
     if constexpr (CMP) {
@@ -850,7 +845,7 @@ __global__ void __launch_bounds__(MAXT, MAXT >= 1024 ? 1 : kColMinBlocks) k_colu
             const int tid = threadIdx.y * TW + threadIdx.x, nth = blockDim.x * blockDim.y;
             if constexpr (TW == 32) {
                 for (int t = tid; t < m; t += nth)
-                    tma_load_4d(stk + (size_t)t * TW, &tmap1, bar, kt * TW, jl, __ldg(xsl + t), scene);
+                    tma_load_4d(stk + (size_t)t * TW, tmap1, bar, kt * TW, jl, __ldg(xsl + t), scene);
             } else {
                 const EntT *row0 = reinterpret_cast<const EntT *>(in) + (long long)scene * P.nvox +
                                    (long long)jl * P.nz + kt * TW;
@@ -868,25 +863,272 @@ __global__ void __launch_bounds__(MAXT, MAXT >= 1024 ? 1 : kColMinBlocks) k_colu
                 void *dst = stk + (size_t)q * P.boxh * TW;
                 if constexpr (PASS == 2) {
                     if constexpr (VX_P2_EVICT_FIRST)   // s1 is read once: keep s2 in L2 for pass 3
-                        tma_load_3d_ef(dst, &tmap, bar, kt * TW, q * P.boxh, (int)outer);
+                        tma_load_3d_ef(dst, tmap, bar, kt * TW, q * P.boxh, (int)outer);
                     else
-                        tma_load_3d(dst, &tmap, bar, kt * TW, q * P.boxh, (int)outer);
+                        tma_load_3d(dst, tmap, bar, kt * TW, q * P.boxh, (int)outer);
                 } else {
                     const int scene = (int)(outer / P.nyl);
                     const int jl = (int)(outer - (long long)scene * P.nyl);
-                    tma_load_4d(dst, &tmap, bar, kt * TW, jl, q * P.boxh, scene);
+                    tma_load_4d(dst, tmap, bar, kt * TW, jl, q * P.boxh, scene);
                 }
             }
         }
     }
     __syncthreads();
     mbar_wait(bar, 0);
-    column_tile<PASS, false, false, FW, true, SCAT, CMP, TW>(in, out, stk, meta, P, tile, &sc);
+    column_tile<PASS, false, false, FW, true, SCAT, CMP, TW>(in, out, stk, meta, P, tile, sc);
 #ifdef VX_PHASE_TIMING
     VX_PT(5);
     __syncthreads();
     VX_PT(6);
 #endif
+}
+
+// does this tile's scene take the windowed search (k_column_ring)?
+__device__ __forceinline__ bool ring_scene(const ColParams &P, int pass, long long outer) {
+    if (!P.fails) return false;
+    const long long scene = pass == 2 ? outer / P.nx : outer / P.nyl;
+    return (P.mcount ? __ldg(P.mcount + scene) : P.L) >= P.ring_min;
+}
+
+template <int PASS, int FW, bool SCAT, bool CMP, int MAXT, int TW = 32>
+__global__ void __launch_bounds__(MAXT, MAXT >= 1024 ? 1 : kColMinBlocks) k_column_tma(const __grid_constant__ CUtensorMap tmap,
+                                                     const __grid_constant__ CUtensorMap tmap1,
+                                                     const typename Col<PASS, false, false, FW>::InT *__restrict__ in,
+                                                     typename Col<PASS, false, false, FW>::OutT *__restrict__ out,
+                                                     const ColParams P, const __grid_constant__ ScatterTab sc) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    // natural tile t -> (tile, outer, kt), or false when it has nothing to do
+    auto natural = [&](long long t, long long &tile, long long &outer, int &kt) -> bool {
+        if constexpr (PASS == 2) {   // surplus CTAs skip their tile before any index math
+            if (P.xs && t >= (long long)__ldg(P.hdr) * P.nkt) return false;
+        }
+        tile = t;
+        kt = (int)(tile % P.nkt);
+        outer = tile / P.nkt;
+        if constexpr (PASS == 2) {
+            if (P.xs) {   // occupied-slice list: CTA rows map to occupied slices, the
+                          // surplus CTAs (empty slices) all sit at the end of the grid
+                const int m = __ldg(P.hdr);
+                // VX_P2_REVERSE: last occupied slice first -- pass 1 wrote the
+                // slices in ascending order, so the newest s1 lines, still in L2,
+                // are read first
+                outer = __ldg(P.xs + (VX_P2_REVERSE ? m - 1 - outer : outer));
+                tile = outer * P.nkt + kt;
+            } else if (P.sflag && !P.sflag[outer]) {
+                return false;   // empty slice: pass 3 never reads it
+            }
+        }
+        // windowed-search mode: the dense scenes' tiles were done by k_column_ring
+        return !ring_scene(P, PASS, outer);
+    };
+    long long tile, outer;
+    int kt;
+    if (!P.fails) {   // one tile per CTA
+        if (natural(blockIdx.x, tile, outer, kt))
+            col_tma_run<PASS, FW, SCAT, CMP, TW>(&tmap, &tmap1, in, out, P, &sc, smem, tile, outer, kt);
+        return;
+    }
+    // after k_column_ring (persistent grid): the other scenes' tiles, then the
+    // tiles the search handed back
+    bool first = true;
+    for (long long t = blockIdx.x; t < P.ntiles; t += gridDim.x) {
+        if (!natural(t, tile, outer, kt)) continue;
+        if (!first) __syncthreads();   // the previous tile's barrier and shared memory are free
+        first = false;
+        col_tma_run<PASS, FW, SCAT, CMP, TW>(&tmap, &tmap1, in, out, P, &sc, smem, tile, outer, kt);
+    }
+    const int nf = __ldcg(P.fails);
+    for (int i = blockIdx.x; i < nf; i += gridDim.x) {
+        if (!first) __syncthreads();
+        first = false;
+        tile = __ldcg(P.fails + 2 + i);
+        kt = (int)(tile % P.nkt);
+        outer = tile / P.nkt;
+        col_tma_run<PASS, FW, SCAT, CMP, TW>(&tmap, &tmap1, in, out, P, &sc, smem, tile, outer, kt);
+    }
+}
+
+// ---- dense tiles: windowed exact search ------------------------------------------
+// When every slice is occupied and sites are dense, each query row's answer
+// lies within a few rows: the reference's lower envelope (edt.py:253-317) gives,
+// for query row q, the FIRST row y minimising (q - y)^2 + w_y (ties: lowest row,
+// SURVEY 0.3).  With keys K_y = (w_y << rb) | y that is min_y (K_y + ((q-y)^2 << rb)),
+// and no row with (q - y)^2 > d_min can win, so rows q, q -+ 1, q -+ 2, ... are
+// scanned until r^2 exceeds the running minimum -- started from the previous
+// row's winner, which bounds the window at once.  One warp = 32 columns (lanes)
+// x one band of rows, all lanes on the same row (coalesced stores); the tile
+// (TMA-staged, then turned into keys in place) is read-only.  A tile whose
+// window would exceed P.ring_cap rows is handed back to the banded kernel.
+template <int PASS, bool SCAT, int TW>
+__global__ void __launch_bounds__(kColThreads, 3) k_column_ring(const __grid_constant__ CUtensorMap tmap,
+                                                                const typename Col<PASS, false, false, 0>::InT *__restrict__ in,
+                                                                typename Col<PASS, false, false, 0>::OutT *__restrict__ out,
+                                                                const ColParams P, const __grid_constant__ ScatterTab sc) {
+    using C = Col<PASS, false, false, 0>;
+    using InT = typename C::InT;
+    using OutT = typename C::OutT;
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint32_t *key = reinterpret_cast<uint32_t *>(smem);
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem + (size_t)P.rows_alloc * TW * 4);
+    int *s_fail = reinterpret_cast<int *>(bar + 1);
+    long long tile = blockIdx.x;
+    if constexpr (PASS == 2) {
+        if (P.xs && (long long)blockIdx.x >= (long long)__ldg(P.hdr) * P.nkt) return;
+    }
+    const int kt = (int)(tile % P.nkt);
+    long long outer = tile / P.nkt;
+    if constexpr (PASS == 2) {
+        if (P.xs) {
+            const int m = __ldg(P.hdr);
+            outer = __ldg(P.xs + (VX_P2_REVERSE ? m - 1 - outer : outer));
+            tile = outer * P.nkt + kt;
+        } else if (P.sflag && !P.sflag[outer]) {
+            return;
+        }
+    }
+    if (!ring_scene(P, PASS, outer)) return;   // the banded kernel takes this scene
+    const int scene = PASS == 2 ? 0 : (int)(outer / P.nyl);
+    const int jl = PASS == 2 ? 0 : (int)(outer - (long long)scene * P.nyl);
+    if (threadIdx.x == 0 && threadIdx.y == 0) {
+        *s_fail = 0;
+        mbar_init(bar, 1);
+        const int nbox = P.rows_alloc / P.boxh;
+        mbar_expect_tx(bar, (uint32_t)(P.rows_alloc * TW * 4));
+        for (int q = 0; q < nbox; ++q) {
+            void *dst = key + (size_t)q * P.boxh * TW;
+            if constexpr (PASS == 2) tma_load_3d(dst, &tmap, bar, kt * TW, q * P.boxh, (int)outer);
+            else tma_load_4d(dst, &tmap, bar, kt * TW, jl, q * P.boxh, scene);
+        }
+    }
+    const int kk = threadIdx.x, b = threadIdx.y;
+    const int k = kt * TW + kk;
+    const bool colok = k < P.nz;
+    const int lo = min(P.L, b * P.W), hi = min(P.L, lo + P.W);
+    const int jq = PASS == 2 ? 0 : P.j0 + jl;
+    long long base, stride;
+    if constexpr (PASS == 2) {
+        base = outer * P.plane + k;
+        stride = P.nz;
+    } else {
+        base = (long long)scene * P.nvox + (long long)jl * P.nz + k;
+        stride = P.splane;
+    }
+    // rows of empty slices hold no pass-2 codes (pass 2 skipped them)
+    const uint8_t *sfl = PASS == 3 && P.sflag3 && (P.mcount ? __ldg(P.mcount + scene) : 0) < P.nx
+                             ? P.sflag3 + (long long)scene * P.nx : nullptr;
+    const int rb = P.rb;
+    __syncthreads();
+    mbar_wait(bar, 0);
+    // the tile's values -> search keys, in place (each thread its band's rows)
+    uint32_t *col = key + kk;
+    if (colok) {
+#pragma unroll 4
+        for (int y = lo; y < hi; ++y) {
+            const uint32_t v = col[y * TW];
+            uint32_t kv = P.kinv;
+            if constexpr (PASS == 2) {
+                if ((int)v >= 0) {
+                    const int dz = k - (int)v;
+                    kv = ((uint32_t)(dz * dz) << rb) | (uint32_t)y;
+                }
+            } else {
+                if (v != 0xffffffffu && (!sfl || sfl[y])) {
+                    const int dy = jq - (int)(v >> P.zb), dz = k - (int)(v & P.zmask);
+                    kv = ((uint32_t)(dy * dy + dz * dz) << rb) | (uint32_t)y;
+                }
+            }
+            col[y * TW] = kv;
+        }
+    }
+    __syncthreads();
+    if (colok && lo < hi) {
+        const uint32_t rmask = (1u << rb) - 1u;
+        const uint32_t one = 1u << rb;
+        // shared byte addresses: this lane's column at row 0 and at row L-1;
+        // windows are clamped to them (a clamped read re-reads an edge row at a
+        // larger distance: a larger key, never a new minimum)
+        constexpr int rowb = TW * 4;
+        const int cb = (int)smem_u32(col), ce = cb + (P.L - 1) * rowb;
+        const int cap = P.ring_cap;
+        // cost guard: a tile whose windows average more than ring_budget steps
+        // per block is cheaper in the banded kernel -- hand it back early
+        const int budget = P.ring_budget;
+        int spent = -2 * budget;
+        const InT *src = in + base;
+        const uint32_t ustride = (uint32_t)stride;   // row offsets fit 32 bits (int32 sites)
+        RowOut<OutT, SCAT> dst;
+        dst.begin(out, base, stride, lo, &sc, outer, k, P.nz);
+        // four query rows per block share one window: step s reads rows
+        // q0 - s and q0 + 3 + s, at distances s..s+3 from the block's rows
+        constexpr int R = 4;
+        int crow = -1;
+        InT code = 0;
+        int wrow[R];
+        InT wcode[R];
+        int pend = 0;   // rows of the previous block waiting for their store
+        auto emit_pending = [&](int q0) {
+#pragma unroll
+            for (int i = 0; i < R; ++i) {
+                if (i < pend) {
+                    OutT o;
+                    if constexpr (PASS == 2) o = ((OutT)wrow[i] << P.zb) | (OutT)(uint32_t)wcode[i];
+                    else o = (int32_t)((uint32_t)wrow[i] * (uint32_t)P.plane + (wcode[i] >> P.zb) * (uint32_t)P.nz +
+                                       (wcode[i] & P.zmask));
+                    dst.put(q0 + i, o, &sc, outer, k, P.nz);
+                }
+            }
+        };
+        int qa = cb + lo * rowb;
+        int q0 = lo;
+        for (; q0 < hi; q0 += R, qa += R * rowb) {
+            if (*(volatile int *)s_fail) break;
+            emit_pending(q0 - R);   // the previous block's codes were fetched a block ago
+            const uint32_t k0 = lds_u32(qa), k1 = lds_u32(min(qa + rowb, ce));
+            const uint32_t k2 = lds_u32(min(qa + 2 * rowb, ce)), k3 = lds_u32(min(qa + 3 * rowb, ce));
+            uint32_t b0 = min(min(k0, k1 + one), min(k2 + 4u * one, k3 + 9u * one));
+            uint32_t b1 = min(min(k0 + one, k1), min(k2 + one, k3 + 4u * one));
+            uint32_t b2 = min(min(k0 + 4u * one, k1 + one), min(k2, k3 + one));
+            uint32_t b3 = min(min(k0 + 9u * one, k1 + 4u * one), min(k2 + one, k3));
+            // o_i = (s + i)^2 << rb; rows 0 and 3 next see distance s, rows 1 and 2 distance s + 1
+            uint32_t o0 = one, o1 = 4u * one, o2 = 9u * one, o3 = 16u * one, d3 = 7u * one;
+            int ro = rowb, sdone = 0;
+            while (max(b0, b3) >= o0 || max(b1, b2) >= o1) {
+                if (sdone >= cap) break;
+                const uint32_t kl = lds_u32(max(qa - ro, cb)), kr = lds_u32(min(qa + 3 * rowb + ro, ce));
+                b0 = min(b0, kl + o0); b1 = min(b1, kl + o1); b2 = min(b2, kl + o2); b3 = min(b3, kl + o3);
+                b0 = min(b0, kr + o3); b1 = min(b1, kr + o2); b2 = min(b2, kr + o1); b3 = min(b3, kr + o0);
+                o0 = o1; o1 = o2; o2 = o3;
+                d3 += 2u * one;
+                o3 += d3;        // (s + 4)^2 = (s + 3)^2 + 2 (s + 3) + 1
+                ro += rowb;
+                ++sdone;
+            }
+            spent += sdone - budget;
+            if (max(b0, b3) >= o0 || max(b1, b2) >= o1 || spent > 0) {   // beyond the cap, or too costly
+                *(volatile int *)s_fail = 1;
+                break;
+            }
+            const uint32_t bb[R] = {b0, b1, b2, b3};
+            pend = min(R, hi - q0);
+#pragma unroll
+            for (int i = 0; i < R; ++i) {
+                const int row = (int)(bb[i] & rmask);
+                if (row != crow) {
+                    crow = row;
+                    code = __ldg(src + (uint32_t)row * ustride);
+                }
+                wrow[i] = row;
+                wcode[i] = code;
+            }
+        }
+        if (q0 >= hi) emit_pending(q0 - R);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && threadIdx.y == 0 && *(volatile int *)s_fail) {
+        const int idx = atomicAdd(P.fails, 1);
+        P.fails[2 + idx] = (int)tile;
+    }
 }
 
 // Columns too long for shared memory: per-CTA stack slab in global scratch,
@@ -1131,6 +1373,41 @@ int pow2ceil(int v) {
 
 constexpr size_t kSmemLimit = 227 * 1024;
 
+// windowed search (k_column_ring): VX_RING=0 disables it, VX_RING_CAP sets the
+// largest search radius (rows) before a tile goes back to the banded kernel,
+// VX_RING_MIN the fraction (percent) of occupied slices from which a scene counts as dense
+inline int ring_cap() {
+    const char *e = getenv("VX_RING_CAP");
+    return e ? std::max(1, std::min(atoi(e), 1024)) : 64;
+}
+inline int ring_budget(int pass) {
+    const char *e = getenv(pass == 2 ? "VX_RING_BUDGET2" : "VX_RING_BUDGET3");
+    return e ? std::max(1, atoi(e)) : 24;
+}
+inline bool ring_enabled() {
+    const char *e = getenv("VX_RING");
+    return !(e && atoi(e) == 0);
+}
+inline int ring_min_for(int nx) {
+    const char *e = getenv("VX_RING_MIN");
+    const int pct = e ? atoi(e) : 90;
+    return std::max(1, (int)(((long long)nx * pct + 99) / 100));
+}
+// keys (w << rb | row) plus the largest window offset ((cap + 4)^2 << rb)
+// stay below the invalid key, which plus that offset stays below 2^32
+constexpr int kRingBlock = 4;
+inline uint32_t ring_kinv(int rb) {
+    const long long c = ring_cap() + kRingBlock + 1;
+    return (uint32_t)(0xFFFFFFFFLL - ((c * c) << rb));
+}
+bool ring_fits(const EdtPlan &p, int pass, int L) {
+    const int rb = std::max(1, bits_of(L - 1));
+    const long long wmax = pass == 2 ? (long long)(p.nz - 1) * (p.nz - 1)
+                                     : (long long)(p.ny - 1) * (p.ny - 1) + (long long)(p.nz - 1) * (p.nz - 1);
+    const long long c = ring_cap() + kRingBlock + 1;
+    return rb <= 12 && ((wmax + c * c + 1) << rb) < (long long)ring_kinv(rb);
+}
+
 // pass 2: `outer` counts slices (nscenes * local nx); pass 3: `outer` counts
 // (scene, local j) with nyl rows of j starting at global row j0.
 ColParams col_params(const EdtPlan &p, int pass, long long nouter, int nyl, int j0) {
@@ -1156,6 +1433,14 @@ ColParams col_params(const EdtPlan &p, int pass, long long nouter, int nyl, int 
     P.xs = nullptr;
     P.hdr = nullptr;
     P.stream_max = -1;
+    P.mcount = nullptr;
+    P.sflag3 = nullptr;
+    P.ring_min = 0x7fffffff;
+    P.fails = nullptr;
+    P.rb = bits_of(P.L - 1) > 0 ? bits_of(P.L - 1) : 1;
+    P.ring_cap = ring_cap();
+    P.ring_budget = ring_budget(pass);
+    P.kinv = ring_kinv(P.rb);
     P.boxh = std::min(P.L, 256);
     P.rows_alloc = (P.L + P.boxh - 1) / P.boxh * P.boxh;
     return P;
@@ -1283,15 +1568,45 @@ cudaError_t launch_col(const void *in, void *out, void *gstack, const EdtPlan &p
                     }
                 }
                 const size_t smem = PASS == 2 ? p.smem2 : p.smem3;
-                if (tw == 16) {
-                    // 32 bands x 16 columns = 512 threads (two bands per warp)
+                if (tw == 16) {   // tile numbering of the ring and banded kernels
                     P.nkt = (p.nz + 15) / 16;
                     P.ntiles = (long long)P.nkt * nouter;
+                }
+                // dense scenes: the windowed search first; the banded launch
+                // below then takes the other scenes' tiles and the tiles the
+                // search handed back (decided per scene on the device)
+                if constexpr (FW <= 1) {
+                    const int rmin = ring_min_for(p.nx);
+                    const int mode3 = PASS == 3 && sp ? sp->p3_mode : 0;
+                    if (sp && sp->fails && ring_enabled() && mode3 != 1 && ring_fits(p, PASS, P.L) &&
+                        tw * P.B <= kColThreads &&
+                        (sp->m_hint < 0 || sp->m_hint >= rmin)) {
+                        P.mcount = sp->hdr;
+                        P.sflag3 = PASS == 3 ? sp->sflag : nullptr;
+                        P.ring_min = rmin;
+                        P.fails = sp->fails;
+                        cudaError_t e = cudaMemsetAsync(sp->fails, 0, 8, st);
+                        if (e != cudaSuccess) return e;
+                        const size_t rsm = (size_t)P.rows_alloc * tw * 4 + 16;
+                        auto rk = tw == 16 ? k_column_ring<PASS, SCAT, 16> : k_column_ring<PASS, SCAT, 32>;
+                        e = allow_smem(rk);
+                        if (e != cudaSuccess) return e;
+                        rk<<<(unsigned)P.ntiles, dim3(tw, P.B), rsm, st>>>(
+                            m, reinterpret_cast<const typename C::InT *>(in), reinterpret_cast<typename C::OutT *>(out),
+                            P, sc);
+                        e = cudaGetLastError();
+                        if (e != cudaSuccess) return e;
+                    }
+                }
+                if (tw == 16) {
+                    // 32 bands x 16 columns = 512 threads (two bands per warp)
                     auto kern = cmp ? k_column_tma<PASS, FW, SCAT, true, kColThreads, 16>
                                     : k_column_tma<PASS, FW, SCAT, false, kColThreads, 16>;
                     cudaError_t e = allow_smem(kern);
                     if (e != cudaSuccess) return e;
-                    kern<<<(unsigned)P.ntiles, dim3(16, P.B), smem, st>>>(
+                    const unsigned g16 = P.fails ? (unsigned)std::min<long long>(P.ntiles, 3LL * num_sms())
+                                                 : (unsigned)P.ntiles;
+                    kern<<<g16, dim3(16, P.B), smem, st>>>(
                         m, m1, reinterpret_cast<const typename C::InT *>(in),
                         reinterpret_cast<typename C::OutT *>(out), P, sc);
                     return cudaGetLastError();
@@ -1304,7 +1619,9 @@ cudaError_t launch_col(const void *in, void *out, void *gstack, const EdtPlan &p
                                        : k_column_tma<PASS, FW, SCAT, false, kColThreads>);
                 cudaError_t e = allow_smem(kern);
                 if (e != cudaSuccess) return e;
-                kern<<<(unsigned)P.ntiles, block, smem, st>>>(m, m1, reinterpret_cast<const typename C::InT *>(in),
+                const unsigned gb = P.fails ? (unsigned)std::min<long long>(P.ntiles, 3LL * num_sms())
+                                            : (unsigned)P.ntiles;
+                kern<<<gb, block, smem, st>>>(m, m1, reinterpret_cast<const typename C::InT *>(in),
                                                               reinterpret_cast<typename C::OutT *>(out), P, sc);
                 return cudaGetLastError();
             }
@@ -1641,9 +1958,16 @@ int pass3_mode_hint(const EdtPlan &p, int m) {
     return m <= smax ? 1 : 2;
 }
 
+// hand-back list of the windowed search: [count, spare, tiles of either pass]
+static size_t fail_list_bytes(const EdtPlan &p, int nscenes) {
+    const size_t t2 = (size_t)((p.nz + p.tw2 - 1) / p.tw2) * p.nx, t3 = (size_t)((p.nz + p.tw3 - 1) / p.tw3) * p.ny;
+    return ((2 + std::max(t2, t3) * nscenes) * 4 + 255) / 256 * 256;
+}
+
 size_t sparse_bytes(const EdtPlan &p, int nscenes) {
     const size_t sx = (size_t)p.nx * nscenes;
-    return (sx + 255) / 256 * 256 + (sx * 4 + 255) / 256 * 256 + ((size_t)nscenes * 4 + 255) / 256 * 256;
+    return (sx + 255) / 256 * 256 + (sx * 4 + 255) / 256 * 256 + ((size_t)nscenes * 4 + 255) / 256 * 256 +
+           fail_list_bytes(p, nscenes);
 }
 
 size_t scratch_bytes_for(const EdtPlan &p, int nscenes) {
@@ -1665,6 +1989,8 @@ SparseRows sparse_rows_at(void *where, const EdtPlan &p, int nscenes) {
     sp.sflag = b;
     sp.xs = reinterpret_cast<int *>(b + (sx + 255) / 256 * 256);
     sp.hdr = reinterpret_cast<int *>(b + (sx + 255) / 256 * 256 + (sx * 4 + 255) / 256 * 256);
+    sp.fails = reinterpret_cast<int *>(b + (sx + 255) / 256 * 256 + (sx * 4 + 255) / 256 * 256 +
+                                       ((size_t)nscenes * 4 + 255) / 256 * 256);
     return sp;
 }
 

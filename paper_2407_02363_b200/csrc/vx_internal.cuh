@@ -48,6 +48,8 @@ struct SparseRows {
     int *m_mirror = nullptr;  // optional host-mapped copy of hdr[0] (the next call's hint)
     int p3_mode = 0;          // pass 3: 0 both kernels, gated on the device by the
                               // count; 1 one warp per tile only; 2 banded only
+    int *fails = nullptr;     // [2 + tiles] hand-back list of the windowed search
+    int m_hint = -1;          // predicted count (>= 0: skip the windowed search when sparse)
 };
 
 // Pass launchers (stream-ordered, no host sync).  Return cudaError_t.
