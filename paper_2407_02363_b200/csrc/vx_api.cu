@@ -902,6 +902,7 @@ struct vx_cycle {
     // device) -> which pass-3 kernels the next tick launches
     int *h_m = nullptr, *d_m = nullptr;
     int p3_mode = 0, g_mode = -1;
+    int m_hint = -1;   // previous tick's occupied-slice count (dense scenes: windowed search)
     int captures = 0, last_graph = 0;   // vx_cycle_info
     unsigned char *h_out = nullptr, *d_out = nullptr;   // packed results (host-mapped)
     // vx_cycle_prefetch: the next cloud is uploaded on a copy stream into one
@@ -1120,6 +1121,7 @@ static cudaError_t edt_passes(vx_cycle *cy, const vx_grid *src, int32_t *site, b
         if (src == cy->env) {   // the per-tick map: feed and use the count hint
             sp.m_mirror = cy->d_m;
             sp.p3_mode = cy->p3_mode;
+            sp.m_hint = cy->m_hint;
         }
         if (list_ready) {
             // the insert's finalize built the list (and the host-mapped hint)
@@ -1316,11 +1318,14 @@ static int cycle_step(vx_cycle *cy, const double *pts, const double *d_pts_in, i
     cy->mark(2);
     if (graph_path) {
         // the graph reads the cloud pointer and its size from the staged block
-        cy->p3_mode = pass3_mode_hint(cy->plan, *(volatile int *)cy->h_m);
+        cy->m_hint = *(volatile int *)cy->h_m;
+        cy->p3_mode = pass3_mode_hint(cy->plan, cy->m_hint);
+        // the kernels the capture contains follow both hints
+        const int gmode = cy->p3_mode * 2 + (ring_hint_on(cy->plan, cy->m_hint) ? 1 : 0);
         // reset modes from the grids' state before this tick (a capture below
         // runs cycle_main_seq, which already marks the grids as reset)
         const int dense_mask = cy->mask->sparse_ok ? 0 : 1, dense_env = cy->env->sparse_ok ? 0 : 1;
-        if (!cy->gexec || cy->g_s != s || cy->g_hit != hit || cy->g_thr != thr || cy->g_mode != cy->p3_mode) {
+        if (!cy->gexec || cy->g_s != s || cy->g_hit != hit || cy->g_thr != thr || cy->g_mode != gmode) {
             drop_graph(cy);
             const long long l0 = c->launches;
             VX_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed));
@@ -1344,7 +1349,7 @@ static int cycle_step(vx_cycle *cy, const double *pts, const double *d_pts_in, i
             cy->g_kernels = c->launches - l0;
             c->launches = l0;
             cy->g_s = s;
-            cy->g_mode = cy->p3_mode;
+            cy->g_mode = gmode;
             cy->g_hit = hit;
             cy->g_thr = thr;
         }
@@ -1373,7 +1378,8 @@ static int cycle_step(vx_cycle *cy, const double *pts, const double *d_pts_in, i
         c->launches += cy->g_kernels;
         if (pf_slot >= 0) VX_CUDA(cudaEventRecord(cy->ev_used[pf_slot], st));   // the tick read the slot
     } else {
-        cy->p3_mode = pass3_mode_hint(cy->plan, *(volatile int *)cy->h_m);
+        cy->m_hint = *(volatile int *)cy->h_m;
+        cy->p3_mode = pass3_mode_hint(cy->plan, cy->m_hint);
         if ((rc = cycle_main_seq(cy, d_pts, npts, nullptr, hit, thr, s, true))) return rc;
         if (pf_slot >= 0) VX_CUDA(cudaEventRecord(cy->ev_used[pf_slot], st));
     }

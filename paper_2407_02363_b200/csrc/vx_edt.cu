@@ -107,6 +107,7 @@ constexpr int kStreamMaxRows = VX_STREAM_MAX_ROWS;
 #define VX_COL_WALK_UNROLL 4   // phase-D rows per loop trip in the banded column kernels
 #endif
 constexpr int kColWalkUnroll = VX_COL_WALK_UNROLL;
+
 constexpr int kColMinBlocks = VX_COL_MIN_BLOCKS;
 
 // bit e (e = 0..3) set iff byte e of w is non-zero
@@ -192,9 +193,11 @@ __global__ void __launch_bounds__(256) k_pass1_v4(const uint8_t *__restrict__ oc
                                                   int32_t *__restrict__ s1,
                                                   long long nlines, int nz,
                                                   const uint8_t *__restrict__ sflag, int ny,
-                                                  const int *__restrict__ xs, const int *__restrict__ hdr) {
+                                                  const int *__restrict__ xs, const int *__restrict__ hdr,
+                                                  int *__restrict__ linestat) {
     const int lane = threadIdx.x & 31;
     const int nq = nz >> 2;
+    int nempty = 0, nseen = 0;   // k-lines without a site / processed (the windowed search's gate)
     uint32_t nib[LPW][CMAX];
     bool act[LPW];
     long long lines[LPW];
@@ -231,7 +234,9 @@ __global__ void __launch_bounds__(256) k_pass1_v4(const uint8_t *__restrict__ oc
         uint32_t any = 0;
 #pragma unroll
         for (int c = 0; c < CMAX; ++c) any |= nib[l][c];
+        ++nseen;
         if (!__any_sync(VX_FULL_MASK, any != 0u)) {   // empty line: no site anywhere (edt.py:212)
+            ++nempty;
 #pragma unroll
             for (int c = 0; c < CMAX; ++c) {
                 const int q = c * 32 + lane;
@@ -241,6 +246,20 @@ __global__ void __launch_bounds__(256) k_pass1_v4(const uint8_t *__restrict__ oc
         }
         pass1_line<CMAX>(nib[l], dst, nq, lane);
     }
+    }
+    if (linestat) {   // per CTA: two atomics
+        __shared__ int s_cnt[2];
+        if (threadIdx.x == 0) s_cnt[0] = s_cnt[1] = 0;
+        __syncthreads();
+        if (lane == 0 && nseen) {
+            atomicAdd(&s_cnt[0], nempty);
+            atomicAdd(&s_cnt[1], nseen);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0 && s_cnt[1]) {
+            atomicAdd(linestat + 2, s_cnt[0]);
+            atomicAdd(linestat + 3, s_cnt[1]);
+        }
     }
 }
 
@@ -302,12 +321,14 @@ struct ColParams {
     const int *xs;         // occupied slice indices, ascending
     const int *hdr;        // hdr[0] = number of occupied slices (device-side)
     int stream_max;        // pass 3: k_pass3_stream takes m <= stream_max (-1: never)
-    // windowed search (k_column_ring) for dense scenes; the banded kernel then
-    // only takes the other scenes' tiles and the tiles the search gave up on
+    // windowed search (ring_tile) for dense scenes, tried first by k_column_tma<RING>
     const int *mcount;     // per-scene occupied-slice counts (nullptr: treat every scene as dense)
     const uint8_t *sflag3; // pass 3: per (scene, slice) flags (rows of empty slices hold no codes)
     int ring_min;          // scenes with >= ring_min occupied slices take the windowed search
-    int *fails;            // [0] count, [1] spare, [2..] tiles handed back to the banded kernel
+    int *rhdr;             // search header: [0] pass-2 / [1] pass-3 fall-back counts, [2] empty
+                           // k-lines and [3] k-lines seen by pass 1 (nullptr: no search)
+    int fslot;             // 0 pass 2, 1 pass 3
+    int nkt2, ny2;         // pass-2 tiling (pass 3's gate on pass 2's hand-backs)
     int rb;                // row bits of the search keys (w << rb | row)
     int ring_cap;          // largest search radius before a tile is handed back
     int ring_budget;       // mean window steps per 4-row block above which a tile is handed back
@@ -884,69 +905,20 @@ __device__ __forceinline__ void col_tma_run(const CUtensorMap *tmap, const CUten
 #endif
 }
 
-// does this tile's scene take the windowed search (k_column_ring)?
+// is the windowed search on for this call?  Pass 1 counted the k-lines without
+// any site: when more than 1 in 10 is empty the rows are too sparse for it.
+// Pass 3 also stays off when pass 2 fell back on more than 1 tile in 8.
+__device__ __forceinline__ bool ring_active(const ColParams &P) {
+    if (!P.rhdr) return false;
+    const int empty = __ldcg(P.rhdr + 2), lines = __ldcg(P.rhdr + 3);
+    if (empty * 10LL > (long long)lines) return false;
+    if (P.fslot == 1 && __ldcg(P.rhdr) * 8LL > (long long)lines / max(P.ny2, 1) * P.nkt2) return false;
+    return true;
+}
+// does this tile's scene take the windowed search?
 __device__ __forceinline__ bool ring_scene(const ColParams &P, int pass, long long outer) {
-    if (!P.fails) return false;
     const long long scene = pass == 2 ? outer / P.nx : outer / P.nyl;
     return (P.mcount ? __ldg(P.mcount + scene) : P.L) >= P.ring_min;
-}
-
-template <int PASS, int FW, bool SCAT, bool CMP, int MAXT, int TW = 32>
-__global__ void __launch_bounds__(MAXT, MAXT >= 1024 ? 1 : kColMinBlocks) k_column_tma(const __grid_constant__ CUtensorMap tmap,
-                                                     const __grid_constant__ CUtensorMap tmap1,
-                                                     const typename Col<PASS, false, false, FW>::InT *__restrict__ in,
-                                                     typename Col<PASS, false, false, FW>::OutT *__restrict__ out,
-                                                     const ColParams P, const __grid_constant__ ScatterTab sc) {
-    extern __shared__ __align__(128) unsigned char smem[];
-    // natural tile t -> (tile, outer, kt), or false when it has nothing to do
-    auto natural = [&](long long t, long long &tile, long long &outer, int &kt) -> bool {
-        if constexpr (PASS == 2) {   // surplus CTAs skip their tile before any index math
-            if (P.xs && t >= (long long)__ldg(P.hdr) * P.nkt) return false;
-        }
-        tile = t;
-        kt = (int)(tile % P.nkt);
-        outer = tile / P.nkt;
-        if constexpr (PASS == 2) {
-            if (P.xs) {   // occupied-slice list: CTA rows map to occupied slices, the
-                          // surplus CTAs (empty slices) all sit at the end of the grid
-                const int m = __ldg(P.hdr);
-                // VX_P2_REVERSE: last occupied slice first -- pass 1 wrote the
-                // slices in ascending order, so the newest s1 lines, still in L2,
-                // are read first
-                outer = __ldg(P.xs + (VX_P2_REVERSE ? m - 1 - outer : outer));
-                tile = outer * P.nkt + kt;
-            } else if (P.sflag && !P.sflag[outer]) {
-                return false;   // empty slice: pass 3 never reads it
-            }
-        }
-        // windowed-search mode: the dense scenes' tiles were done by k_column_ring
-        return !ring_scene(P, PASS, outer);
-    };
-    long long tile, outer;
-    int kt;
-    if (!P.fails) {   // one tile per CTA
-        if (natural(blockIdx.x, tile, outer, kt))
-            col_tma_run<PASS, FW, SCAT, CMP, TW>(&tmap, &tmap1, in, out, P, &sc, smem, tile, outer, kt);
-        return;
-    }
-    // after k_column_ring (persistent grid): the other scenes' tiles, then the
-    // tiles the search handed back
-    bool first = true;
-    for (long long t = blockIdx.x; t < P.ntiles; t += gridDim.x) {
-        if (!natural(t, tile, outer, kt)) continue;
-        if (!first) __syncthreads();   // the previous tile's barrier and shared memory are free
-        first = false;
-        col_tma_run<PASS, FW, SCAT, CMP, TW>(&tmap, &tmap1, in, out, P, &sc, smem, tile, outer, kt);
-    }
-    const int nf = __ldcg(P.fails);
-    for (int i = blockIdx.x; i < nf; i += gridDim.x) {
-        if (!first) __syncthreads();
-        first = false;
-        tile = __ldcg(P.fails + 2 + i);
-        kt = (int)(tile % P.nkt);
-        outer = tile / P.nkt;
-        col_tma_run<PASS, FW, SCAT, CMP, TW>(&tmap, &tmap1, in, out, P, &sc, smem, tile, outer, kt);
-    }
 }
 
 // ---- dense tiles: windowed exact search ------------------------------------------
@@ -954,40 +926,26 @@ __global__ void __launch_bounds__(MAXT, MAXT >= 1024 ? 1 : kColMinBlocks) k_colu
 // lies within a few rows: the reference's lower envelope (edt.py:253-317) gives,
 // for query row q, the FIRST row y minimising (q - y)^2 + w_y (ties: lowest row,
 // SURVEY 0.3).  With keys K_y = (w_y << rb) | y that is min_y (K_y + ((q-y)^2 << rb)),
-// and no row with (q - y)^2 > d_min can win, so rows q, q -+ 1, q -+ 2, ... are
-// scanned until r^2 exceeds the running minimum -- started from the previous
-// row's winner, which bounds the window at once.  One warp = 32 columns (lanes)
-// x one band of rows, all lanes on the same row (coalesced stores); the tile
-// (TMA-staged, then turned into keys in place) is read-only.  A tile whose
-// window would exceed P.ring_cap rows is handed back to the banded kernel.
+// and no row with (q - y)^2 > d_min can win, so the window around q grows one
+// row per side until the next distance squared exceeds the running minimum.
+// One warp = 32 columns (lanes) x one band of rows, all lanes on the same rows
+// (coalesced stores); four query rows share one window; the tile (TMA-staged,
+// then turned into keys in place) is read-only.  Returns false when a window
+// would exceed P.ring_cap rows or the windows cost more than P.ring_budget steps
+// per block on average: the caller then runs the banded kernel on the tile.
 template <int PASS, bool SCAT, int TW>
-__global__ void __launch_bounds__(kColThreads, 3) k_column_ring(const __grid_constant__ CUtensorMap tmap,
-                                                                const typename Col<PASS, false, false, 0>::InT *__restrict__ in,
-                                                                typename Col<PASS, false, false, 0>::OutT *__restrict__ out,
-                                                                const ColParams P, const __grid_constant__ ScatterTab sc) {
+__device__ __forceinline__ bool ring_tile(const typename Col<PASS, false, false, 0>::InT *__restrict__ in,
+                                          typename Col<PASS, false, false, 0>::OutT *__restrict__ out,
+                                          const ColParams &P, const ScatterTab *scp, unsigned char *smem,
+                                          const CUtensorMap *tmapp, long long tile, long long outer, int kt) {
     using C = Col<PASS, false, false, 0>;
     using InT = typename C::InT;
     using OutT = typename C::OutT;
-    extern __shared__ __align__(128) unsigned char smem[];
+    const ScatterTab &sc = *scp;
+    const CUtensorMap &tmap = *tmapp;
     uint32_t *key = reinterpret_cast<uint32_t *>(smem);
     uint64_t *bar = reinterpret_cast<uint64_t *>(smem + (size_t)P.rows_alloc * TW * 4);
     int *s_fail = reinterpret_cast<int *>(bar + 1);
-    long long tile = blockIdx.x;
-    if constexpr (PASS == 2) {
-        if (P.xs && (long long)blockIdx.x >= (long long)__ldg(P.hdr) * P.nkt) return;
-    }
-    const int kt = (int)(tile % P.nkt);
-    long long outer = tile / P.nkt;
-    if constexpr (PASS == 2) {
-        if (P.xs) {
-            const int m = __ldg(P.hdr);
-            outer = __ldg(P.xs + (VX_P2_REVERSE ? m - 1 - outer : outer));
-            tile = outer * P.nkt + kt;
-        } else if (P.sflag && !P.sflag[outer]) {
-            return;
-        }
-    }
-    if (!ring_scene(P, PASS, outer)) return;   // the banded kernel takes this scene
     const int scene = PASS == 2 ? 0 : (int)(outer / P.nyl);
     const int jl = PASS == 2 ? 0 : (int)(outer - (long long)scene * P.nyl);
     if (threadIdx.x == 0 && threadIdx.y == 0) {
@@ -1067,16 +1025,19 @@ __global__ void __launch_bounds__(kColThreads, 3) k_column_ring(const __grid_con
         int wrow[R];
         InT wcode[R];
         int pend = 0;   // rows of the previous block waiting for their store
+        const uint32_t plane = (uint32_t)P.plane, nzu = (uint32_t)P.nz, zb = (uint32_t)P.zb, zmask = P.zmask;
+        auto out_of = [&](int row, InT c) -> OutT {
+            if constexpr (PASS == 2) return ((OutT)row << zb) | (OutT)(uint32_t)c;
+            else return (int32_t)((uint32_t)row * plane + (c >> zb) * nzu + (c & zmask));
+        };
         auto emit_pending = [&](int q0) {
+            if (pend == R) {   // full block: four straight stores
 #pragma unroll
-            for (int i = 0; i < R; ++i) {
-                if (i < pend) {
-                    OutT o;
-                    if constexpr (PASS == 2) o = ((OutT)wrow[i] << P.zb) | (OutT)(uint32_t)wcode[i];
-                    else o = (int32_t)((uint32_t)wrow[i] * (uint32_t)P.plane + (wcode[i] >> P.zb) * (uint32_t)P.nz +
-                                       (wcode[i] & P.zmask));
-                    dst.put(q0 + i, o, &sc, outer, k, P.nz);
-                }
+                for (int i = 0; i < R; ++i) dst.put(q0 + i, out_of(wrow[i], wcode[i]), &sc, outer, k, P.nz);
+            } else {
+#pragma unroll
+                for (int i = 0; i < R; ++i)
+                    if (i < pend) dst.put(q0 + i, out_of(wrow[i], wcode[i]), &sc, outer, k, P.nz);
             }
         };
         int qa = cb + lo * rowb;
@@ -1090,22 +1051,31 @@ __global__ void __launch_bounds__(kColThreads, 3) k_column_ring(const __grid_con
             uint32_t b1 = min(min(k0 + one, k1), min(k2 + one, k3 + 4u * one));
             uint32_t b2 = min(min(k0 + 4u * one, k1 + one), min(k2, k3 + one));
             uint32_t b3 = min(min(k0 + 9u * one, k1 + 4u * one), min(k2 + one, k3));
-            // o_i = (s + i)^2 << rb; rows 0 and 3 next see distance s, rows 1 and 2 distance s + 1
-            uint32_t o0 = one, o1 = 4u * one, o2 = 9u * one, o3 = 16u * one, d3 = 7u * one;
+            // o_i = (s + i)^2 << rb; rows 0 and 3 next see distance s, rows 1 and 2
+            // distance s + 1.  Two steps per trip (one exit test; an extra step
+            // only adds larger keys)
+            uint32_t o0 = one, o1 = 4u * one, o2 = 9u * one, o3 = 16u * one, d3 = 9u * one;
+            const int qb = qa + 3 * rowb;
             int ro = rowb, sdone = 0;
-            while (max(b0, b3) >= o0 || max(b1, b2) >= o1) {
-                if (sdone >= cap) break;
-                const uint32_t kl = lds_u32(max(qa - ro, cb)), kr = lds_u32(min(qa + 3 * rowb + ro, ce));
+            bool more = (max(b0, b3) >= o0) | (max(b1, b2) >= o1);
+            while (more & (sdone < cap)) {
+                const uint32_t o4 = o3 + d3;   // (s + 4)^2
+                d3 += 2u * one;
+                uint32_t kl = lds_u32(max(qa - ro, cb)), kr = lds_u32(min(qb + ro, ce));
+                const uint32_t kl2 = lds_u32(max(qa - ro - rowb, cb)), kr2 = lds_u32(min(qb + ro + rowb, ce));
                 b0 = min(b0, kl + o0); b1 = min(b1, kl + o1); b2 = min(b2, kl + o2); b3 = min(b3, kl + o3);
                 b0 = min(b0, kr + o3); b1 = min(b1, kr + o2); b2 = min(b2, kr + o1); b3 = min(b3, kr + o0);
-                o0 = o1; o1 = o2; o2 = o3;
+                b0 = min(b0, kl2 + o1); b1 = min(b1, kl2 + o2); b2 = min(b2, kl2 + o3); b3 = min(b3, kl2 + o4);
+                b0 = min(b0, kr2 + o4); b1 = min(b1, kr2 + o3); b2 = min(b2, kr2 + o2); b3 = min(b3, kr2 + o1);
+                o0 = o2; o1 = o3; o2 = o4;
+                o3 = o4 + d3;                  // (s + 5)^2
                 d3 += 2u * one;
-                o3 += d3;        // (s + 4)^2 = (s + 3)^2 + 2 (s + 3) + 1
-                ro += rowb;
-                ++sdone;
+                ro += 2 * rowb;
+                sdone += 2;
+                more = (max(b0, b3) >= o0) | (max(b1, b2) >= o1);
             }
             spent += sdone - budget;
-            if (max(b0, b3) >= o0 || max(b1, b2) >= o1 || spent > 0) {   // beyond the cap, or too costly
+            if (more | (spent > 0)) {   // beyond the cap, or too costly
                 *(volatile int *)s_fail = 1;
                 break;
             }
@@ -1116,7 +1086,7 @@ __global__ void __launch_bounds__(kColThreads, 3) k_column_ring(const __grid_con
                 const int row = (int)(bb[i] & rmask);
                 if (row != crow) {
                     crow = row;
-                    code = __ldg(src + (uint32_t)row * ustride);
+                    code = __ldg(src + (size_t)((uint32_t)row * ustride));
                 }
                 wrow[i] = row;
                 wcode[i] = code;
@@ -1125,10 +1095,51 @@ __global__ void __launch_bounds__(kColThreads, 3) k_column_ring(const __grid_con
         if (q0 >= hi) emit_pending(q0 - R);
     }
     __syncthreads();
-    if (threadIdx.x == 0 && threadIdx.y == 0 && *(volatile int *)s_fail) {
-        const int idx = atomicAdd(P.fails, 1);
-        P.fails[2 + idx] = (int)tile;
+    const bool failed = *(volatile int *)s_fail != 0;
+    if (failed && threadIdx.x == 0 && threadIdx.y == 0) atomicAdd(P.rhdr + P.fslot, 1);   // pass 3's gate
+    return !failed;
+}
+
+
+// Passes 2/3 with TMA-staged tiles, one tile per CTA.  RING: dense scenes first
+// try the windowed search on the tile; on a fall-back the tile is re-staged
+// and takes the banded path (column_tile).
+template <int PASS, int FW, bool SCAT, bool CMP, int MAXT, int TW = 32, bool RING = false>
+__global__ void __launch_bounds__(MAXT, MAXT >= 1024 ? 1 : (RING ? 3 : kColMinBlocks)) k_column_tma(const __grid_constant__ CUtensorMap tmap,
+                                                     const __grid_constant__ CUtensorMap tmap1,
+                                                     const typename Col<PASS, false, false, FW>::InT *__restrict__ in,
+                                                     typename Col<PASS, false, false, FW>::OutT *__restrict__ out,
+                                                     const ColParams P, const __grid_constant__ ScatterTab sc) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    long long tile = blockIdx.x;
+    if constexpr (PASS == 2) {   // surplus CTAs leave before any index math
+        if (P.xs && (long long)blockIdx.x >= (long long)__ldg(P.hdr) * P.nkt) return;
     }
+    const int kt = (int)(tile % P.nkt);
+    long long outer = tile / P.nkt;
+    if constexpr (PASS == 2) {
+        if (P.xs) {   // occupied-slice list: CTA rows map to occupied slices, the
+                      // surplus CTAs (empty slices) all sit at the end of the grid
+            const int m = __ldg(P.hdr);
+            // VX_P2_REVERSE: last occupied slice first -- pass 1 wrote the
+            // slices in ascending order, so the newest s1 lines, still in L2,
+            // are read first
+            outer = __ldg(P.xs + (VX_P2_REVERSE ? m - 1 - outer : outer));
+            tile = outer * P.nkt + kt;
+        } else if (P.sflag && !P.sflag[outer]) {
+            return;   // empty slice: pass 3 never reads it
+        }
+    }
+    if constexpr (RING && FW <= 1) {
+        if (ring_active(P) && ring_scene(P, PASS, outer)) {
+            if (ring_tile<PASS, SCAT, TW>(reinterpret_cast<const typename Col<PASS, false, false, 0>::InT *>(in),
+                                          reinterpret_cast<typename Col<PASS, false, false, 0>::OutT *>(out), P,
+                                          &sc, smem, &tmap, tile, outer, kt))
+                return;
+            __syncthreads();   // the search's shared memory and barrier are free again
+        }
+    }
+    col_tma_run<PASS, FW, SCAT, CMP, TW>(&tmap, &tmap1, in, out, P, &sc, smem, tile, outer, kt);
 }
 
 // Columns too long for shared memory: per-CTA stack slab in global scratch,
@@ -1373,7 +1384,7 @@ int pow2ceil(int v) {
 
 constexpr size_t kSmemLimit = 227 * 1024;
 
-// windowed search (k_column_ring): VX_RING=0 disables it, VX_RING_CAP sets the
+// windowed search (ring_tile): VX_RING=0 disables it, VX_RING_CAP sets the
 // largest search radius (rows) before a tile goes back to the banded kernel,
 // VX_RING_MIN the fraction (percent) of occupied slices from which a scene counts as dense
 inline int ring_cap() {
@@ -1399,6 +1410,11 @@ constexpr int kRingBlock = 4;
 inline uint32_t ring_kinv(int rb) {
     const long long c = ring_cap() + kRingBlock + 1;
     return (uint32_t)(0xFFFFFFFFLL - ((c * c) << rb));
+}
+// may this call use the windowed search at all (host side; the device gates it per call)?
+bool ring_possible(const EdtPlan &p, const SparseRows *sp) {
+    return sp && sp->fails && ring_enabled() && p.tma2 && p.tma3 &&
+           (sp->m_hint < 0 || sp->m_hint >= ring_min_for(p.nx));
 }
 bool ring_fits(const EdtPlan &p, int pass, int L) {
     const int rb = std::max(1, bits_of(L - 1));
@@ -1436,7 +1452,10 @@ ColParams col_params(const EdtPlan &p, int pass, long long nouter, int nyl, int 
     P.mcount = nullptr;
     P.sflag3 = nullptr;
     P.ring_min = 0x7fffffff;
-    P.fails = nullptr;
+    P.rhdr = nullptr;
+    P.fslot = pass == 2 ? 0 : 1;
+    P.nkt2 = (p.nz + p.tw2 - 1) / p.tw2;
+    P.ny2 = p.ny;
     P.rb = bits_of(P.L - 1) > 0 ? bits_of(P.L - 1) : 1;
     P.ring_cap = ring_cap();
     P.ring_budget = ring_budget(pass);
@@ -1568,61 +1587,40 @@ cudaError_t launch_col(const void *in, void *out, void *gstack, const EdtPlan &p
                     }
                 }
                 const size_t smem = PASS == 2 ? p.smem2 : p.smem3;
-                if (tw == 16) {   // tile numbering of the ring and banded kernels
+                if (tw == 16) {   // 32 bands x 16 columns = 512 threads (two bands per warp)
                     P.nkt = (p.nz + 15) / 16;
                     P.ntiles = (long long)P.nkt * nouter;
                 }
-                // dense scenes: the windowed search first; the banded launch
-                // below then takes the other scenes' tiles and the tiles the
-                // search handed back (decided per scene on the device)
+                // dense scenes first try the windowed search inside the same
+                // kernel (decided per scene on the device)
+                bool ring = false;
                 if constexpr (FW <= 1) {
-                    const int rmin = ring_min_for(p.nx);
                     const int mode3 = PASS == 3 && sp ? sp->p3_mode : 0;
-                    if (sp && sp->fails && ring_enabled() && mode3 != 1 && ring_fits(p, PASS, P.L) &&
-                        tw * P.B <= kColThreads &&
-                        (sp->m_hint < 0 || sp->m_hint >= rmin)) {
+                    if (ring_possible(p, sp) && mode3 != 1 && ring_fits(p, PASS, P.L) && tw * P.B <= kColThreads) {
                         P.mcount = sp->hdr;
                         P.sflag3 = PASS == 3 ? sp->sflag : nullptr;
-                        P.ring_min = rmin;
-                        P.fails = sp->fails;
-                        cudaError_t e = cudaMemsetAsync(sp->fails, 0, 8, st);
-                        if (e != cudaSuccess) return e;
-                        const size_t rsm = (size_t)P.rows_alloc * tw * 4 + 16;
-                        auto rk = tw == 16 ? k_column_ring<PASS, SCAT, 16> : k_column_ring<PASS, SCAT, 32>;
-                        e = allow_smem(rk);
-                        if (e != cudaSuccess) return e;
-                        rk<<<(unsigned)P.ntiles, dim3(tw, P.B), rsm, st>>>(
-                            m, reinterpret_cast<const typename C::InT *>(in), reinterpret_cast<typename C::OutT *>(out),
-                            P, sc);
-                        e = cudaGetLastError();
-                        if (e != cudaSuccess) return e;
+                        P.ring_min = ring_min_for(p.nx);
+                        P.rhdr = sp->fails;   // zeroed by launch_pass1 of this call
+                        ring = true;
                     }
-                }
-                if (tw == 16) {
-                    // 32 bands x 16 columns = 512 threads (two bands per warp)
-                    auto kern = cmp ? k_column_tma<PASS, FW, SCAT, true, kColThreads, 16>
-                                    : k_column_tma<PASS, FW, SCAT, false, kColThreads, 16>;
-                    cudaError_t e = allow_smem(kern);
-                    if (e != cudaSuccess) return e;
-                    const unsigned g16 = P.fails ? (unsigned)std::min<long long>(P.ntiles, 3LL * num_sms())
-                                                 : (unsigned)P.ntiles;
-                    kern<<<g16, dim3(16, P.B), smem, st>>>(
-                        m, m1, reinterpret_cast<const typename C::InT *>(in),
-                        reinterpret_cast<typename C::OutT *>(out), P, sc);
-                    return cudaGetLastError();
                 }
                 // long columns (L > 512) with 32-column tiles take 32 bands =
                 // 1024 threads: one CTA per SM (VX_NARROW_TILES=0)
-                auto kern = P.B > kMaxBands
-                                ? (cmp ? k_column_tma<PASS, FW, SCAT, true, 1024> : k_column_tma<PASS, FW, SCAT, false, 1024>)
-                                : (cmp ? k_column_tma<PASS, FW, SCAT, true, kColThreads>
-                                       : k_column_tma<PASS, FW, SCAT, false, kColThreads>);
+                auto kern = tw == 16
+                                ? (ring ? (cmp ? k_column_tma<PASS, FW, SCAT, true, kColThreads, 16, true>
+                                               : k_column_tma<PASS, FW, SCAT, false, kColThreads, 16, true>)
+                                        : (cmp ? k_column_tma<PASS, FW, SCAT, true, kColThreads, 16>
+                                               : k_column_tma<PASS, FW, SCAT, false, kColThreads, 16>))
+                                : P.B > kMaxBands
+                                      ? (cmp ? k_column_tma<PASS, FW, SCAT, true, 1024> : k_column_tma<PASS, FW, SCAT, false, 1024>)
+                                      : (ring ? (cmp ? k_column_tma<PASS, FW, SCAT, true, kColThreads, 32, true>
+                                                     : k_column_tma<PASS, FW, SCAT, false, kColThreads, 32, true>)
+                                              : (cmp ? k_column_tma<PASS, FW, SCAT, true, kColThreads>
+                                                     : k_column_tma<PASS, FW, SCAT, false, kColThreads>));
                 cudaError_t e = allow_smem(kern);
                 if (e != cudaSuccess) return e;
-                const unsigned gb = P.fails ? (unsigned)std::min<long long>(P.ntiles, 3LL * num_sms())
-                                            : (unsigned)P.ntiles;
-                kern<<<gb, block, smem, st>>>(m, m1, reinterpret_cast<const typename C::InT *>(in),
-                                                              reinterpret_cast<typename C::OutT *>(out), P, sc);
+                kern<<<(unsigned)P.ntiles, dim3(tw, P.B), smem, st>>>(m, m1, reinterpret_cast<const typename C::InT *>(in),
+                                                                   reinterpret_cast<typename C::OutT *>(out), P, sc);
                 return cudaGetLastError();
             }
         }
@@ -1784,12 +1782,21 @@ cudaError_t launch_pass1(const uint8_t *occ, int32_t *s1, long long nslices, int
         grid2 = (unsigned)std::min<long long>(grid2, (long long)num_sms() * 8 * VX_P1_WAVES);
     }
     const bool vec = (nz % 4 == 0) && ((uintptr_t)occ % 16 == 0) && ((uintptr_t)s1 % 16 == 0);
-    if (vec && nz <= 128) k_pass1_v4<1, 2><<<grid2, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny, xs, hdr);
-    else if (vec && nz <= 256) k_pass1_v4<2, 2><<<grid2, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny, xs, hdr);
-    else if (vec && nz <= 512 && xs && VX_P1_LPW512 == 2) k_pass1_v4<4, 2><<<grid2, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny, xs, hdr);
-    else if (vec && nz <= 512) k_pass1_v4<4, 1><<<grid, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny, xs, hdr);
-    else if (vec && nz <= 1024) k_pass1_v4<8, 1><<<grid, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny, xs, hdr);
-    else if (vec && nz <= 2048) k_pass1_v4<16, 1><<<grid, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny, xs, hdr);
+    // the windowed search's header (hand-back counts, k-line statistics) starts
+    // at zero for this call; pass 1 counts the empty k-lines into it
+    int *ls = nullptr;
+    if (sp && sp->fails && ring_enabled() &&
+        (sp->m_hint < 0 || sp->m_hint >= ring_min_for((int)(nslices / std::max(sp->nscenes, 1))))) {
+        ls = sp->fails;
+        cudaError_t e = cudaMemsetAsync(ls, 0, 16, st);
+        if (e != cudaSuccess) return e;
+    }
+    if (vec && nz <= 128) k_pass1_v4<1, 2><<<grid2, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny, xs, hdr, ls);
+    else if (vec && nz <= 256) k_pass1_v4<2, 2><<<grid2, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny, xs, hdr, ls);
+    else if (vec && nz <= 512 && xs && VX_P1_LPW512 == 2) k_pass1_v4<4, 2><<<grid2, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny, xs, hdr, ls);
+    else if (vec && nz <= 512) k_pass1_v4<4, 1><<<grid, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny, xs, hdr, ls);
+    else if (vec && nz <= 1024) k_pass1_v4<8, 1><<<grid, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny, xs, hdr, ls);
+    else if (vec && nz <= 2048) k_pass1_v4<16, 1><<<grid, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny, xs, hdr, ls);
     else k_pass1_generic<<<grid, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny);
     return cudaGetLastError();
 }
@@ -1943,6 +1950,10 @@ cudaError_t launch_slice_list(const uint8_t *occ, const EdtPlan &p, const Sparse
 // which pass-3 kernels to launch given a predicted occupied-slice count m
 // (the previous call's, read from SparseRows::m_mirror): mirrors the gates of
 // launch_col.  Any mode is correct for any m; a wrong guess only costs time.
+bool ring_hint_on(const EdtPlan &p, int m) {
+    return ring_enabled() && (m < 0 || m >= ring_min_for(p.nx));
+}
+
 int pass3_mode_hint(const EdtPlan &p, int m) {
     if (m < 0) return 0;
     const long long ntiles = (long long)((p.nz + 31) / 32) * p.ny;
@@ -1958,11 +1969,8 @@ int pass3_mode_hint(const EdtPlan &p, int m) {
     return m <= smax ? 1 : 2;
 }
 
-// hand-back list of the windowed search: [count, spare, tiles of either pass]
-static size_t fail_list_bytes(const EdtPlan &p, int nscenes) {
-    const size_t t2 = (size_t)((p.nz + p.tw2 - 1) / p.tw2) * p.nx, t3 = (size_t)((p.nz + p.tw3 - 1) / p.tw3) * p.ny;
-    return ((2 + std::max(t2, t3) * nscenes) * 4 + 255) / 256 * 256;
-}
+// the windowed search's header (fall-back counts, pass-1 k-line counts)
+static size_t fail_list_bytes(const EdtPlan &, int) { return 256; }
 
 size_t sparse_bytes(const EdtPlan &p, int nscenes) {
     const size_t sx = (size_t)p.nx * nscenes;
@@ -1991,6 +1999,7 @@ SparseRows sparse_rows_at(void *where, const EdtPlan &p, int nscenes) {
     sp.hdr = reinterpret_cast<int *>(b + (sx + 255) / 256 * 256 + (sx * 4 + 255) / 256 * 256);
     sp.fails = reinterpret_cast<int *>(b + (sx + 255) / 256 * 256 + (sx * 4 + 255) / 256 * 256 +
                                        ((size_t)nscenes * 4 + 255) / 256 * 256);
+    sp.nscenes = nscenes;
     return sp;
 }
 

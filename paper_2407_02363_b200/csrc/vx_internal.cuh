@@ -48,7 +48,8 @@ struct SparseRows {
     int *m_mirror = nullptr;  // optional host-mapped copy of hdr[0] (the next call's hint)
     int p3_mode = 0;          // pass 3: 0 both kernels, gated on the device by the
                               // count; 1 one warp per tile only; 2 banded only
-    int *fails = nullptr;     // [2 + tiles] hand-back list of the windowed search
+    int *fails = nullptr;     // windowed search header: fall-back counts, pass-1 k-line counts
+    int nscenes = 1;
     int m_hint = -1;          // predicted count (>= 0: skip the windowed search when sparse)
 };
 
@@ -72,6 +73,7 @@ cudaError_t launch_slice_list(const uint8_t *occ, const EdtPlan &p, const Sparse
                               int nscenes = 1);
 cudaError_t launch_slice_list_only(const EdtPlan &p, const SparseRows &sp, cudaStream_t st);
 int pass3_mode_hint(const EdtPlan &p, int m);   // SparseRows::p3_mode from a predicted count
+bool ring_hint_on(const EdtPlan &p, int m);     // would a call with this predicted count launch the windowed search?
 struct DevCounters;
 // same from a grid's touched list (valid when it covers every occupied voxel)
 cudaError_t launch_slice_list_touched(const int32_t *touched, const DevCounters *ctr, const uint8_t *occ,

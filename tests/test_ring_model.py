@@ -35,15 +35,24 @@ def ring_column(w, valid, cap=64, R=4):
         k0, k1, k2, k3 = g(q0), g(q0 + 1), g(q0 + 2), g(q0 + 3)
         b = [min(k0, k1 + one, k2 + 4 * one, k3 + 9 * one), min(k0 + one, k1, k2 + one, k3 + 4 * one),
              min(k0 + 4 * one, k1 + one, k2, k3 + one), min(k0 + 9 * one, k1 + 4 * one, k2 + one, k3)]
-        o, d3, steps = [one, 4 * one, 9 * one, 16 * one], 7 * one, 0
-        while max(b[0], b[3]) >= o[0] or max(b[1], b[2]) >= o[1]:
-            if steps >= cap:
-                return None
-            kl, kr = g(q0 - 1 - steps), g(q0 + 4 + steps)
-            b = [min(b[i], (kl + o[i]) & M32, (kr + o[3 - i]) & M32) for i in range(4)]
+        o0, o1, o2, o3, d3, steps = one, 4 * one, 9 * one, 16 * one, 9 * one, 0
+        more = max(b[0], b[3]) >= o0 or max(b[1], b[2]) >= o1
+        while more and steps < cap:   # two steps per trip, as the kernel
+            o4 = o3 + d3
             d3 += 2 * one
-            o = [o[1], o[2], o[3], o[3] + d3]
-            steps += 1
+            s = steps + 1
+            kl, kr, kl2, kr2 = g(q0 - s), g(q0 + 3 + s), g(q0 - s - 1), g(q0 + 4 + s)
+            offl, offr = (o0, o1, o2, o3), (o3, o2, o1, o0)
+            offl2, offr2 = (o1, o2, o3, o4), (o4, o3, o2, o1)
+            b = [min(b[i], (kl + offl[i]) & M32, (kr + offr[i]) & M32, (kl2 + offl2[i]) & M32,
+                     (kr2 + offr2[i]) & M32) for i in range(4)]
+            o0, o1, o2 = o2, o3, o4
+            o3 = o4 + d3
+            d3 += 2 * one
+            steps += 2
+            more = max(b[0], b[3]) >= o0 or max(b[1], b[2]) >= o1
+        if more:
+            return None
         out += [v & (one - 1) for v in b][: max(0, min(R, L - q0))]
     return out
 
