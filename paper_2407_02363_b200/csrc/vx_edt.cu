@@ -97,6 +97,9 @@ constexpr int kStreamMaxRows = VX_STREAM_MAX_ROWS;
 #ifndef VX_P1_WAVES
 #define VX_P1_WAVES 1   // pass 1 over occupied slices: persistent CTAs per SM / 8
 #endif
+#ifndef VX_P1_X16
+#define VX_P1_X16 1     // pass 1 with 16 voxels per lane for 256 < nz <= 1024 (nz % 16 == 0)
+#endif
 #ifndef VX_P1_LPW512
 #define VX_P1_LPW512 1  // lines per warp iteration for nz <= 512 (occupied-slice path)
 #endif
@@ -246,6 +249,137 @@ __global__ void __launch_bounds__(256) k_pass1_v4(const uint8_t *__restrict__ oc
         }
         pass1_line<CMAX>(nib[l], dst, nq, lane);
     }
+    }
+    if (linestat) {   // per CTA: two atomics
+        __shared__ int s_cnt[2];
+        if (threadIdx.x == 0) s_cnt[0] = s_cnt[1] = 0;
+        __syncthreads();
+        if (lane == 0 && nseen) {
+            atomicAdd(&s_cnt[0], nempty);
+            atomicAdd(&s_cnt[1], nseen);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0 && s_cnt[1]) {
+            atomicAdd(linestat + 2, s_cnt[0]);
+            atomicAdd(linestat + 3, s_cnt[1]);
+        }
+    }
+}
+
+// Pass 1, 16 voxels per lane (nz % 16 == 0, 256 < nz <= 512 * CH): one
+// 16-byte load per lane and 512-voxel chunk, so a warp reads a 512-voxel line
+// in one instruction.  Per voxel the nearest site before (l) and after (r)
+// comes from a running scan over the lane's 16 voxels, seeded by the nearest
+// site in the lanes before / after (ballot + one shuffle); the answer is l if
+// k - l <= r - k (edt.py:217-224; l + r >= 2k), with missing sides at -/+2^30.
+template <int CH>
+__global__ void __launch_bounds__(256, 6) k_pass1_x16(const uint8_t *__restrict__ occ, int32_t *__restrict__ s1,
+                                                   long long nlines, int nz, const uint8_t *__restrict__ sflag,
+                                                   int ny, const int *__restrict__ xs, const int *__restrict__ hdr,
+                                                   int *__restrict__ linestat) {
+    constexpr int NONE_L = -(1 << 30), NONE_R = 1 << 30;
+    __shared__ int4 s_stage[8][128];   // per warp: one 512-voxel chunk of s1 (2 KB)
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    const unsigned gt = lane == 31 ? 0u : ~((2u << lane) - 1u);
+    int nempty = 0, nseen = 0;
+    const int m = xs ? __ldg(hdr) : 0;
+    const long long total = xs ? (long long)m * ny : nlines;
+    const long long wstep = (long long)gridDim.x * (blockDim.x >> 5);
+    for (long long line = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); line < total;
+         line += wstep) {
+        long long L = line;
+        if (xs) {   // lines of occupied slices, slot-major
+            const uint32_t slot = (uint32_t)line / (uint32_t)ny;
+            L = (long long)__ldg(xs + slot) * ny + (line - (long long)slot * ny);
+        } else if (sflag && !sflag[(uint32_t)line / (uint32_t)ny]) {
+            continue;   // empty slice: nothing downstream reads it (warp-uniform)
+        }
+        const uint4 *src = reinterpret_cast<const uint4 *>(occ + L * nz);
+        uint32_t msk[CH];
+#pragma unroll
+        for (int c = 0; c < CH; ++c) {
+            const int q = c * 32 + lane;   // 16-byte unit
+            uint32_t mm = 0;
+            if (q * 16 < nz) {
+                const uint4 v = __ldcs(src + q);
+                mm = nibble4(v.x) | (nibble4(v.y) << 4) | (nibble4(v.z) << 8) | (nibble4(v.w) << 12);
+            }
+            msk[c] = mm;
+        }
+        ++nseen;
+        unsigned any = 0;
+#pragma unroll
+        for (int c = 0; c < CH; ++c) any |= msk[c];
+        int4 *dst = reinterpret_cast<int4 *>(s1 + L * nz);
+        if (!__any_sync(VX_FULL_MASK, any != 0u)) {   // empty line: no site anywhere (edt.py:212)
+            ++nempty;
+            const int nu = nz >> 2;   // 16-byte units of the line (coalesced rows)
+            for (int j = lane; j < nu; j += 32) dst[j] = make_int4(-1, -1, -1, -1);
+            continue;
+        }
+        int4 *stage = s_stage[threadIdx.x >> 5];
+        // warp-uniform carries: last site before chunk c, first site after it
+        unsigned bal[CH];
+        int lastc[CH], firstc[CH];
+        int run = NONE_L;
+#pragma unroll
+        for (int c = 0; c < CH; ++c) {
+            bal[c] = __ballot_sync(VX_FULL_MASK, msk[c] != 0u);
+            lastc[c] = run;
+            const int hl = bal[c] ? 31 - __clz(bal[c]) : 0;
+            const uint32_t mb = __shfl_sync(VX_FULL_MASK, msk[c], hl);
+            if (bal[c]) run = (c * 32 + hl) * 16 + 31 - __clz(mb);
+        }
+        run = NONE_R;
+#pragma unroll
+        for (int c = CH - 1; c >= 0; --c) {
+            firstc[c] = run;
+            const int ll = bal[c] ? __ffs(bal[c]) - 1 : 0;
+            const uint32_t mb = __shfl_sync(VX_FULL_MASK, msk[c], ll);
+            if (bal[c]) run = (c * 32 + ll) * 16 + __ffs(mb) - 1;
+        }
+#pragma unroll
+        for (int c = 0; c < CH; ++c) {
+            const int q = c * 32 + lane;
+            const int base = q * 16;
+            const uint32_t mm = msk[c];
+            const unsigned pm = bal[c] & lt, nm = bal[c] & gt;
+            const int lp = pm ? 31 - __clz(pm) : 0, ln = nm ? __ffs(nm) - 1 : 0;
+            const uint32_t mbp = __shfl_sync(VX_FULL_MASK, mm, lp);
+            const uint32_t mbn = __shfl_sync(VX_FULL_MASK, mm, ln);
+            int l = pm ? (c * 32 + lp) * 16 + 31 - __clz(mbp) : lastc[c];   // last site < base
+            int r = nm ? (c * 32 + ln) * 16 + __ffs(mbn) - 1 : firstc[c];   // first site > base + 15
+            // backward over the lane's 16 voxels: r runs, l is the last site
+            // <= e in the lane (one FLO) or the carry.  The four 16-byte groups
+            // go through this warp's shared staging (XOR-swizzled 16-byte
+            // units: conflict-free both ways) so that the global stores are
+            // 512-byte coalesced rows (plain stores: pass 2 reads s1 from L2)
+            if (base < nz) {
+#pragma unroll
+                for (int g = 3; g >= 0; --g) {
+                    int o[4];
+#pragma unroll
+                    for (int u = 3; u >= 0; --u) {
+                        const int e = 4 * g + u;
+                        if (mm & (1u << e)) r = base + e;
+                        const uint32_t le = mm & ((2u << e) - 1u);
+                        const int lv = le ? base + 31 - __clz(le) : l;
+                        o[u] = (lv + r >= 2 * (base + e)) ? lv : r;   // ties -> lower k
+                    }
+                    const int j = lane * 4 + g;
+                    stage[j ^ ((j >> 3) & 7)] = make_int4(o[0], o[1], o[2], o[3]);
+                }
+            }
+            __syncwarp();
+            const int nu = min(128, (nz - c * 512) >> 2);   // 16-byte units of this chunk
+#pragma unroll
+            for (int g = 0; g < 4; ++g) {
+                const int j = g * 32 + lane;
+                if (j < nu) dst[c * 128 + j] = stage[j ^ ((j >> 3) & 7)];
+            }
+            __syncwarp();
+        }
     }
     if (linestat) {   // per CTA: two atomics
         __shared__ int s_cnt[2];
@@ -1794,7 +1928,13 @@ cudaError_t launch_pass1(const uint8_t *occ, int32_t *s1, long long nslices, int
     if (vec && nz <= 128) k_pass1_v4<1, 2><<<grid2, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny, xs, hdr, ls);
     else if (vec && nz <= 256) k_pass1_v4<2, 2><<<grid2, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny, xs, hdr, ls);
     else if (vec && nz <= 512 && xs && VX_P1_LPW512 == 2) k_pass1_v4<4, 2><<<grid2, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny, xs, hdr, ls);
+    else if (vec && nz % 16 == 0 && nz <= 512 && VX_P1_X16)   // persistent: 6 CTAs of 8 warps per SM
+        k_pass1_x16<1><<<(unsigned)std::min<long long>(grid, (long long)num_sms() * 6), 256, 0, st>>>(
+            occ, s1, nlines, nz, sflag, ny, xs, hdr, ls);
     else if (vec && nz <= 512) k_pass1_v4<4, 1><<<grid, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny, xs, hdr, ls);
+    else if (vec && nz % 16 == 0 && nz <= 1024 && VX_P1_X16)
+        k_pass1_x16<2><<<(unsigned)std::min<long long>(grid, (long long)num_sms() * 6), 256, 0, st>>>(
+            occ, s1, nlines, nz, sflag, ny, xs, hdr, ls);
     else if (vec && nz <= 1024) k_pass1_v4<8, 1><<<grid, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny, xs, hdr, ls);
     else if (vec && nz <= 2048) k_pass1_v4<16, 1><<<grid, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny, xs, hdr, ls);
     else k_pass1_generic<<<grid, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny);
