@@ -60,6 +60,16 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def bench_config(world: int) -> dict:
+    """The workload both arms run (identical dicts: the driver compares them)."""
+    return {"workload": "512^3 camera tick: sparse reset, desk7 mask stamp (8 links, FK frames per "
+                        "step), 300k-pt depth-camera cloud scatter with robot mask, exact EDT + "
+                        "nearest-site index (env; self map static -> memo), 30 spheres x 2 maps gather",
+            "grid": list(DIMS), "voxel_size": VS, "points": POINTS, "spheres": 30,
+            "parallelism": f"dp{world} (independent scene per rank)",
+            "l2": "inputs larger than L2: one EDT streams 2.8 GB per step"}
+
+
 def desk7():
     from paper_2407_02363_b200.synth import desk7_model
     return desk7_model()
@@ -253,16 +263,123 @@ def run_reference(args, world, rank):
         "n_gpus": args.gpus, "steps": steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
         "data": "synthetic",
-        "config": {"workload": "512^3 camera tick (map update + exact EDT + 30x2 sphere query), "
-                               "CPU oracle port of voxarm edt.py/grids.py/engine.py",
-                   "grid": list(DIMS), "voxel_size": VS, "points": POINTS, "spheres": 30},
+        "config": bench_config(args.gpus),
+        "impl_detail": "oracle/ C port of voxarm edt.py/grids.py/engine.py (OpenMP, all host threads)",
         "edt_gvoxel_s": n / edt / 1e9,
         "stage_ms": {k: 1e3 * statistics.mean(s[k] for s in stages) for k in stages[0]},
         "cpu_baseline": {"value": value, "unit": "Gvoxel/s", "cores": threads, "kind": "port",
                          "sample": f"{steps} full 512^3 camera ticks (300k pts, 8 links, 30 spheres)"},
         "e2e": {"value": value, "unit": "Gvoxel/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if not args.no_cpu_baseline:
+        line["cpu_baseline_reference"] = voxarm_reference(d)
     print(json.dumps(line), flush=True)
+
+
+def voxarm_reference(d, budget_s: float = 90.0):
+    """The genuine reference, timed: voxarm itself (pip-installed from
+    /root/reference into baseline/_ref; numba, NUMBA_NUM_THREADS = host
+    threads) on this box's cores, warmed up.  Two legs:
+      * pba_edt (edt.py:466-484) on the C3 grid, 512^3 Bernoulli(0.02),
+        workers = host threads and workers = 1;
+      * the engine's camera branch (engine.py:234-280) on the headline
+        512^3 tick: clear x3, self/mask insert_voxel_set, insert_point_cloud
+        (k = 0) with the robot mask, occupancy_mask + blake2b + pba_edt of the
+        env map, _site_world for 30 spheres x 2 maps (the static self map's
+        EDT memoised, as the engine's digest memo does).
+    Returns a dict (or {"unavailable": why})."""
+    nthreads = len(os.sched_getaffinity(0))
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "voxarm")):
+        return {"unavailable": "baseline/_ref has no voxarm install"}
+    os.environ["NUMBA_NUM_THREADS"] = str(nthreads)
+    if ref not in sys.path:
+        sys.path.append(ref)
+    try:
+        import hashlib
+
+        import voxarm
+        from voxarm.grids import FilterConfig, PointCloud, VoxelGrid, VoxelSet
+        from paper_2407_02363_b200 import synth
+    except Exception as e:   # numba missing on the box, etc.
+        return {"unavailable": f"voxarm import failed: {e!r}"[:200]}
+    out = {"kind": "reference", "impl": f"voxarm {getattr(voxarm, '__version__', '')} (numba) from baseline/_ref",
+           "cores": nthreads}
+    t_start = time.perf_counter()
+    occ = synth.bernoulli_occupancy(DIMS, 0.02, 0)
+    voxarm.pba_edt(occ[:64, :64, :64], workers=nthreads)   # JIT compile
+    legs = {}
+    for w in (nthreads, 1):
+        if time.perf_counter() - t_start > budget_s / 2:
+            break
+        voxarm.pba_edt(occ, workers=w)   # warm
+        ts = []
+        for _ in range(2):
+            t0 = time.perf_counter()
+            voxarm.pba_edt(occ, workers=w)
+            ts.append(time.perf_counter() - t0)
+            if w == 1:
+                break
+        legs[f"workers_{w}"] = {"ms": 1e3 * min(ts), "gvoxel_s": float(np.prod(DIMS)) / min(ts) / 1e9}
+    out["pba_edt_512^3_bernoulli_0.02"] = legs
+    del occ
+    # the engine's camera branch on the headline tick
+    env = VoxelGrid(DIMS, VS, ORIGIN)
+    selfg = VoxelGrid(DIMS, VS, ORIGIN)
+    mask = VoxelGrid(DIMS, VS, ORIGIN)
+    vsets = [VoxelSet(np.asarray(o, np.float64), VS, ijk) for ijk, o in d["links"]]
+    fields, digests = {}, {}
+
+    def tick(step):
+        pts, frames, centers = scene_inputs(step, 0, d)
+        st = {}
+        t0 = time.perf_counter()
+        env.clear(); selfg.clear(); mask.clear()
+        st["clear"] = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        for li in d["o_links"]:
+            selfg.insert_voxel_set(vsets[li], frames[li])
+        for li in range(len(vsets)):
+            mask.insert_voxel_set(vsets[li], frames[li])
+        env.insert_point_cloud(PointCloud(pts), FilterConfig(k_neighbors=0), robot_mask=mask)
+        st["insert"] = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        for key, grid in (("env", env), ("self", selfg)):
+            o = grid.occupancy_mask()
+            dig = hashlib.blake2b(o.tobytes(), digest_size=16).digest()
+            if digests.get(key) != dig:
+                fields[key] = voxarm.pba_edt(o, voxel_size=VS, workers=nthreads)
+                digests[key] = dig
+        st["edt"] = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        org = np.asarray(ORIGIN, np.float64)
+        dims = np.asarray(DIMS, np.int64)
+        for key in ("env", "self"):   # engine.py:212-221 per sphere
+            for c in centers:
+                idx = np.clip(np.floor((c - org) / VS).astype(np.int64), 0, dims - 1)
+                site = fields[key].site_index(tuple(int(v) for v in idx))
+                if site is not None:
+                    _ = org + (np.asarray(site) + 0.5) * VS
+        st["query"] = time.perf_counter() - t0
+        return st
+
+    tick(0)   # warm (and the self map's one EDT)
+    ts, stages = [], []
+    for step in range(1, 4):
+        if time.perf_counter() - t_start > budget_s:
+            break
+        t0 = time.perf_counter()
+        stages.append(tick(step))
+        ts.append(time.perf_counter() - t0)
+    if ts:
+        t = statistics.mean(ts)
+        out["camera_tick_512^3"] = {
+            "ms_per_step": t * 1e3, "value": float(np.prod(DIMS)) / t / 1e9, "unit": "Gvoxel/s",
+            "ticks": len(ts), "stage_ms": {k: 1e3 * statistics.mean(s_[k] for s_ in stages) for k in stages[0]}}
+        out["value"] = out["camera_tick_512^3"]["value"]
+        out["unit"] = "Gvoxel/s"
+        out["sample"] = f"{len(ts)} headline 512^3 camera ticks after 1 warm-up tick (voxarm's own code)"
+    return out
 
 
 def cpu_baseline_sample(d):
@@ -422,13 +539,7 @@ def run_gpu(args, world, rank, local):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": t_max * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-        "config": {"workload": "512^3 camera tick: sparse reset, desk7 mask stamp (8 links, FK "
-                               "frames per step), 300k-pt depth-camera cloud scatter with robot "
-                               "mask, exact EDT + nearest-site index (env; self map static -> memo), "
-                               "30 spheres x 2 maps gather",
-                   "grid": list(DIMS), "voxel_size": VS, "points": POINTS, "spheres": 30,
-                   "parallelism": f"dp{world} (independent scene per GPU)",
-                   "l2": "inputs larger than L2: one EDT streams 2.8 GB per step"},
+        "config": bench_config(world),
         "edt_gvoxel_s": world * n / edt_t / 1e9 if edt_t > 0 else None,
         "edt_ms": edt_t * 1e3,
         "edt_roofline_frac": (EDT_BYTES_PER_VOXEL * n / edt_t / 1e9) / peak if edt_t > 0 else None,
@@ -458,6 +569,7 @@ def run_gpu(args, world, rank, local):
         line["outlier_filter"] = outlier_timing()
     if not args.no_cpu_baseline and world == 1:
         line["cpu_baseline"] = cpu_baseline_sample(d)
+        line["cpu_baseline_reference"] = voxarm_reference(d)
     print(json.dumps(line), flush=True)
 
 

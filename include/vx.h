@@ -127,6 +127,10 @@ int vx_edt(vx_ctx *ctx, const uint8_t *occ, int nx, int ny, int nz, double voxel
 /* pba_edt(grid.occupancy_mask(threshold)) without leaving the device */
 int vx_edt_grid(vx_grid *g, double threshold, vx_field **out);
 /* line_nearest_sites (edt.py:444-452): pass 1 only, int32 out */
+/* brute_force_edt (edt.py:487-508): exhaustive nearest site per voxel, ties
+ * to the lexicographically smallest -- the reference's own test oracle, run on
+ * the GPU (O(voxels x sites): grids up to ~48^3 as the reference intends). */
+int vx_brute_force_edt(vx_ctx *ctx, const uint8_t *occupancy, int nx, int ny, int nz, vx_field **out);
 int vx_line_nearest_sites(vx_ctx *ctx, const uint8_t *occ, int nx, int ny, int nz,
                           int32_t *s1_out);
 int vx_field_destroy(vx_field *f);

@@ -5,6 +5,7 @@
 #include "vx.h"
 #include "vx_internal.cuh"
 
+#include <algorithm>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -634,6 +635,40 @@ extern "C" int vx_edt_grid(vx_grid *g, double thr, vx_field **out) {
         vx_field_destroy(f);
         return rc;
     }
+    *out = f;
+    return VX_OK;
+}
+
+// brute_force_edt (edt.py:487-508) on the GPU: site compaction in flat-index
+// order, then an exhaustive minimum per voxel with lexicographic ties
+extern "C" int vx_brute_force_edt(vx_ctx *c, const uint8_t *occ, int nx, int ny, int nz, vx_field **out) {
+    if (!c || !occ || !out) return fail(VX_EINVAL, "NULL argument");
+    int rc = check_edt_dims(nx, ny, nz);
+    if (rc) return rc;
+    const size_t n = (size_t)nx * ny * nz;
+    VX_CUDA(c->staging.ensure(n));
+    VX_CUDA(cudaMemcpyAsync(c->staging.p, occ, n, cudaMemcpyHostToDevice, c->stream));
+    const uint8_t *d_occ = (const uint8_t *)c->staging.p;
+    VX_CUDA(c->exp.ensure(occ_scratch_bytes((long long)n)));
+    cudaError_t e = launch_occ_layout(d_occ, (long long)n, c->exp.p, c->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "brute_force_edt (layout)");
+    long long total = 0;
+    VX_CUDA(cudaMemcpyAsync(&total, occ_total_ptr(c->exp.p, (long long)n), 8, cudaMemcpyDeviceToHost, c->stream));
+    VX_CUDA(cudaStreamSynchronize(c->stream));
+    VX_CUDA(c->exp_out.ensure((size_t)std::max(total, 1LL) * 24));
+    if (total) {
+        e = launch_occ_write(d_occ, (long long)n, ny, nz, c->exp.p, (long long *)c->exp_out.p, c->stream);
+        if (e != cudaSuccess) return cuda_fail(e, "brute_force_edt (sites)");
+    }
+    vx_field *f = nullptr;
+    rc = field_new(c, nx, ny, nz, &f);
+    if (rc) return rc;
+    e = launch_brute_force((const long long *)c->exp_out.p, total, nx, ny, nz, f->site, c->stream);
+    if (e != cudaSuccess) {
+        vx_field_destroy(f);
+        return cuda_fail(e, "brute_force_edt");
+    }
+    c->launches += 4;
     *out = f;
     return VX_OK;
 }

@@ -233,6 +233,49 @@ size_t occ_scratch_bytes(long long n) {
 }
 
 // per-chunk counts + scan; the total lands at occ_total_ptr
+// brute_force_edt (edt.py:487-508): per voxel the minimum over every occupied
+// voxel, ties to the lexicographically smallest (the sites arrive in flat-index
+// order from the compaction, and only a strictly smaller distance replaces the
+// current best).  O(N x sites): meant for the reference's test sizes (<= ~48^3).
+// Sites are staged through shared memory in blocks of 1024.
+__global__ void __launch_bounds__(256) k_brute_force(const long long *__restrict__ sites, long long nsites, int nx,
+                                                     int ny, int nz, int32_t *__restrict__ out) {
+    __shared__ int3 s[1024];
+    const long long n = (long long)nx * ny * nz;
+    const long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const int i = (int)(v / ((long long)ny * nz)), j = (int)((v / nz) % ny), k = (int)(v % nz);
+    long long best = -1;
+    long long bl = -1;
+    for (long long b0 = 0; b0 < nsites; b0 += 1024) {
+        const int nb = (int)min(1024LL, nsites - b0);
+        __syncthreads();
+        for (int t = threadIdx.x; t < nb; t += blockDim.x) {
+            const long long *q = sites + 3 * (b0 + t);
+            s[t] = make_int3((int)q[0], (int)q[1], (int)q[2]);
+        }
+        __syncthreads();
+        if (v < n) {
+            for (int t = 0; t < nb; ++t) {
+                const long long di = i - s[t].x, dj = j - s[t].y, dk = k - s[t].z;
+                const long long d = di * di + dj * dj + dk * dk;
+                if (best < 0 || d < best) {
+                    best = d;
+                    bl = ((long long)s[t].x * ny + s[t].y) * nz + s[t].z;
+                }
+            }
+        }
+    }
+    if (v < n) out[v] = (int32_t)bl;   // -1 (NO_SITE) when there is no site
+}
+
+cudaError_t launch_brute_force(const long long *sites, long long nsites, int nx, int ny, int nz, int32_t *out,
+                               cudaStream_t st) {
+    const long long n = (long long)nx * ny * nz;
+    if (n == 0) return cudaSuccess;
+    k_brute_force<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(sites, nsites, nx, ny, nz, out);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_occ_layout(const uint8_t *occ, long long n, void *scratch, cudaStream_t st) {
     const long long nb = (n + kOccChunk - 1) / kOccChunk;
     long long *cnt = (long long *)scratch, *off = cnt + nb;

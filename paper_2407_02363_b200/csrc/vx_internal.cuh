@@ -178,6 +178,9 @@ cudaError_t launch_occ_layout(const uint8_t *occ, long long n, void *scratch, cu
 const long long *occ_total_ptr(void *scratch, long long n);
 cudaError_t launch_occ_write(const uint8_t *occ, long long n, int ny, int nz, const void *scratch,
                              long long *out, cudaStream_t st);
+// brute_force_edt: sites (K,3) int64 in flat-index order -> site (lexicographic ties)
+cudaError_t launch_brute_force(const long long *sites, long long nsites, int nx, int ny, int nz, int32_t *out,
+                               cudaStream_t st);
 
 int num_sms();
 

@@ -7,6 +7,9 @@ Same names, signatures, results and exceptions as the reference:
   query_nearest_site  edt.py:148-161
   BandConfig / default_band_config edt.py:32-52 (validated; the GPU band
   layout is chosen per shape -- the result is band-invariant, test_edt.py:88-95)
+  brute_force_edt     edt.py:487-508  -> vx_brute_force_edt (exhaustive, on the GPU)
+  ProximateStack / proximate_sites_1d  edt.py:55-100 (host API helpers for
+  one column's surviving sites; the GPU passes never call them)
 The site array is bit-identical to the reference's (lexicographic
 minimum nearest site).
 """
@@ -203,6 +206,55 @@ def line_nearest_sites(occupancy: np.ndarray, m1: int = 1, workers: int | None =
     _lib.check(_lib.load().vx_line_nearest_sites(ctx.handle, _lib.ptr(occ), *occ.shape,
                                                  _lib.ptr(s1)))
     return s1
+
+
+def brute_force_edt(occupancy: np.ndarray, voxel_size: float = 1.0) -> DistanceField:
+    """edt.py:487-508: exhaustive nearest site per voxel, ties to the
+    lexicographically smallest site -- the reference's test oracle, computed
+    on the GPU (vx_brute_force_edt).  Meant for grids up to about 48^3."""
+    occ = _as_occ(occupancy)
+    if occ.size == 0:
+        return DistanceField(np.empty(occ.shape, np.int32), voxel_size)
+    ctx = _lib.default_context()
+    h = ctypes.c_void_p()
+    _lib.check(_lib.load().vx_brute_force_edt(ctx.handle, _lib.ptr(occ), *occ.shape, ctypes.byref(h)))
+    return DistanceField(None, voxel_size, _handle=h, _dims=occ.shape, _ctx=ctx)
+
+
+@dataclass
+class ProximateStack:
+    """edt.py:55-67: the surviving (sweep_coord, site) entries of one column,
+    in sweep order; each owns a non-empty 1D Voronoi interval."""
+
+    entries: list
+
+    def sites(self) -> list:
+        return [site for _, site in self.entries]
+
+
+def _dominated(y_a: int, w_a: int, y_b: int, w_b: int, y_c: int, w_c: int) -> bool:
+    """edt.py:70-73: b on or above the segment a-c of (y, w + y^2), which the
+    GPU column kernels test in the same integer form."""
+    return (w_b + y_b * y_b - w_a - y_a * y_a) * (y_c - y_b) >= (w_c + y_c * y_c - w_b - y_b * y_b) * (y_b - y_a)
+
+
+def proximate_sites_1d(sites, column: int) -> ProximateStack:
+    """edt.py:76-100: prune an ordered (sweep_coord, site) list to the sites
+    whose interval on `column` is non-empty; site = (x, y), weight
+    (x - column)^2, exact Python integers.  Raises ValueError unless the
+    sweep coordinates strictly increase."""
+    kept: list = []   # (coord, weight, site)
+    prev = None
+    for coord, site in sites:
+        c = int(coord)
+        if prev is not None and c <= prev:
+            raise ValueError("sites must be strictly increasing in sweep coordinate")
+        prev = c
+        w = (int(site[0]) - int(column)) ** 2
+        while len(kept) >= 2 and _dominated(kept[-2][0], kept[-2][1], kept[-1][0], kept[-1][1], c, w):
+            kept.pop()
+        kept.append((c, w, site))
+    return ProximateStack(entries=[(c, site) for c, _, site in kept])
 
 
 def pba_edt(occupancy: np.ndarray, band_cfg: BandConfig | None = None, voxel_size: float = 1.0,

@@ -303,3 +303,20 @@ def statistical_outlier_filter(points: np.ndarray, k_neighbors: int,
                                            pts.shape[0], int(k_neighbors), float(std_multiplier),
                                            _lib.ptr(keep), ctypes.byref(removed)))
     return pts[keep.view(np.bool_)]
+
+
+def load_point_cloud(path) -> PointCloud:
+    """grids.py:243-256: a text cloud, one "x y z" per line, '#' comments and
+    blank lines skipped; ValueError on a short line (host file I/O)."""
+    rows = []
+    with open(path) as fh:
+        for raw in fh:
+            text = raw.strip()
+            if not text or text.startswith("#"):
+                continue
+            fields = text.split()
+            if len(fields) < 3:
+                raise ValueError(f"bad point line: {text!r}")
+            rows.append([float(v) for v in fields[:3]])
+    return PointCloud(points=np.asarray(rows, dtype=np.float64).reshape(-1, 3))
+

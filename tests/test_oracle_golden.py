@@ -190,3 +190,34 @@ def test_bench512_tick0_vs_reference():
     lin, world, _ = O.site_world(site, bench.VS, bench.ORIGIN, centers)
     for q, w in enumerate(g["env_world"]):
         assert (lin[q] == -1) if w is None else (world[q].tolist() == w)
+
+
+def test_shim_proximate_stack_matches_oracle_and_reference_cases():
+    """The shim's host API mirror of edt.py:55-100 (ProximateStack,
+    proximate_sites_1d) against the oracle restatement (itself pinned on the
+    reference's cases, test_proximate_stack_cases) and its ValueError."""
+    from paper_2407_02363_b200 import ProximateStack, proximate_sites_1d
+    rng = np.random.default_rng(9)
+    for _ in range(300):
+        n = int(rng.integers(0, 12))
+        coords = np.sort(rng.choice(40, size=n, replace=False))
+        sites = [(int(c), (int(rng.integers(-20, 20)), int(c))) for c in coords]
+        col = int(rng.integers(-10, 10))
+        got = proximate_sites_1d(sites, col)
+        assert isinstance(got, ProximateStack)
+        assert got.sites() == O.proximate_sites_1d(sites, col)
+        assert [c for c, _ in got.entries] == [c for c, s in sites if s in got.sites()]
+    with pytest.raises(ValueError):
+        proximate_sites_1d([(3, (0, 0)), (3, (1, 0))], 0)
+
+
+def test_shim_load_point_cloud(tmp_path):
+    """grids.py:243-256: comments and blank lines skipped, short lines rejected."""
+    from paper_2407_02363_b200 import load_point_cloud
+    f = tmp_path / "c.txt"
+    f.write_text("# cloud\n0.5 1 2\n\n -1e-3 4 5.25 extra\n")
+    pc = load_point_cloud(f)
+    assert pc.points.tolist() == [[0.5, 1.0, 2.0], [-1e-3, 4.0, 5.25]]
+    f.write_text("1 2\n")
+    with pytest.raises(ValueError):
+        load_point_cloud(f)
