@@ -131,6 +131,25 @@ int vx_edt_grid(vx_grid *g, double threshold, vx_field **out);
  * to the lexicographically smallest -- the reference's own test oracle, run on
  * the GPU (O(voxels x sites): grids up to ~48^3 as the reference intends). */
 int vx_brute_force_edt(vx_ctx *ctx, const uint8_t *occupancy, int nx, int ny, int nz, vx_field **out);
+/* A field to be filled by vx_edt_grid_into (pooled: no allocation per EDT). */
+int vx_field_create(vx_ctx *ctx, int nx, int ny, int nz, vx_field **out);
+/* pba_edt(grid.occupancy_mask(threshold)) into `field` (same dims), on the
+ * device: the occupancy never leaves it.  Replaces the engine's per-tick
+ * occupancy_mask -> pba_edt round trip (engine.py:259-268). */
+int vx_edt_grid_into(vx_grid *g, double threshold, vx_field *field);
+/* The engine's memo key (engine.py:259-268: blake2b of the occupancy mask)
+ * as a device digest of the occupied-voxel set: O(touched voxels) when the
+ * grid's touched list covers its occupancy, else one pass over it; equal
+ * occupancy gives equal digests.  16 bytes cross the bus. */
+int vx_grid_occupancy_digest(vx_grid *g, double threshold, uint64_t digest[2]);
+/* _site_world (engine.py:212-221) for s centres on field a and (optionally)
+ * field b in one round trip: lin/world/dist hold a's s results, then b's. */
+int vx_fields_site_world(vx_field *a, vx_field *b, const double origin[3], double voxel_size,
+                         const double *centers, int64_t s, int32_t *site_lin, double *site_world,
+                         double *dist);
+/* Bytes this context's ABI calls have copied host->device [0] and
+ * device->host [1] since it was created (evidence: no per-tick grid copy). */
+int vx_ctx_transfer_bytes(const vx_ctx *ctx, int64_t out[2]);
 int vx_line_nearest_sites(vx_ctx *ctx, const uint8_t *occ, int nx, int ny, int nz,
                           int32_t *s1_out);
 int vx_field_destroy(vx_field *f);

@@ -36,7 +36,8 @@ EXPORTS = (
     "vx_cycle_destroy", "vx_cycle_step", "vx_cycle_wait", "vx_cycle_fields", "vx_cycle_grids",
     "vx_cycle_profile", "vx_cycle_phase_ms", "vx_cycle_step_device", "vx_edt_pass12_scatter",
     "vx_cycle_use_graph", "vx_grid_insert_points_ex", "vx_outlier_mask", "vx_cycle_set_avoidance",
-    "vx_cycle_set_joint_frames", "vx_cycle_rows", "vx_cycle_prefetch", "vx_cycle_step_staged", "vx_cycle_info", "vx_brute_force_edt", "vx_grid_occupied_voxels", "vx_field_sq_distance",
+    "vx_cycle_set_joint_frames", "vx_cycle_rows", "vx_cycle_prefetch", "vx_cycle_step_staged", "vx_cycle_info", "vx_brute_force_edt", "vx_field_create", "vx_edt_grid_into",
+    "vx_grid_occupancy_digest", "vx_fields_site_world", "vx_ctx_transfer_bytes", "vx_grid_occupied_voxels", "vx_field_sq_distance",
     "vx_field_dump_squared",
 )
 CYCLE_PHASES = ("h2d", "self_map", "mask_stamp_reset", "scatter", "edt_pass1", "edt_pass2",
@@ -125,6 +126,11 @@ def load():
             "vx_cycle_prefetch": ([P, P, i64, P], i32),
             "vx_cycle_info": ([P, P], i32),
             "vx_brute_force_edt": ([P, P, i32, i32, i32, PP], i32),
+            "vx_field_create": ([P, i32, i32, i32, PP], i32),
+            "vx_edt_grid_into": ([P, f64, P], i32),
+            "vx_grid_occupancy_digest": ([P, f64, P], i32),
+            "vx_fields_site_world": ([P, P, P, f64, P, i64, P, P, P], i32),
+            "vx_ctx_transfer_bytes": ([P, P], i32),
             "vx_cycle_step_staged": ([P, ctypes.c_uint64, P, f32, f64, P, i32, i32], i32),
             "vx_grid_occupied_voxels": ([P, f64, P, i64, ctypes.POINTER(ctypes.c_int64)], i32),
             "vx_field_sq_distance": ([P, P, i32], i32),

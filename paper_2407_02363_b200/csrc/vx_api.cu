@@ -74,6 +74,7 @@ struct vx_ctx {
     cudaStream_t stream = nullptr;
     DevBuf scratch, staging, staging2, temp, outl, exp, exp_out;
     long long launches = 0;
+    long long h2d = 0, d2h = 0;   // bytes moved by the ABI's own copies (vx_ctx_transfer_bytes)
 };
 
 struct vx_grid {
@@ -319,6 +320,7 @@ extern "C" int vx_grid_insert_points(vx_grid *g, const double *xyz, int64_t n, f
     VX_CUDA(c->staging.ensure((size_t)n * 3 * sizeof(double)));
     VX_CUDA(cudaMemcpyAsync(c->staging.p, xyz, (size_t)n * 3 * sizeof(double), cudaMemcpyHostToDevice,
                             c->stream));
+    c->h2d += (long long)n * 24;
     int rc = insert_device(g, (const double *)c->staging.p, n, nullptr, hit, thr, mask);
     if (rc) return rc;
     vx_insert_stats s;
@@ -391,6 +393,7 @@ extern "C" int vx_grid_insert_points_ex(vx_grid *g, const double *xyz, int64_t n
     vx_ctx *c = g->ctx;
     VX_CUDA(c->staging.ensure((size_t)n * 24));
     VX_CUDA(cudaMemcpyAsync(c->staging.p, xyz, (size_t)n * 24, cudaMemcpyHostToDevice, c->stream));
+    c->h2d += (long long)n * 24;
     uint8_t *keep = nullptr;
     long long rem = 0;
     int rc = outlier_device(c, (const double *)c->staging.p, n, k_neighbors, std_multiplier, &keep, &rem);
@@ -466,6 +469,7 @@ extern "C" int vx_grid_insert_voxel_sets(vx_grid *g, int nsets, const int32_t *c
     VX_CUDA(c->staging2.ensure(host.size()));
     unsigned char *d = (unsigned char *)c->staging2.p;
     VX_CUDA(cudaMemcpyAsync(d, host.data(), host.size(), cudaMemcpyHostToDevice, c->stream));
+    c->h2d += (long long)host.size();
     int rc = stamp_sets(g, nsets, (const int32_t *)d, (const int64_t *)(d + b_ijk),
                         (const double *)(d + b_ijk + b_off), (const double *)(d + b_ijk + b_off + b_org),
                         T ? (const double *)(d + b_ijk + b_off + b_org + b_vs) : nullptr, value, total);
@@ -482,6 +486,7 @@ extern "C" int vx_grid_insert_voxel_sets(vx_grid *g, int nsets, const int32_t *c
 extern "C" int vx_grid_read_cells(vx_grid *g, float *out) {
     if (!g || !out) return fail(VX_EINVAL, "NULL argument");
     VX_CUDA(cudaMemcpyAsync(out, g->cells, g->n * sizeof(float), cudaMemcpyDeviceToHost, g->ctx->stream));
+    g->ctx->d2h += g->n * 4;
     VX_CUDA(cudaStreamSynchronize(g->ctx->stream));
     return VX_OK;
 }
@@ -491,6 +496,7 @@ extern "C" int vx_grid_write_cells(vx_grid *g, const float *in) {
     bool oor = false;
     for (long long v = 0; v < g->n && !oor; ++v) oor = !(in[v] >= kLMin && in[v] <= kLMax);
     VX_CUDA(cudaMemcpyAsync(g->cells, in, g->n * sizeof(float), cudaMemcpyHostToDevice, g->ctx->stream));
+    g->ctx->h2d += g->n * 4;
     cudaError_t e = launch_occupancy(g->cells, g->occ, g->n, kOccThr, g->ctx->stream);
     if (e != cudaSuccess) return cuda_fail(e, "occupancy");
     g->ctx->launches += 1;
@@ -523,6 +529,7 @@ extern "C" int vx_grid_occupancy(vx_grid *g, double thr, uint8_t *out) {
     int rc = grid_occ_device(g, thr, &d);
     if (rc) return rc;
     VX_CUDA(cudaMemcpyAsync(out, d, g->n, cudaMemcpyDeviceToHost, g->ctx->stream));
+    g->ctx->d2h += g->n;
     VX_CUDA(cudaStreamSynchronize(g->ctx->stream));
     return VX_OK;
 }
@@ -610,6 +617,7 @@ extern "C" int vx_edt(vx_ctx *c, const uint8_t *occ, int nx, int ny, int nz, dou
     const size_t n = (size_t)nx * ny * nz;
     VX_CUDA(c->staging.ensure(n));
     VX_CUDA(cudaMemcpyAsync(c->staging.p, occ, n, cudaMemcpyHostToDevice, c->stream));
+    c->h2d += (long long)n;
     vx_field *f = nullptr;
     rc = field_new(c, nx, ny, nz, &f);
     if (rc) return rc;
@@ -673,6 +681,94 @@ extern "C" int vx_brute_force_edt(vx_ctx *c, const uint8_t *occ, int nx, int ny,
     return VX_OK;
 }
 
+extern "C" int vx_field_create(vx_ctx *c, int nx, int ny, int nz, vx_field **out) {
+    if (!c || !out) return fail(VX_EINVAL, "NULL argument");
+    int rc = check_edt_dims(nx, ny, nz);
+    if (rc) return rc;
+    return field_new(c, nx, ny, nz, out);
+}
+
+// pba_edt(grid.occupancy_mask(thr)) into an existing field (a pooled buffer:
+// no allocation per call); the data never leaves the device
+extern "C" int vx_edt_grid_into(vx_grid *g, double thr, vx_field *f) {
+    if (!g || !f) return fail(VX_EINVAL, "NULL argument");
+    if (f->nx != g->g.nx || f->ny != g->g.ny || f->nz != g->g.nz || !f->owned)
+        return fail(VX_EINVAL, "field dims (%d, %d, %d) do not match the grid (%d, %d, %d)", f->nx, f->ny, f->nz,
+                    g->g.nx, g->g.ny, g->g.nz);
+    const uint8_t *d = nullptr;
+    int rc = grid_occ_device(g, thr, &d);
+    if (rc) return rc;
+    return edt_run(g->ctx, d, g->g.nx, g->g.ny, g->g.nz, 1, f->site, nullptr, 0);
+}
+
+// engine.py:259-268's memo key without the N-byte copy: a digest of the
+// occupied-voxel set at `thr` computed on the device (O(touched voxels) when
+// the grid's touched list covers its occupancy); 16 bytes come back.  Equal
+// occupancy => equal digest; unequal occupancy collides with probability
+// ~2^-64, as a 128-bit blake2b of the mask does at ~2^-128.
+extern "C" int vx_grid_occupancy_digest(vx_grid *g, double thr, uint64_t digest[2]) {
+    if (!g || !digest) return fail(VX_EINVAL, "NULL argument");
+    vx_ctx *c = g->ctx;
+    const uint8_t *d = nullptr;
+    int rc = grid_occ_device(g, thr, &d);
+    if (rc) return rc;
+    const bool list = d == g->occ && g->sparse_ok;
+    // the sums go to a buffer that does not hold the occupancy (temp does when
+    // thr is not the cached 0.5)
+    DevBuf &accb = d == (const uint8_t *)c->temp.p ? c->exp : c->temp;
+    VX_CUDA(accb.ensure(64));
+    unsigned long long *acc = reinterpret_cast<unsigned long long *>(accb.p);
+    cudaError_t e = launch_occ_digest(d, g->n, g->touched, g->ctr, list, acc, c->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "occupancy digest");
+    c->launches += 1;
+    unsigned long long h[3];
+    VX_CUDA(cudaMemcpyAsync(h, acc, sizeof h, cudaMemcpyDeviceToHost, c->stream));
+    c->d2h += sizeof h;
+    VX_CUDA(cudaStreamSynchronize(c->stream));
+    digest[0] = h[0] ^ (h[2] * 0x9E3779B97F4A7C15ull);
+    digest[1] = h[1] + h[2];
+    return VX_OK;
+}
+
+// _site_world (engine.py:212-221) for s centres on up to two fields in one
+// round trip: outputs [field a's s results, field b's s results]
+extern "C" int vx_fields_site_world(vx_field *a, vx_field *b, const double origin[3], double vs,
+                                    const double *centers, int64_t s, int32_t *lin, double *world, double *dist) {
+    if (!a || !origin || (s > 0 && (!centers || !lin || !world || !dist))) return fail(VX_EINVAL, "NULL argument");
+    if (b && (b->nx != a->nx || b->ny != a->ny || b->nz != a->nz)) return fail(VX_EINVAL, "field dims differ");
+    if (s <= 0) return VX_OK;
+    vx_ctx *c = a->ctx;
+    const int nf = b ? 2 : 1;
+    const size_t bc = (size_t)s * 3 * sizeof(double);
+    const size_t bl = ((size_t)nf * s * 4 + 15) & ~(size_t)15;
+    VX_CUDA(c->temp.ensure(bc + bl + nf * bc + (size_t)nf * s * 8));
+    unsigned char *d = (unsigned char *)c->temp.p;
+    VX_CUDA(cudaMemcpyAsync(d, centers, bc, cudaMemcpyHostToDevice, c->stream));
+    c->h2d += (long long)bc;
+    GridGeom g{a->nx, a->ny, a->nz, vs, origin[0], origin[1], origin[2]};
+    int32_t *dl = (int32_t *)(d + bc);
+    double *dw = (double *)(d + bc + bl), *dd = (double *)(d + bc + bl + nf * bc);
+    for (int q = 0; q < nf; ++q) {
+        cudaError_t e = launch_site_world((q ? b : a)->site, g, (const double *)d, (int)s, dl + q * s,
+                                          dw + (size_t)q * s * 3, dd + (size_t)q * s, c->stream);
+        if (e != cudaSuccess) return cuda_fail(e, "site_world");
+        c->launches += 1;
+    }
+    VX_CUDA(cudaMemcpyAsync(lin, dl, (size_t)nf * s * 4, cudaMemcpyDeviceToHost, c->stream));
+    VX_CUDA(cudaMemcpyAsync(world, dw, (size_t)nf * bc, cudaMemcpyDeviceToHost, c->stream));
+    VX_CUDA(cudaMemcpyAsync(dist, dd, (size_t)nf * s * 8, cudaMemcpyDeviceToHost, c->stream));
+    c->d2h += (long long)nf * s * (4 + 24 + 8);
+    VX_CUDA(cudaStreamSynchronize(c->stream));
+    return VX_OK;
+}
+
+extern "C" int vx_ctx_transfer_bytes(const vx_ctx *c, int64_t out[2]) {
+    if (!c || !out) return fail(VX_EINVAL, "NULL argument");
+    out[0] = c->h2d;
+    out[1] = c->d2h;
+    return VX_OK;
+}
+
 extern "C" int vx_line_nearest_sites(vx_ctx *c, const uint8_t *occ, int nx, int ny, int nz, int32_t *s1) {
     if (!c || !occ || !s1) return fail(VX_EINVAL, "NULL argument");
     int rc = check_edt_dims(nx, ny, nz);
@@ -709,6 +805,7 @@ extern "C" int vx_field_read_site(vx_field *f, int32_t *out) {
     if (!f || !out) return fail(VX_EINVAL, "NULL argument");
     const size_t n = (size_t)f->nx * f->ny * f->nz;
     VX_CUDA(cudaMemcpyAsync(out, f->site, n * 4, cudaMemcpyDeviceToHost, f->ctx->stream));
+    f->ctx->d2h += (long long)n * 4;
     VX_CUDA(cudaStreamSynchronize(f->ctx->stream));
     return VX_OK;
 }
@@ -764,6 +861,7 @@ extern "C" int vx_field_site_at(vx_field *f, int64_t i, int64_t j, int64_t k, in
                     (long long)j, (long long)k, f->nx, f->ny, f->nz);
     const size_t off = ((size_t)i * f->ny + j) * f->nz + k;
     VX_CUDA(cudaMemcpyAsync(out, f->site + off, 4, cudaMemcpyDeviceToHost, f->ctx->stream));
+    f->ctx->d2h += 4;
     VX_CUDA(cudaStreamSynchronize(f->ctx->stream));
     return VX_OK;
 }

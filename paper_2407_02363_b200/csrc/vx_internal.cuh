@@ -141,6 +141,10 @@ cudaError_t launch_stamp(const int32_t *ijk, const int64_t *offsets, int nsets,
                          int capacity, int64_t total, cudaStream_t st);
 cudaError_t launch_occupancy(const float *cells, uint8_t *out, int64_t n, float thr,
                              cudaStream_t st);
+// occupancy-set digest {sum mix1, sum mix2, count}: from the touched list when
+// use_list (and it did not overflow), else over all n voxels
+cudaError_t launch_occ_digest(const uint8_t *occ, int64_t n, const int32_t *touched, const DevCounters *ctr,
+                              bool use_list, unsigned long long *out, cudaStream_t st);
 
 // ---- statistical outlier filter (grids.py:224-240) ---------------------------
 size_t outlier_scratch_bytes(long long n);

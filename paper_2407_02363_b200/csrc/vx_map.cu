@@ -404,6 +404,55 @@ __global__ void k_occupancy(const float *__restrict__ cells, uint8_t *__restrict
         out[v] = cells[v] > thr ? 1 : 0;                              // grids.py:207-208
 }
 
+// Occupancy-set digest (the engine's memo key, engine.py:259-268, without the
+// N-byte copy and blake2b): two order-independent 64-bit sums of mixed voxel
+// indices plus the count, so any traversal order gives the same digest.  From
+// the touched list (unique first touches since the last clear) when it covers
+// every occupied voxel: O(K); otherwise over the whole occupancy array.
+__device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ void digest_add(unsigned long long *out, bool occ, long long v) {
+    unsigned long long a = occ ? mix64((unsigned long long)v) : 0ull;
+    unsigned long long b = occ ? mix64((unsigned long long)v ^ 0xD6E8FEB86659FD93ull) : 0ull;
+    unsigned c = occ ? 1u : 0u;
+    for (int d = 16; d; d >>= 1) {   // warp sums, one atomic per warp and word
+        a += __shfl_xor_sync(VX_FULL_MASK, a, d);
+        b += __shfl_xor_sync(VX_FULL_MASK, b, d);
+        c += __shfl_xor_sync(VX_FULL_MASK, c, d);
+    }
+    if ((threadIdx.x & 31) == 0 && c) {
+        atomicAdd(out, a);
+        atomicAdd(out + 1, b);
+        atomicAdd(out + 2, (unsigned long long)c);
+    }
+}
+
+__global__ void k_occ_digest(const uint8_t *__restrict__ occ, long long n, const int32_t *__restrict__ touched,
+                             const DevCounters *__restrict__ ctr, int use_list, unsigned long long *__restrict__ out) {
+    const long long nth = (long long)gridDim.x * blockDim.x;
+    const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (use_list && !ctr->overflow) {
+        const long long cnt = ctr->touched;
+        const long long trips = (cnt + nth - 1) / nth;   // uniform trip count: full warps
+        for (long long it = 0; it < trips; ++it) {
+            const long long t = tid + it * nth;
+            const int v = t < cnt ? touched[t] : -1;
+            digest_add(out, v >= 0 && occ[v] != 0, v);
+        }
+    } else {
+        const long long trips = (n + nth - 1) / nth;
+        for (long long it = 0; it < trips; ++it) {
+            const long long v = tid + it * nth;
+            digest_add(out, v < n && occ[v] != 0, v);
+        }
+    }
+}
+
 unsigned grid_for(long long work, int block) {
     long long g = (work + block - 1) / block;
     const long long cap = (long long)num_sms() * 8;
@@ -472,6 +521,14 @@ cudaError_t launch_stamp(const int32_t *ijk, const int64_t *offsets, int nsets,
                                                       total);
     else
         k_stamp_commit<<<1, 1, 0, st>>>(ctr, capacity);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_occ_digest(const uint8_t *occ, int64_t n, const int32_t *touched, const DevCounters *ctr,
+                              bool use_list, unsigned long long *out, cudaStream_t st) {
+    cudaError_t e = cudaMemsetAsync(out, 0, 3 * sizeof(unsigned long long), st);
+    if (e != cudaSuccess) return e;
+    k_occ_digest<<<(unsigned)(num_sms() * 4), 256, 0, st>>>(occ, n, touched, ctr, use_list ? 1 : 0, out);
     return cudaGetLastError();
 }
 

@@ -87,3 +87,46 @@ def test_engine_fields_are_device_fields():
         for _ in range(8):
             eng.step()
         assert eng._fields["self"] is f0
+
+
+def test_engine_memo_contract_static_scene():
+    """test_sim.py:125-133 under the bridge: with the occupancy unchanged the
+    engine keeps both field objects (the device digest memo agrees with the
+    reference's blake2b memo)."""
+    from voxarm.engine import SimEngine
+    sc = _scenario(OBSTACLES[0], duration=0.5)
+    with voxarm_bridge.installed():
+        eng = SimEngine(sc)
+        for _ in range(8):
+            eng.step()
+        env0, self0 = eng._fields["env"], eng._fields["self"]
+        for _ in range(10):
+            eng.step()
+        assert eng._fields["env"] is env0
+        assert eng._fields["self"] is self0
+
+
+def test_engine_path_moves_no_grid_per_tick():
+    """The bridged camera tick never copies a grid, an occupancy mask or a
+    site array across the bus: per camera tick the host->device bytes are the
+    cloud plus the link voxel sets, and device->host per control tick is the
+    batched sphere lookup (both maps, ~1.5 KB) plus two 16-byte digests and
+    insert stats on camera ticks."""
+    from voxarm.engine import SimEngine
+    sc = _scenario(OBSTACLES[1], duration=0.5)
+    n = int(np.prod(sc.grid.dims))
+    with voxarm_bridge.installed():
+        eng = SimEngine(sc)
+        eng.step()   # first camera tick: allocations, self map EDT
+        h0, d0 = voxarm_bridge.transfer_bytes()
+        cams = 0
+        for _ in range(40):
+            rec = eng.step()
+            cams += rec.timings["insert"] > 0.0
+        h1, d1 = voxarm_bridge.transfer_bytes()
+    assert cams >= 5
+    points = sum(m.cloud_points(0.0).shape[0] for m in eng.movers)
+    link_bytes = sum(v.indices.nbytes for v in eng.link_voxels)
+    assert (h1 - h0) / cams < points * 24 + 2 * link_bytes + 64 * 1024
+    assert (d1 - d0) / 40 < 4096, (d1 - d0) / 40   # per control tick: the sphere lookups
+    assert (d1 - d0) < n    # not even one occupancy mask over all 40 ticks
