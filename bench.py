@@ -28,6 +28,7 @@ cpu_baseline  the oracle port of the reference path (oracle/, OpenMP on all
 from __future__ import annotations
 
 import argparse
+import contextlib
 import ctypes
 import json
 import os
@@ -382,6 +383,60 @@ def voxarm_reference(d, budget_s: float = 90.0):
     return out
 
 
+def engine_bridge_timing(ticks_small: int = 240, ticks_big: int = 40):
+    """voxarm's own closed-loop engine (SimEngine.step, engine.py:225-322,
+    from baseline/_ref) with the device-resident bridge installed, on the
+    shipped walker_crossing scenario at its 96^3 grid and re-gridded to the
+    512^3 headline grid; the CPU engine beside it at 96^3.  Per control tick:
+    mean ms, camera-tick mean ms, and the bytes libvx moved per tick (no grid,
+    mask or site array crosses the bus)."""
+    import dataclasses
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "voxarm")):
+        return {"unavailable": "baseline/_ref has no voxarm install"}
+    if ref not in sys.path:
+        sys.path.append(ref)
+    try:
+        from voxarm.engine import SimEngine
+        from voxarm.scenario import GridSpec, load_scenario, shipped_scenario_path
+        from paper_2407_02363_b200 import voxarm_bridge
+    except Exception as e:
+        return {"unavailable": f"voxarm import failed: {e!r}"[:200]}
+    base = load_scenario(shipped_scenario_path("walker_crossing"))
+    big = dataclasses.replace(base, grid=GridSpec(dims=DIMS, voxel_size=VS, origin=ORIGIN))
+
+    def run(sc, ticks, gpu):
+        ctx = voxarm_bridge.installed() if gpu else contextlib.nullcontext()
+        with ctx:
+            eng = SimEngine(sc)
+            for _ in range(3):
+                eng.step()
+            b0 = voxarm_bridge.transfer_bytes() if gpu else (0, 0)
+            ts, cam = [], []
+            for _ in range(ticks):
+                t0 = time.perf_counter()
+                rec = eng.step()
+                dt = time.perf_counter() - t0
+                ts.append(dt)
+                if rec.timings["insert"] > 0.0:
+                    cam.append(dt)
+            b1 = voxarm_bridge.transfer_bytes() if gpu else (0, 0)
+        out = {"ticks": ticks, "ms_per_tick": 1e3 * statistics.mean(ts),
+               "camera_tick_ms": 1e3 * statistics.mean(cam) if cam else None, "camera_ticks": len(cam)}
+        if gpu:
+            out["h2d_bytes_per_tick"] = (b1[0] - b0[0]) / ticks
+            out["d2h_bytes_per_tick"] = (b1[1] - b0[1]) / ticks
+        return out
+
+    res = {"scenario": "walker_crossing (shipped), default k=8 outlier filter",
+           "96^3_gpu_bridge": run(base, ticks_small, True),
+           "96^3_cpu_engine": run(base, min(ticks_small, 60), False),
+           "512^3_gpu_bridge": run(big, ticks_big, True)}
+    n96 = float(np.prod(base.grid.dims))
+    res["96^3_grid_bytes"] = n96
+    return res
+
+
 def cpu_baseline_sample(d):
     """Bounded CPU sample (~10-30 s): two full 512^3 ticks after one warm-up."""
     from oracle import oracle as O
@@ -567,6 +622,7 @@ def run_gpu(args, world, rank, local):
         line["edt_sweep"] = edt_sweep(ctx, stream)
         line["small_configs"] = small_configs(d)
         line["outlier_filter"] = outlier_timing()
+        line["engine_bridge"] = engine_bridge_timing()
     if not args.no_cpu_baseline and world == 1:
         line["cpu_baseline"] = cpu_baseline_sample(d)
         line["cpu_baseline_reference"] = voxarm_reference(d)
