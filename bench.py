@@ -838,8 +838,10 @@ def c4_batch_camera(ctx, stream, rank: int, world: int):
 
 def c5_slab(rank: int, world: int):
     """Config C5: one 1024^3 grid slab-decomposed across the ranks (i-slabs;
-    passes 1-2 local, the pass-2 epilogue writes the j-slab transpose into the
-    NCCL all-to-all send blocks, pass 3 on the received j-slab).  Strong
+    passes 1-2 local in 4 slice groups, the pass-2 epilogue writes the j-slab
+    transpose into per-destination send blocks, each group's NCCL send/recv
+    queued on the library stream behind its pass 2 so it overlaps the next
+    group's compute, pass 3 on the received j-slab).  Strong
     scaling: the whole grid is fixed, time = max over ranks of the device time
     of one SlabEDT call.  Bernoulli(0.02) occupancy generated on the device."""
     import torch
@@ -866,7 +868,10 @@ def c5_slab(rank: int, world: int):
     torch.cuda.empty_cache()
     return {"ranks": world, "ms": t * 1e3, "gvoxel_s": n ** 3 / t / 1e9,
             "hbm_frac_per_gpu": EDT_BYTES_PER_VOXEL * n ** 3 / world / t / 1e9 / peaks()[0],
-            "exchange": "nccl all_to_all_single (pass-2 epilogue writes the send blocks)",
+            "exchange": "nccl grouped send/recv per slice group, stream-ordered (pass-2 epilogue writes the "
+                        "send blocks; own rows straight into the receive buffer)",
+            "nvlink_bytes_per_rank": 4 * (i1 - i0) * (n - (even_split(n, world)[rank + 1] - even_split(n, world)[rank])) * n
+            if world > 1 else 0,
             "occupancy": "Bernoulli(0.02), generated on the device", "scaling": "strong (one 1024^3 grid)"}
 
 

@@ -147,6 +147,12 @@ int vx_grid_occupancy_digest(vx_grid *g, double threshold, uint64_t digest[2]);
 int vx_fields_site_world(vx_field *a, vx_field *b, const double origin[3], double voxel_size,
                          const double *centers, int64_t s, int32_t *site_lin, double *site_world,
                          double *dist);
+/* Slab mode: _site_world on this rank's j-slab d_site (device, (nx, nyl, nz),
+ * rows j0 .. j0+nyl-1, global flat site indices); centres whose clipped row
+ * lies outside the slab return site_lin -2 (another rank answers them). */
+int vx_site_world_slab(vx_ctx *ctx, const int32_t *d_site, int nx, int ny, int nz, int j0, int nyl,
+                       const double origin[3], double voxel_size, const double *centers, int64_t s,
+                       int32_t *site_lin, double *site_world, double *dist);
 /* Bytes this context's ABI calls have copied host->device [0] and
  * device->host [1] since it was created (evidence: no per-tick grid copy). */
 int vx_ctx_transfer_bytes(const vx_ctx *ctx, int64_t out[2]);

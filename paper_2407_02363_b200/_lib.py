@@ -37,7 +37,7 @@ EXPORTS = (
     "vx_cycle_profile", "vx_cycle_phase_ms", "vx_cycle_step_device", "vx_edt_pass12_scatter",
     "vx_cycle_use_graph", "vx_grid_insert_points_ex", "vx_outlier_mask", "vx_cycle_set_avoidance",
     "vx_cycle_set_joint_frames", "vx_cycle_rows", "vx_cycle_prefetch", "vx_cycle_step_staged", "vx_cycle_info", "vx_brute_force_edt", "vx_field_create", "vx_edt_grid_into",
-    "vx_grid_occupancy_digest", "vx_fields_site_world", "vx_ctx_transfer_bytes", "vx_grid_occupied_voxels", "vx_field_sq_distance",
+    "vx_grid_occupancy_digest", "vx_fields_site_world", "vx_ctx_transfer_bytes", "vx_site_world_slab", "vx_grid_occupied_voxels", "vx_field_sq_distance",
     "vx_field_dump_squared",
 )
 CYCLE_PHASES = ("h2d", "self_map", "mask_stamp_reset", "scatter", "edt_pass1", "edt_pass2",
@@ -131,6 +131,7 @@ def load():
             "vx_grid_occupancy_digest": ([P, f64, P], i32),
             "vx_fields_site_world": ([P, P, P, f64, P, i64, P, P, P], i32),
             "vx_ctx_transfer_bytes": ([P, P], i32),
+            "vx_site_world_slab": ([P, P, i32, i32, i32, i32, i32, P, f64, P, i64, P, P, P], i32),
             "vx_cycle_step_staged": ([P, ctypes.c_uint64, P, f32, f64, P, i32, i32], i32),
             "vx_grid_occupied_voxels": ([P, f64, P, i64, ctypes.POINTER(ctypes.c_int64)], i32),
             "vx_field_sq_distance": ([P, P, i32], i32),

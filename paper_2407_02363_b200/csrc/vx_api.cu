@@ -73,6 +73,7 @@ struct vx_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
     DevBuf scratch, staging, staging2, temp, outl, exp, exp_out;
+    DevBuf slabhdr;   // slab mode: the windowed search's header (pass-1 counts, fall-backs)
     long long launches = 0;
     long long h2d = 0, d2h = 0;   // bytes moved by the ABI's own copies (vx_ctx_transfer_bytes)
 };
@@ -142,6 +143,7 @@ extern "C" int vx_ctx_destroy(vx_ctx *c) {
     c->exp.release();
     c->exp_out.release();
     c->outl.release();
+    c->slabhdr.release();
     cudaStreamDestroy(c->stream);
     delete c;
     return VX_OK;
@@ -762,6 +764,35 @@ extern "C" int vx_fields_site_world(vx_field *a, vx_field *b, const double origi
     return VX_OK;
 }
 
+// slab mode: _site_world on this rank's j-slab (device site
+// array (nx, nyl, nz) holding rows j0.., global flat indices); centres whose
+// row another rank holds come back with lin -2 (the caller gathers)
+extern "C" int vx_site_world_slab(vx_ctx *c, const int32_t *d_site, int nx, int ny, int nz, int j0, int nyl,
+                                  const double origin[3], double vs, const double *centers, int64_t s,
+                                  int32_t *lin, double *world, double *dist) {
+    if (!c || !d_site || !origin || (s > 0 && (!centers || !lin || !world || !dist)))
+        return fail(VX_EINVAL, "NULL argument");
+    if (j0 < 0 || nyl < 0 || j0 + nyl > ny) return fail(VX_EINVAL, "bad j-slab [%d, %d) of %d", j0, j0 + nyl, ny);
+    if (s <= 0) return VX_OK;
+    const size_t bc = (size_t)s * 3 * sizeof(double);
+    const size_t bl = ((size_t)s * 4 + 15) & ~(size_t)15;
+    VX_CUDA(c->temp.ensure(bc + bl + bc + (size_t)s * 8));
+    unsigned char *d = (unsigned char *)c->temp.p;
+    VX_CUDA(cudaMemcpyAsync(d, centers, bc, cudaMemcpyHostToDevice, c->stream));
+    c->h2d += (long long)bc;
+    GridGeom g{nx, ny, nz, vs, origin[0], origin[1], origin[2]};
+    cudaError_t e = launch_site_world(d_site, g, (const double *)d, (int)s, (int32_t *)(d + bc),
+                                      (double *)(d + bc + bl), (double *)(d + bc + bl + bc), c->stream, j0, nyl);
+    if (e != cudaSuccess) return cuda_fail(e, "site_world_slab");
+    c->launches += 1;
+    VX_CUDA(cudaMemcpyAsync(lin, d + bc, (size_t)s * 4, cudaMemcpyDeviceToHost, c->stream));
+    VX_CUDA(cudaMemcpyAsync(world, d + bc + bl, bc, cudaMemcpyDeviceToHost, c->stream));
+    VX_CUDA(cudaMemcpyAsync(dist, d + bc + bl + bc, (size_t)s * 8, cudaMemcpyDeviceToHost, c->stream));
+    c->d2h += (long long)s * 36;
+    VX_CUDA(cudaStreamSynchronize(c->stream));
+    return VX_OK;
+}
+
 extern "C" int vx_ctx_transfer_bytes(const vx_ctx *c, int64_t out[2]) {
     if (!c || !out) return fail(VX_EINVAL, "NULL argument");
     out[0] = c->h2d;
@@ -927,6 +958,20 @@ extern "C" int vx_edt_pass12_device(vx_ctx *c, const uint8_t *d_occ, int nx, int
     return VX_OK;
 }
 
+// slab-mode calls have no occupied-slice list, only the search header
+static int slab_rows(vx_ctx *c, SparseRows *sp) {
+    if (!c->slabhdr.p) {
+        VX_CUDA(c->slabhdr.ensure(256));
+        VX_CUDA(cudaMemsetAsync(c->slabhdr.p, 0, c->slabhdr.n, c->stream));
+    }
+    *sp = SparseRows{};
+    sp->sflag = nullptr;
+    sp->xs = nullptr;
+    sp->hdr = nullptr;
+    sp->fails = static_cast<int *>(c->slabhdr.p);
+    return VX_OK;
+}
+
 extern "C" int vx_edt_pass12_scatter(vx_ctx *c, const uint8_t *d_occ, int nx, int ny, int nz, int nxl,
                                      int nranks, void *const *dst, const int *j_starts, long long x_base,
                                      void *d_scratch, size_t scratch_bytes) {
@@ -956,9 +1001,11 @@ extern "C" int vx_edt_pass12_scatter(vx_ctx *c, const uint8_t *d_occ, int nx, in
         return fail(VX_EINVAL, "scratch too small");
     }
     int32_t *s1 = (int32_t *)d_scratch;
-    cudaError_t e = launch_pass1(d_occ, s1, nxl, ny, nz, c->stream);
+    SparseRows sp;
+    if ((rc = slab_rows(c, &sp))) return rc;
+    cudaError_t e = launch_pass1(d_occ, s1, nxl, ny, nz, c->stream, &sp);
     if (e != cudaSuccess) return cuda_fail(e, "pass12_scatter (pass 1)");
-    e = launch_pass2_scatter(s1, tab, (unsigned char *)d_scratch + s1b, p, nxl, c->stream);
+    e = launch_pass2_scatter(s1, tab, (unsigned char *)d_scratch + s1b, p, nxl, c->stream, &sp);
     if (e != cudaSuccess) return cuda_fail(e, "pass12_scatter (pass 2)");
     c->launches += 2;
     return VX_OK;
@@ -979,7 +1026,9 @@ extern "C" int vx_edt_pass3_device(vx_ctx *c, const void *d_s2, int nx, int ny, 
             return fail(VX_EINVAL, "scratch too small");
         }
     }
-    cudaError_t e = launch_pass3(d_s2, d_site, d_scratch, p, 1, j0, nyl, c->stream);
+    SparseRows sp;
+    if ((rc = slab_rows(c, &sp))) return rc;
+    cudaError_t e = launch_pass3(d_s2, d_site, d_scratch, p, 1, j0, nyl, c->stream, &sp);
     if (e != cudaSuccess) return cuda_fail(e, "pass3");
     c->launches += 1;
     return VX_OK;

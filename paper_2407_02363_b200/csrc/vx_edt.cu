@@ -1947,8 +1947,8 @@ cudaError_t launch_pass2(const int32_t *s1, void *s2, void *gstack, const EdtPla
 }
 
 cudaError_t launch_pass2_scatter(const int32_t *s1, const ScatterTab &sc, void *gstack, const EdtPlan &p,
-                                 long long nslices, cudaStream_t st) {
-    return dispatch_col<2, true>(s1, nullptr, gstack, p, nslices, p.ny, 0, sc, st);
+                                 long long nslices, cudaStream_t st, const SparseRows *sp) {
+    return dispatch_col<2, true>(s1, nullptr, gstack, p, nslices, p.ny, 0, sc, st, sp);
 }
 
 cudaError_t launch_pass3(const void *s2, int32_t *site, void *gstack, const EdtPlan &p,

@@ -61,7 +61,7 @@ cudaError_t launch_pass2(const int32_t *s1, void *s2, void *gstack, const EdtPla
                          long long nslices, cudaStream_t st, const SparseRows *sp = nullptr);
 // pass 2 with the fused exchange epilogue (slab mode)
 cudaError_t launch_pass2_scatter(const int32_t *s1, const ScatterTab &sc, void *gstack, const EdtPlan &p,
-                                 long long nslices, cudaStream_t st);
+                                 long long nslices, cudaStream_t st, const SparseRows *sp = nullptr);
 // pass 3 over nscenes buffers of shape (nx, nyl, nz) holding global rows
 // j0 .. j0+nyl-1 (slab mode); site codes are global flat indices.
 cudaError_t launch_pass3(const void *s2, int32_t *site, void *gstack, const EdtPlan &p,
@@ -155,9 +155,11 @@ cudaError_t outlier_filter(const double *pts, long long n, int k, double stdm, c
                            size_t scratch_bytes, cudaStream_t st);
 
 // ---- query ----------------------------------------------------------------
+// j0 / nyl: site holds rows j0 .. j0+nyl-1 (slab mode; -1 = all rows);
+// centres in other rows get lin -2
 cudaError_t launch_site_world(const int32_t *site, GridGeom g, const double *centers,
                               int s, int32_t *out_lin, double *out_world, double *out_dist,
-                              cudaStream_t st);
+                              cudaStream_t st, int j0 = 0, int nyl = -1);
 
 // the tick's gather on both maps + the packed host-mapped result block
 cudaError_t launch_gather_pack(const int32_t *site_env, const int32_t *site_self, GridGeom g,

@@ -27,14 +27,24 @@ __device__ __forceinline__ long long clip_index(double f, int n) {
     return v;
 }
 
+// j0 / nyl: the site array holds rows j0 .. j0 + nyl - 1 of every slice (a
+// slab-mode j-slab, global flat indices); a centre whose row is not held
+// gets lin = -2 (another rank owns it)
 __device__ __forceinline__ void site_world_one(const int32_t *__restrict__ site, const GridGeom &g,
                                                const double *__restrict__ centers, int q, int32_t *out_lin,
-                                               double *out_world, double *out_dist) {
+                                               double *out_world, double *out_dist, int j0 = 0, int nyl = -1) {
     const double cx = centers[3 * q], cy = centers[3 * q + 1], cz = centers[3 * q + 2];
     const long long i = clip_index(floor(__ddiv_rn(__dsub_rn(cx, g.ox), g.vs)), g.nx);
     const long long j = clip_index(floor(__ddiv_rn(__dsub_rn(cy, g.oy), g.vs)), g.ny);
     const long long k = clip_index(floor(__ddiv_rn(__dsub_rn(cz, g.oz), g.vs)), g.nz);
-    const int32_t lin = site[(i * g.ny + j) * g.nz + k];
+    if (nyl < 0) nyl = g.ny;
+    if (j < j0 || j >= (long long)j0 + nyl) {
+        out_lin[q] = -2;
+        out_world[3 * q] = out_world[3 * q + 1] = out_world[3 * q + 2] = CUDART_NAN;
+        out_dist[q] = CUDART_NAN;
+        return;
+    }
+    const int32_t lin = site[(i * nyl + (j - j0)) * g.nz + k];
     out_lin[q] = lin;
     if (lin < 0) {
         out_world[3 * q] = out_world[3 * q + 1] = out_world[3 * q + 2] = CUDART_NAN;
@@ -56,10 +66,10 @@ __device__ __forceinline__ void site_world_one(const int32_t *__restrict__ site,
 __global__ void k_site_world(const int32_t *__restrict__ site, GridGeom g,
                              const double *__restrict__ centers, int s,
                              int32_t *__restrict__ out_lin, double *__restrict__ out_world,
-                             double *__restrict__ out_dist) {
+                             double *__restrict__ out_dist, int j0, int nyl) {
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= s) return;
-    site_world_one(site, g, centers, q, out_lin, out_world, out_dist);
+    site_world_one(site, g, centers, q, out_lin, out_world, out_dist, j0, nyl);
 }
 
 // the camera tick's gather: both maps in one launch (row r = map * s +
@@ -101,9 +111,9 @@ cudaError_t launch_gather_pack(const int32_t *site_env, const int32_t *site_self
 
 cudaError_t launch_site_world(const int32_t *site, GridGeom g, const double *centers, int s,
                               int32_t *out_lin, double *out_world, double *out_dist,
-                              cudaStream_t st) {
+                              cudaStream_t st, int j0, int nyl) {
     if (s <= 0) return cudaSuccess;
-    k_site_world<<<(s + 127) / 128, 128, 0, st>>>(site, g, centers, s, out_lin, out_world, out_dist);
+    k_site_world<<<(s + 127) / 128, 128, 0, st>>>(site, g, centers, s, out_lin, out_world, out_dist, j0, nyl);
     return cudaGetLastError();
 }
 

@@ -7,16 +7,23 @@ and 2 (along j) are local to a slab (edt.py:168-317 never mix slices).  Pass 3
 are transposed from i-slabs to j-slabs: rank q receives rows j in
 [j0_q, j1_q) of every slice, i.e. a (nx, nyl_q, nz) array, and runs pass 3
 on it with global coordinates.  The result stays j-sliced (no transpose
-back): rank q holds site[:, j0_q:j1_q, :] with global flat indices.
+back): rank q holds site[:, j0_q:j1_q, :] with global flat indices.  Sphere
+queries (engine.py:212-221) go to the rank that owns a centre's row j
+(site_world: every rank answers its rows, one small all-gather).
 
 The exchange is fused into pass 2's epilogue (vx_edt_pass12_scatter): each
-code row is stored straight to its destination, so there is no separate pack
-pass.  Two transports:
-  * "nccl": the destination is this rank's all-to-all send block for q, and one
-    NCCL all_to_all_single over NVLink moves the blocks (the baseline);
-  * "p2p":  the destination is rank q's receive buffer itself, mapped into this
-    process over NVLink (torch symmetric memory); a barrier replaces the
-    collective, and the transfer overlaps pass-2 compute tile by tile.
+code row is stored straight to its destination, so there is no pack pass.
+Rows a rank keeps are stored into its own receive buffer.  Two transports:
+  * "nccl": the destinations are this rank's send blocks, and NCCL
+    send/recv moves them.  The slab is processed in `chunks` slice groups:
+    chunk c's sends and receives are issued (grouped, on the library stream,
+    no host synchronisation) as soon as its pass 2 is queued, so NVLink
+    carries chunk c while pass 2 computes chunk c+1; pass 3 waits on the
+    receives on the same stream;
+  * "p2p":  the destinations are the peers' receive buffers themselves,
+    mapped into this process over NVLink (torch symmetric memory); the
+    transfer overlaps pass-2 compute tile by tile and a barrier on the
+    library stream replaces the collective.
 Bytes crossing NVLink per rank: 4 B x nxl x (ny - nyl) x nz each way.
 """
 
@@ -61,6 +68,20 @@ class CudaBackend:
             self.ctx.handle, ctypes.c_void_p(s2_jslab.data_ptr()), nx, ny, nz, int(j0), nyl,
             ctypes.c_void_p(site_jslab.data_ptr()), None, 0))
 
+    def site_world_slab(self, site_jslab, dims, j0: int, centers, origin, voxel_size: float):
+        nx, ny, nz = dims
+        c = np.ascontiguousarray(centers, np.float64).reshape(-1, 3)
+        s = c.shape[0]
+        lin = np.empty(s, np.int32)
+        world = np.empty((s, 3), np.float64)
+        dist = np.empty(s, np.float64)
+        org = np.ascontiguousarray(origin, np.float64).reshape(3)
+        _lib.check(self.L.vx_site_world_slab(
+            self.ctx.handle, ctypes.c_void_p(site_jslab.data_ptr()), nx, ny, nz, int(j0),
+            int(site_jslab.shape[1]), _lib.ptr(org), float(voxel_size), _lib.ptr(c), s,
+            _lib.ptr(lin), _lib.ptr(world), _lib.ptr(dist)))
+        return lin, world, dist
+
     def stream(self):
         import torch
         return torch.cuda.ExternalStream(self.ctx.stream_handle())
@@ -77,9 +98,11 @@ class SlabEDT:
     """Exact EDT of a (nx, ny, nz) grid held as i-slabs by the ranks of a
     torch.distributed group.  Call with this rank's occupancy slab
     (uint8, (i1-i0, ny, nz)); returns its j-slab of the site array (int32,
-    (nx, j1-j0, nz), global flat indices)."""
+    (nx, j1-j0, nz), global flat indices), ordered before later work on the
+    caller's current stream."""
 
-    def __init__(self, dims, group=None, exchange: str = "nccl", backend=None, device=None):
+    def __init__(self, dims, group=None, exchange: str = "nccl", backend=None, device=None,
+                 chunks: int | None = None):
         import torch
         import torch.distributed as dist
         self.dims = tuple(int(d) for d in dims)
@@ -101,27 +124,28 @@ class SlabEDT:
         r = self.rank
         self.nxl = self.i_starts[r + 1] - self.i_starts[r]
         self.nyl = self.j_starts[r + 1] - self.j_starts[r]
+        # slice groups of the pipelined exchange (the same split rule on every rank)
+        self.chunks = max(1, int(chunks if chunks is not None else (4 if self.world > 1 else 1)))
+        self.c_starts = [even_split(self.i_starts[q + 1] - self.i_starts[q], self.chunks)
+                         for q in range(self.world)]
         # receive buffer (this rank's pass-3 input) and send blocks
         self.recv = torch.empty((nx, self.nyl, nz), dtype=torch.int32, device=self.device)
         self.site = torch.empty((nx, self.nyl, nz), dtype=torch.int32, device=self.device)
         self._symm = None
         if exchange == "nccl":
-            self.send = torch.empty(self.nxl * ny * nz, dtype=torch.int32, device=self.device)
-            self.in_splits = [self.nxl * (self.j_starts[q + 1] - self.j_starts[q]) * nz
-                              for q in range(self.world)]
-            self.out_splits = [(self.i_starts[q + 1] - self.i_starts[q]) * self.nyl * nz
-                               for q in range(self.world)]
+            # chunk-major send blocks: chunk c, destination q -> [slices of c][nyl_q][nz]
+            self.send = torch.empty(max(1, self.nxl * ny * nz), dtype=torch.int32, device=self.device)
         else:
             self._setup_p2p()
 
     # -- p2p transport: peers' receive buffers mapped over NVLink --------------
     def _setup_p2p(self):
         import torch
+        import torch.distributed as dist
         import torch.distributed._symmetric_memory as symm_mem
         nx, ny, nz = self.dims
         maxl = max(self.j_starts[q + 1] - self.j_starts[q] for q in range(self.world))
         buf = symm_mem.empty(nx * maxl * nz, dtype=torch.int32, device=self.device)
-        import torch.distributed as dist
         hdl = symm_mem.rendezvous(buf, self.group if self.group is not None else dist.group.WORLD)
         self._symm = (buf, hdl)
         self.recv = buf[: nx * self.nyl * nz].view(nx, self.nyl, nz)
@@ -131,47 +155,119 @@ class SlabEDT:
             peer = hdl.get_buffer(q, (nx * nyl_q * nz,), torch.int32)
             self.peer_ptrs.append(peer.data_ptr())
 
-    def destinations(self):
-        """(dst pointers, x_base) for this rank's pass-2 epilogue."""
+    def _send_block(self, c: int, q: int):
+        """(offset, count) of chunk c's block for destination q in self.send."""
+        ny, nz = self.dims[1], self.dims[2]
+        cs = self.c_starts[self.rank]
+        n_c = cs[c + 1] - cs[c]
+        return cs[c] * ny * nz + n_c * self.j_starts[q] * nz, n_c * (self.j_starts[q + 1] - self.j_starts[q]) * nz
+
+    def destinations(self, c: int = 0):
+        """(dst pointers, x_base) of chunk c's pass-2 epilogue: send blocks
+        (nccl) or peer receive buffers (p2p); this rank's own rows always go
+        straight into its receive buffer."""
         nz = self.dims[2]
-        if self.exchange == "nccl":
-            base = self.send.data_ptr()
-            ptrs = [base + 4 * self.nxl * self.j_starts[q] * nz for q in range(self.world)]
+        r = self.rank
+        x0 = self.i_starts[r] + self.c_starts[r][c]
+        if self.exchange == "p2p":
+            ptrs = [p + 4 * x0 * (self.j_starts[q + 1] - self.j_starts[q]) * nz
+                    for q, p in enumerate(self.peer_ptrs)]
             return ptrs, 0
-        return self.peer_ptrs, self.i_starts[self.rank]
+        own = self.recv.data_ptr() + 4 * x0 * self.nyl * nz
+        base = self.send.data_ptr()
+        return [own if q == r else base + 4 * self._send_block(c, q)[0] for q in range(self.world)], 0
+
+    def _exchange_ops(self, c: int):
+        """Chunk c's NCCL sends (this rank's rows for q) and receives (q's
+        chunk-c slices of this rank's rows, straight into recv)."""
+        import torch.distributed as dist
+        nz = self.dims[2]
+        ops = []
+        for q in range(self.world):
+            if q == self.rank:
+                continue
+            off, cnt = self._send_block(c, q)
+            if cnt:
+                ops.append(dist.P2POp(dist.isend, self.send[off:off + cnt], q, self.group))
+            cq = self.c_starts[q]
+            x0, x1 = self.i_starts[q] + cq[c], self.i_starts[q] + cq[c + 1]
+            if (x1 - x0) * self.nyl * nz:
+                ops.append(dist.P2POp(dist.irecv, self.recv[x0:x1].view(-1), q, self.group))
+        return ops
 
     def __call__(self, occ_slab):
+        import contextlib
+
         import torch
         import torch.distributed as dist
         if tuple(occ_slab.shape) != (self.nxl, self.dims[1], self.dims[2]):
             raise ValueError(f"rank {self.rank} expects a slab of shape "
                              f"{(self.nxl, self.dims[1], self.dims[2])}")
-        ptrs, x_base = self.destinations()
-        if self.exchange == "p2p":
-            # every peer is done reading its receive buffer (the previous
-            # call's pass 3) before anyone's pass-2 epilogue writes into it;
-            # the barrier kernel runs on the library stream, so it is ordered
-            # after this rank's pass 3 and before its pass 2
-            with torch.cuda.stream(self.backend.stream()):
+        cuda = self.device.type == "cuda"
+        lib = self.backend.stream() if cuda else None
+        caller = torch.cuda.current_stream(self.device) if cuda else None
+        if cuda:   # the occupancy was produced on the caller's stream
+            lib.wait_stream(caller)
+        with torch.cuda.stream(lib) if cuda else contextlib.nullcontext():
+            if self.exchange == "p2p":
+                # every peer is done reading its receive buffer (the previous
+                # call's pass 3) before anyone's pass-2 epilogue writes into it
                 self._symm[1].barrier()
-        self.backend.pass12_scatter(occ_slab, self.dims, ptrs, self.j_starts, x_base)
-        if self.exchange == "nccl":
-            self.backend.synchronize()
-            if self.world > 1:
-                dist.all_to_all_single(self.recv.view(-1), self.send, self.out_splits,
-                                       self.in_splits, group=self.group)
+                ptrs, x_base = self.destinations(0)
+                self.backend.pass12_scatter(occ_slab, self.dims, ptrs, self.j_starts, x_base)
+                self._symm[1].barrier()   # the peers' NVLink stores have landed
             else:
-                self.recv.view(-1).copy_(self.send)
-            self.backend.synchronize()
+                reqs = []
+                cs = self.c_starts[self.rank]
+                for c in range(self.chunks):
+                    if cs[c + 1] > cs[c]:
+                        ptrs, x_base = self.destinations(c)
+                        self.backend.pass12_scatter(occ_slab[cs[c]:cs[c + 1]], self.dims, ptrs,
+                                                    self.j_starts, x_base)
+                    if self.world > 1:
+                        ops = self._exchange_ops(c)
+                        if ops:   # queued behind chunk c's pass 2 on this stream
+                            reqs += dist.batch_isend_irecv(ops)
+                for rq in reqs:   # the library stream waits for the transfers
+                    rq.wait()
+            self.backend.pass3(self.recv, self.site, self.dims, self.j_starts[self.rank])
+        if cuda:
+            caller.wait_stream(lib)
         else:
-            # the peers' NVLink stores into this rank's buffer have landed
-            # once every rank's pass 2 is past this barrier; pass 3 is queued
-            # behind it on the same (library) stream
-            with torch.cuda.stream(self.backend.stream()):
-                self._symm[1].barrier()
-        self.backend.pass3(self.recv, self.site, self.dims, self.j_starts[self.rank])
-        self.backend.synchronize()
+            self.backend.synchronize()
         return self.site
+
+    def site_world(self, centers, origin, voxel_size: float):
+        """_site_world (engine.py:212-221) plus the tasks.py:102-104 distance
+        for every centre on the j-sliced field: each rank answers the centres
+        whose clipped row j it holds (vx_site_world_slab), one all-gather of
+        (S, 5) values picks the owner's answer.  Returns (lin int32 (S,),
+        world (S,3), dist (S,)) on every rank, as engine.site_world does on a
+        whole field (lin -1 / NaN / inf where there is no site)."""
+        import torch
+        import torch.distributed as dist
+        if self.device.type == "cuda":
+            torch.cuda.current_stream(self.device).synchronize()
+        lin, world, dist_ = self.backend.site_world_slab(self.site, self.dims, self.j_starts[self.rank],
+                                                         centers, origin, voxel_size)
+        mine = np.concatenate([lin.astype(np.float64)[:, None], world, dist_[:, None]], axis=1)
+        if self.world == 1:
+            allv = [mine]
+        else:
+            t = torch.from_numpy(np.ascontiguousarray(mine)).to(self.device)
+            parts = [torch.empty_like(t) for _ in range(self.world)]
+            dist.all_gather(parts, t, group=self.group)
+            allv = [p_.cpu().numpy() for p_ in parts]
+        s = lin.shape[0]
+        out_lin = np.full(s, -2, np.int32)
+        out_world = np.empty((s, 3), np.float64)
+        out_dist = np.empty(s, np.float64)
+        for v in allv:
+            own = v[:, 0] != -2
+            out_lin[own] = v[own, 0].astype(np.int32)
+            out_world[own] = v[own, 1:4]
+            out_dist[own] = v[own, 4]
+        return out_lin, out_world, out_dist
 
 
 def emulate_ranks(occ, world: int, exchange: str = "p2p", backend=None):

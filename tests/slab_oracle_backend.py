@@ -48,5 +48,31 @@ class OracleBackend:
         s2z = np.where(valid, c & ((1 << zb) - 1), -1).astype(np.int32)
         site_jslab.numpy()[...] = O.column_transform_slab(s2y, s2z, j0, ny)
 
+    def site_world_slab(self, site_jslab, dims, j0, centers, origin, voxel_size):
+        """engine.py:212-221 on a j-slab (numpy): lin -2 for rows not held."""
+        nx, ny, nz = dims
+        site = site_jslab.numpy()
+        nyl = site.shape[1]
+        c = np.asarray(centers, np.float64).reshape(-1, 3)
+        org = np.asarray(origin, np.float64)
+        idx = np.clip(np.floor((c - org) / voxel_size).astype(np.int64), 0, np.array(dims) - 1)
+        s = c.shape[0]
+        lin = np.full(s, -2, np.int32)
+        world = np.full((s, 3), np.nan)
+        dist = np.full(s, np.nan)
+        for q in range(s):
+            i, j, k = idx[q]
+            if not (j0 <= j < j0 + nyl):
+                continue
+            v = int(site[i, j - j0, k])
+            lin[q] = v
+            if v < 0:
+                dist[q] = np.inf
+                continue
+            si, sj, sk = v // (ny * nz), (v // nz) % ny, v % nz
+            world[q] = org + (np.array([si, sj, sk], np.float64) + 0.5) * voxel_size
+            dist[q] = np.linalg.norm(world[q] - c[q])
+        return lin, world, dist
+
     def synchronize(self):
         pass

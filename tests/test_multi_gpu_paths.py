@@ -89,9 +89,9 @@ from paper_2407_02363_b200 import synth
 from paper_2407_02363_b200.slab import SlabEDT
 torch.cuda.set_device(0)
 dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
-for exchange in ("p2p", "nccl"):
+for exchange, chunks in (("p2p", None), ("nccl", 1), ("nccl", 3)):
     for dims, p, seed in [((64, 48, 40), 0.03, 4), ((33, 20, 16), 0.2, 5)]:
-        slab = SlabEDT(dims, exchange=exchange)
+        slab = SlabEDT(dims, exchange=exchange, chunks=chunks)
         for rep in range(3):   # repeated calls reuse the receive buffer
             occ = synth.bernoulli_occupancy(dims, p, seed + rep)
             site = slab(torch.from_numpy(occ).cuda()).cpu().numpy()
@@ -114,3 +114,49 @@ def test_slab_p2p_symmetric_memory_world1():
     r = subprocess.run([sys.executable, "-c", _P2P_SCRIPT], env=env, capture_output=True, text=True,
                        timeout=600)
     assert r.returncode == 0 and "P2P-WORLD1-OK" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
+
+
+def test_slab_site_world_on_j_slabs_vs_whole_field():
+    """vx_site_world_slab: split a whole field into j-slabs (2/3/5 ranks'
+    worth); every centre is answered by exactly the slab that holds its
+    clipped row, and the combined answers equal K6 on the whole field
+    (engine.py:212-221; world point bit-exact, distance rtol 1e-6)."""
+    from paper_2407_02363_b200.engine import site_world
+    from paper_2407_02363_b200.slab import CudaBackend, even_split
+    dims, vs, origin = (40, 50, 36), 0.05, np.array([-1.0, -1.2, -0.3])
+    occ = synth.bernoulli_occupancy(dims, 0.01, 8)
+    fld = pba_edt(occ, voxel_size=vs)
+    full = torch.from_numpy(fld.site).cuda()
+    rng = np.random.default_rng(3)
+    centers = rng.uniform(origin - 0.3, origin + np.array(dims) * vs + 0.3, size=(64, 3))
+    want = site_world(fld, origin, vs, centers)
+    be = CudaBackend()
+    for world in (2, 3, 5):
+        js = even_split(dims[1], world)
+        lin = np.full(64, -2, np.int32)
+        wpt = np.full((64, 3), np.nan)
+        dd = np.full(64, np.nan)
+        for q in range(world):
+            part = full[:, js[q]:js[q + 1]].contiguous()
+            l_, w_, d_ = be.site_world_slab(part, dims, js[q], centers, origin, vs)
+            own = l_ != -2
+            assert not (own & (lin != -2)).any()   # one owner per centre
+            lin[own], wpt[own], dd[own] = l_[own], w_[own], d_[own]
+        assert np.array_equal(lin, want[0])
+        ok = want[0] >= 0
+        assert np.array_equal(wpt[ok], want[1][ok])
+        np.testing.assert_allclose(dd[ok], want[2][ok], rtol=1e-6)
+
+
+def test_slab_single_rank_site_world():
+    from paper_2407_02363_b200.engine import site_world
+    dims, vs, origin = (48, 40, 32), 0.04, np.zeros(3)
+    occ = synth.bernoulli_occupancy(dims, 0.05, 3)
+    slab = SlabEDT(dims, exchange="nccl", chunks=3)
+    slab(torch.from_numpy(occ).cuda())
+    centers = np.random.default_rng(1).uniform(-0.2, 2.0, size=(30, 3))
+    got = slab.site_world(centers, origin, vs)
+    want = site_world(pba_edt(occ, voxel_size=vs), origin, vs, centers)
+    assert np.array_equal(got[0], want[0])
+    ok = want[0] >= 0
+    assert np.array_equal(got[1][ok], want[1][ok])

@@ -31,14 +31,29 @@ def _worker(rank, world, port, q):
     try:
         for dims, p, seed in CASES:
             occ = (np.random.default_rng(seed).random(dims) < p).astype(np.uint8)
-            slab_edt = SlabEDT(dims, exchange="nccl", backend=OracleBackend(), device=torch.device("cpu"))
-            i0, i1 = slab_edt.i_starts[rank], slab_edt.i_starts[rank + 1]
-            site = slab_edt(torch.from_numpy(occ[i0:i1].copy())).clone()
-            parts = [None] * world
-            dist.all_gather_object(parts, site.numpy())
+            ok = True
+            for chunks in (1, 3, 16):   # pipelined exchange: slice groups (more groups than slices too)
+                slab_edt = SlabEDT(dims, exchange="nccl", backend=OracleBackend(), device=torch.device("cpu"),
+                                   chunks=chunks)
+                i0, i1 = slab_edt.i_starts[rank], slab_edt.i_starts[rank + 1]
+                for rep in range(2):   # buffers reused across calls
+                    site = slab_edt(torch.from_numpy(occ[i0:i1].copy())).clone()
+                    parts = [None] * world
+                    dist.all_gather_object(parts, site.numpy())
+                    full = np.concatenate(parts, axis=1)
+                    ok = ok and bool(np.array_equal(full, O.pba_edt_site(occ)))
+                # sphere queries routed to the row owner (engine.py:212-221)
+                vs, origin = 0.05, np.array([-0.3, 0.2, -0.1])
+                rng = np.random.default_rng(seed + 100)
+                lo, hi = origin - 0.2, origin + np.array(dims) * vs + 0.2   # some centres outside
+                centers = rng.uniform(lo, hi, size=(25, 3))
+                lin, world_pt, dd = slab_edt.site_world(centers, origin, vs)
+                rl, rw, rd = O.site_world(O.pba_edt_site(occ), vs, origin, centers)
+                okq = np.array_equal(lin, rl) and np.array_equal(world_pt[rl >= 0], rw[rl >= 0]) and \
+                    np.allclose(dd[rl >= 0], rd[rl >= 0], rtol=1e-6) and bool(np.all(np.isinf(dd[rl < 0])))
+                ok = ok and okq
             if rank == 0:
-                full = np.concatenate(parts, axis=1)
-                q.put((dims, bool(np.array_equal(full, O.pba_edt_site(occ)))))
+                q.put((dims, ok))
     finally:
         dist.destroy_process_group()
 
