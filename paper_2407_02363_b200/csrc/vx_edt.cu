@@ -368,6 +368,7 @@ __global__ void __launch_bounds__(256, 6) k_pass1_x16(const uint8_t *__restrict_
                         o[u] = (lv + r >= 2 * (base + e)) ? lv : r;   // ties -> lower k
                     }
                     const int j = lane * 4 + g;
+                    VX_ASSERT((j ^ ((j >> 3) & 7)) < 128, "pass-1 staging slot");
                     stage[j ^ ((j >> 3) & 7)] = make_int4(o[0], o[1], o[2], o[3]);
                 }
             }
@@ -376,6 +377,7 @@ __global__ void __launch_bounds__(256, 6) k_pass1_x16(const uint8_t *__restrict_
 #pragma unroll
             for (int g = 0; g < 4; ++g) {
                 const int j = g * 32 + lane;
+                VX_ASSERT(c * 512 + 4 * j < nz || j >= nu, "pass-1 store inside the line");
                 if (j < nu) dst[c * 128 + j] = stage[j ^ ((j >> 3) & 7)];
             }
             __syncwarp();
@@ -677,6 +679,7 @@ struct RowOut {
                 seek(y, sc, slice, k, nz);
             }
         }
+        VX_ASSERT(p != nullptr, "column output pointer");
         *p = v;
         p += step;
     }
@@ -758,6 +761,7 @@ __device__ __forceinline__ void column_tile(const typename Col<PASS, S2W, EW, FW
                     Fa = C::F(P, t, jq, k);
                 }
             }
+            VX_ASSERT(alo + n < (STAGED ? P.rows_alloc : P.L), "column stack slot");
             stk[(size_t)(alo + n) * TW + kk] = ec;
             ya = yb; Fa = Fb;
             yb = yc; Fb = Fc;
@@ -1117,6 +1121,7 @@ __device__ __forceinline__ bool ring_tile(const typename Col<PASS, false, false,
     if (colok) {
 #pragma unroll 4
         for (int y = lo; y < hi; ++y) {
+            VX_ASSERT(y >= 0 && y < P.rows_alloc, "ring key row");
             const uint32_t v = col[y * TW];
             uint32_t kv = P.kinv;
             if constexpr (PASS == 2) {
@@ -1179,6 +1184,7 @@ __device__ __forceinline__ bool ring_tile(const typename Col<PASS, false, false,
         for (; q0 < hi; q0 += R, qa += R * rowb) {
             if (*(volatile int *)s_fail) break;
             emit_pending(q0 - R);   // the previous block's codes were fetched a block ago
+            VX_ASSERT(qa >= cb && qa <= ce, "ring block row");
             const uint32_t k0 = lds_u32(qa), k1 = lds_u32(min(qa + rowb, ce));
             const uint32_t k2 = lds_u32(min(qa + 2 * rowb, ce)), k3 = lds_u32(min(qa + 3 * rowb, ce));
             uint32_t b0 = min(min(k0, k1 + one), min(k2 + 4u * one, k3 + 9u * one));
@@ -1218,6 +1224,7 @@ __device__ __forceinline__ bool ring_tile(const typename Col<PASS, false, false,
 #pragma unroll
             for (int i = 0; i < R; ++i) {
                 const int row = (int)(bb[i] & rmask);
+                VX_ASSERT(i >= pend || (row >= 0 && row < P.L && bb[i] < P.kinv), "ring winner row");
                 if (row != crow) {
                     crow = row;
                     code = __ldg(src + (size_t)((uint32_t)row * ustride));
@@ -1359,6 +1366,7 @@ __global__ void __launch_bounds__(kWarpCtaThreads, 1) k_pass3_stream(const uint3
     uint32_t *gst = ovf + gw * (long long)max(P.L - kStreamCap, 0) * 32 + lane - (long long)kStreamCap * 32;
     auto ent = [&](int i) -> uint32_t { return i < kStreamCap ? sst[i * 32] : gst[(long long)i * 32]; };
     auto put = [&](int i, uint32_t e) {
+        VX_ASSERT(i >= 0 && i < P.L, "stream hull slot");
         if (i < kStreamCap) sst[i * 32] = e;
         else gst[(long long)i * 32] = e;
     };

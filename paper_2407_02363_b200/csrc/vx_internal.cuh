@@ -6,6 +6,24 @@
 
 #define VX_FULL_MASK 0xffffffffu
 
+// Checked builds (make EXTRA=-DVX_CHECK; tools/checked_suite.sh): device-side
+// bounds and invariant assertions on the kernels' shared-memory and global
+// index arithmetic; a violation prints its site and traps (the launch fails
+// loudly).  Compiled out otherwise.
+#ifdef VX_CHECK
+#include <cstdio>
+#define VX_ASSERT(cond, what)                                                             \
+    do {                                                                                  \
+        if (!(cond)) {                                                                    \
+            printf("VX_CHECK failed: %s (%s:%d) block %d thread %d\n", what, __FILE__, __LINE__, \
+                   (int)blockIdx.x, (int)threadIdx.x);                                    \
+            __trap();                                                                     \
+        }                                                                                 \
+    } while (0)
+#else
+#define VX_ASSERT(cond, what) do {} while (0)
+#endif
+
 namespace vx {
 
 // Launch configuration / layout decisions for one EDT problem.  Computed on

@@ -277,6 +277,7 @@ __global__ void k_finalize(float *__restrict__ cells, uint8_t *__restrict__ occ,
         const int base = ctr->touched, cnt = ctr->pending;
         for (long long t = tid; t < cnt; t += nth) {
             const int v = touched[base + t];
+            VX_ASSERT(v >= 0 && v < n, "finalize voxel");
             if (apply_hits(cells, occ, counts, v, hit, occ_thr, fresh != 0)) mark(v);
         }
     }
