@@ -495,8 +495,11 @@ extern "C" int vx_grid_read_cells(vx_grid *g, float *out) {
 
 extern "C" int vx_grid_write_cells(vx_grid *g, const float *in) {
     if (!g || !in) return fail(VX_EINVAL, "NULL argument");
+    // cells an insert's dense clip would change outside the touched voxels
+    // (grids.py:187 clips every voxel: out of range, NaN, and -0.0 -> +0.0)
     bool oor = false;
-    for (long long v = 0; v < g->n && !oor; ++v) oor = !(in[v] >= kLMin && in[v] <= kLMax);
+    for (long long v = 0; v < g->n && !oor; ++v)
+        oor = !(in[v] >= kLMin && in[v] <= kLMax) || (in[v] == 0.0f && std::signbit(in[v]));
     VX_CUDA(cudaMemcpyAsync(g->cells, in, g->n * sizeof(float), cudaMemcpyHostToDevice, g->ctx->stream));
     g->ctx->h2d += g->n * 4;
     cudaError_t e = launch_occupancy(g->cells, g->occ, g->n, kOccThr, g->ctx->stream);
