@@ -7,12 +7,13 @@ L = _lib.load(); ctx = _lib.default_context()
 stream = torch.cuda.ExternalStream(ctx.stream_handle())
 args = sys.argv[1:]
 for i in range(0, len(args), 3):
-    n, p, seed = int(args[i]), float(args[i + 1]), int(args[i + 2])
-    occ = torch.from_numpy(synth.bernoulli_occupancy((n, n, n), p, seed)).cuda()
-    site = torch.empty((n, n, n), dtype=torch.int32, device="cuda")
-    sb = L.vx_edt_scratch_bytes(n, n, n, 1)
+    dims = tuple(int(v) for v in args[i].split(",")) if "," in args[i] else (int(args[i]),) * 3
+    p, seed = float(args[i + 1]), int(args[i + 2])
+    occ = torch.from_numpy(synth.bernoulli_occupancy(dims, p, seed)).cuda()
+    site = torch.empty(dims, dtype=torch.int32, device="cuda")
+    sb = L.vx_edt_scratch_bytes(*dims, 1)
     scr = torch.empty(sb, dtype=torch.uint8, device="cuda")
-    a = (ctx.handle, ctypes.c_void_p(occ.data_ptr()), n, n, n, 1, ctypes.c_void_p(site.data_ptr()),
+    a = (ctx.handle, ctypes.c_void_p(occ.data_ptr()), *dims, 1, ctypes.c_void_p(site.data_ptr()),
          ctypes.c_void_p(scr.data_ptr()), sb)
     for _ in range(2): _lib.check(L.vx_edt_device(*a))
     torch.cuda.synchronize()
@@ -21,5 +22,6 @@ for i in range(0, len(args), 3):
     for _ in range(3): _lib.check(L.vx_edt_device(*a))
     e1.record(stream); torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / 3
-    print(f"{n}^3 p={p}: {ms:.3f} ms  {n**3/ms/1e6:.1f} Gvox/s", flush=True)
+    nv = dims[0] * dims[1] * dims[2]
+    print(f"{'x'.join(map(str, dims))} p={p}: {ms:.3f} ms  {nv/ms/1e6:.1f} Gvox/s", flush=True)
     del occ, site, scr; torch.cuda.empty_cache()
