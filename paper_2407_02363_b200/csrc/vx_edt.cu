@@ -1272,7 +1272,9 @@ __global__ void __launch_bounds__(MAXT, MAXT >= 1024 ? 1 : (RING ? 3 : kColMinBl
         }
     }
     if constexpr (RING && FW <= 1) {
-        if (ring_active(P) && ring_scene(P, PASS, outer)) {
+        // the scene's slice count first (one cached load): sparse scenes never
+        // touch the search header
+        if (ring_scene(P, PASS, outer) && ring_active(P)) {
             if (ring_tile<PASS, SCAT, TW>(reinterpret_cast<const typename Col<PASS, false, false, 0>::InT *>(in),
                                           reinterpret_cast<typename Col<PASS, false, false, 0>::OutT *>(out), P,
                                           &sc, smem, &tmap, tile, outer, kt))
