@@ -1153,14 +1153,12 @@ __device__ __forceinline__ bool ring_tile(const typename Col<PASS, false, false,
         const int budget = P.ring_budget;
         int spent = -2 * budget;
         const InT *src = in + base;
-        const uint32_t ustride = (uint32_t)stride;   // row offsets fit 32 bits (int32 sites)
+        const uint32_t ustride4 = (uint32_t)stride * (uint32_t)sizeof(InT);   // row byte offsets fit 32 bits
         RowOut<OutT, SCAT> dst;
         dst.begin(out, base, stride, lo, &sc, outer, k, P.nz);
         // four query rows per block share one window: step s reads rows
         // q0 - s and q0 + 3 + s, at distances s..s+3 from the block's rows
         constexpr int R = 4;
-        int crow = -1;
-        InT code = 0;
         int wrow[R];
         InT wcode[R];
         int pend = 0;   // rows of the previous block waiting for their store
@@ -1196,8 +1194,31 @@ __device__ __forceinline__ bool ring_tile(const typename Col<PASS, false, false,
             // only adds larger keys)
             uint32_t o0 = one, o1 = 4u * one, o2 = 9u * one, o3 = 16u * one, d3 = 9u * one;
             const int qb = qa + 3 * rowb;
-            int ro = rowb, sdone = 0;
             bool more = (max(b0, b3) >= o0) | (max(b1, b2) >= o1);
+            // interior trips first: while both windows stay inside the column
+            // (left rows q0-1-2t, q0-2-2t >= 0; right rows q0+4+2t, q0+5+2t <= L-1)
+            // the loads need no clamps -- two running pointers, immediate offsets
+            const int tfree = min(min(q0, P.L - R - q0), cap) >> 1;   // warp-uniform
+            const uint32_t *pl = col + (q0 - 1) * TW, *pr = col + (q0 + R) * TW;
+            int t = 0;
+#pragma unroll 3
+            for (; more && t < tfree; ++t) {
+                const uint32_t o4 = o3 + d3;   // (s + 4)^2
+                d3 += 2u * one;
+                const uint32_t kl = pl[0], kl2 = pl[-TW], kr = pr[0], kr2 = pr[TW];
+                b0 = min(b0, kl + o0); b1 = min(b1, kl + o1); b2 = min(b2, kl + o2); b3 = min(b3, kl + o3);
+                b0 = min(b0, kr + o3); b1 = min(b1, kr + o2); b2 = min(b2, kr + o1); b3 = min(b3, kr + o0);
+                b0 = min(b0, kl2 + o1); b1 = min(b1, kl2 + o2); b2 = min(b2, kl2 + o3); b3 = min(b3, kl2 + o4);
+                b0 = min(b0, kr2 + o4); b1 = min(b1, kr2 + o3); b2 = min(b2, kr2 + o2); b3 = min(b3, kr2 + o1);
+                o0 = o2; o1 = o3; o2 = o4;
+                o3 = o4 + d3;                  // (s + 5)^2
+                d3 += 2u * one;
+                pl -= 2 * TW;
+                pr += 2 * TW;
+                more = (max(b0, b3) >= o0) | (max(b1, b2) >= o1);
+            }
+            // then the clamped steps near the column ends
+            int ro = (1 + 2 * t) * rowb, sdone = 2 * t;
             while (more & (sdone < cap)) {
                 const uint32_t o4 = o3 + d3;   // (s + 4)^2
                 d3 += 2u * one;
@@ -1223,14 +1244,13 @@ __device__ __forceinline__ bool ring_tile(const typename Col<PASS, false, false,
             pend = min(R, hi - q0);
 #pragma unroll
             for (int i = 0; i < R; ++i) {
+                // every block row holds a real winner (a clamped read only repeats
+                // an edge row); its code is loaded now and stored a block later
                 const int row = (int)(bb[i] & rmask);
-                VX_ASSERT(i >= pend || (row >= 0 && row < P.L && bb[i] < P.kinv), "ring winner row");
-                if (row != crow) {
-                    crow = row;
-                    code = __ldg(src + (size_t)((uint32_t)row * ustride));
-                }
+                VX_ASSERT(row >= 0 && row < P.L && bb[i] < P.kinv, "ring winner row");
                 wrow[i] = row;
-                wcode[i] = code;
+                wcode[i] = __ldg(reinterpret_cast<const InT *>(reinterpret_cast<const char *>(src) +
+                                                              (unsigned long long)(uint32_t)row * ustride4));
             }
         }
         if (q0 >= hi) emit_pending(q0 - R);
