@@ -436,6 +436,10 @@ __global__ void __launch_bounds__(256) k_pass1_generic(const uint8_t *__restrict
 // ---------------------------------------------------------------------------
 // Passes 2 and 3: lower-envelope (strict lower hull) per column.
 // ---------------------------------------------------------------------------
+// row bits of the windowed search's keys (w << kRingRb | row): columns of up to
+// 1024 rows; fixed so that the key constants compile to immediates
+constexpr int kRingRb = 10;
+
 struct ColParams {
     int nx, ny, nz;
     int L;             // column length (ny for pass 2, nx for pass 3)
@@ -1113,7 +1117,7 @@ __device__ __forceinline__ bool ring_tile(const typename Col<PASS, false, false,
     // rows of empty slices hold no pass-2 codes (pass 2 skipped them)
     const uint8_t *sfl = PASS == 3 && P.sflag3 && (P.mcount ? __ldg(P.mcount + scene) : 0) < P.nx
                              ? P.sflag3 + (long long)scene * P.nx : nullptr;
-    const int rb = P.rb;
+    constexpr int rb = kRingRb;   // fixed: the key constants are immediates
     __syncthreads();
     mbar_wait(bar, 0);
     // the tile's values -> search keys, in place (each thread its band's rows)
@@ -1581,11 +1585,11 @@ bool ring_possible(const EdtPlan &p, const SparseRows *sp) {
            (sp->m_hint < 0 || sp->m_hint >= ring_min_for(p.nx));
 }
 bool ring_fits(const EdtPlan &p, int pass, int L) {
-    const int rb = std::max(1, bits_of(L - 1));
+    const int rb = kRingRb;
     const long long wmax = pass == 2 ? (long long)(p.nz - 1) * (p.nz - 1)
                                      : (long long)(p.ny - 1) * (p.ny - 1) + (long long)(p.nz - 1) * (p.nz - 1);
     const long long c = ring_cap() + kRingBlock + 1;
-    return rb <= 12 && ((wmax + c * c + 1) << rb) < (long long)ring_kinv(rb);
+    return L <= (1 << rb) && ((wmax + c * c + 1) << rb) < (long long)ring_kinv(rb);
 }
 
 // pass 2: `outer` counts slices (nscenes * local nx); pass 3: `outer` counts
@@ -1620,7 +1624,7 @@ ColParams col_params(const EdtPlan &p, int pass, long long nouter, int nyl, int 
     P.fslot = pass == 2 ? 0 : 1;
     P.nkt2 = (p.nz + p.tw2 - 1) / p.tw2;
     P.ny2 = p.ny;
-    P.rb = bits_of(P.L - 1) > 0 ? bits_of(P.L - 1) : 1;
+    P.rb = kRingRb;
     P.ring_cap = ring_cap();
     P.ring_budget = ring_budget(pass);
     P.kinv = ring_kinv(P.rb);

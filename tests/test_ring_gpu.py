@@ -46,7 +46,8 @@ def test_reference_golden_cases(env, monkeypatch):
 @pytest.mark.parametrize("env", KNOBS, ids=KID)
 @pytest.mark.parametrize("dims,p", [((96, 96, 96), 0.02), ((64, 70, 36), 0.3), ((80, 64, 100), 0.05),
                                     ((128, 96, 64), 0.005), ((40, 600, 32), 0.02), ((600, 40, 32), 0.02),
-                                    ((70, 50, 200), 0.6), ((50, 64, 64), 0.0005)],
+                                    ((70, 50, 200), 0.6), ((50, 64, 64), 0.0005), ((1100, 40, 32), 0.02),
+                                    ((40, 1100, 32), 0.02)],
                          ids=lambda v: "x".join(map(str, v)) if isinstance(v, tuple) else str(v))
 def test_dense_grids_vs_oracle(dims, p, env, monkeypatch):
     """Densities from 0.05 % to 60 %, ragged k tiles (nz % 32 != 0), columns
