@@ -272,7 +272,7 @@ __global__ void __launch_bounds__(256) k_pass1_v4(const uint8_t *__restrict__ oc
 // comes from a running scan over the lane's 16 voxels, seeded by the nearest
 // site in the lanes before / after (ballot + one shuffle); the answer is l if
 // k - l <= r - k (edt.py:217-224; l + r >= 2k), with missing sides at -/+2^30.
-template <int CH>
+template <int CH, bool FULL>
 __global__ void __launch_bounds__(256, 6) k_pass1_x16(const uint8_t *__restrict__ occ, int32_t *__restrict__ s1,
                                                    long long nlines, int nz, const uint8_t *__restrict__ sflag,
                                                    int ny, const int *__restrict__ xs, const int *__restrict__ hdr,
@@ -318,7 +318,11 @@ __global__ void __launch_bounds__(256, 6) k_pass1_x16(const uint8_t *__restrict_
             for (int j = lane; j < nu; j += 32) dst[j] = make_int4(-1, -1, -1, -1);
             continue;
         }
-        int4 *stage = s_stage[threadIdx.x >> 5];
+        // this warp's staging block; per lane, the XOR-swizzled 16-byte slots it
+        // writes (units lane*4 + g) and reads (units g*32 + lane), as shared addresses
+        const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(s_stage[threadIdx.x >> 5]);
+        const uint32_t st_idx = (uint32_t)((lane * 4) ^ ((lane >> 1) & 7));   // unit (lane*4 + g) ^ g's swizzle
+        const uint32_t ld_idx = (uint32_t)(lane ^ (lane >> 3));               // unit (g*32 + lane) ^ swizzle
         // warp-uniform carries: last site before chunk c, first site after it
         unsigned bal[CH];
         int lastc[CH], firstc[CH];
@@ -348,37 +352,45 @@ __global__ void __launch_bounds__(256, 6) k_pass1_x16(const uint8_t *__restrict_
             const int lp = pm ? 31 - __clz(pm) : 0, ln = nm ? __ffs(nm) - 1 : 0;
             const uint32_t mbp = __shfl_sync(VX_FULL_MASK, mm, lp);
             const uint32_t mbn = __shfl_sync(VX_FULL_MASK, mm, ln);
-            int l = pm ? (c * 32 + lp) * 16 + 31 - __clz(mbp) : lastc[c];   // last site < base
-            int r = nm ? (c * 32 + ln) * 16 + __ffs(mbn) - 1 : firstc[c];   // first site > base + 15
-            // backward over the lane's 16 voxels: r runs, l is the last site
-            // <= e in the lane (one FLO) or the carry.  The four 16-byte groups
-            // go through this warp's shared staging (XOR-swizzled 16-byte
-            // units: conflict-free both ways) so that the global stores are
-            // 512-byte coalesced rows (plain stores: pass 2 reads s1 from L2)
-            if (base < nz) {
+            // sites relative to the lane's first voxel: l is the last site before it
+            // (< 0), r the first after its 16 voxels (>= 16); far sentinels when none
+            const int lrel = (pm ? (c * 32 + lp) * 16 + 31 - __clz(mbp) : lastc[c]) - base;
+            int rrel = (nm ? (c * 32 + ln) * 16 + __ffs(mbn) - 1 : firstc[c]) - base;
+            // backward over the lane's 16 voxels: rrel runs, the last site <= e is
+            // one FLO of the masked bits (or lrel); ties -> lower k.  The four
+            // 16-byte groups go through this warp's shared staging (XOR-swizzled
+            // 16-byte units: conflict-free both ways) so that the global stores
+            // are 512-byte coalesced rows (plain stores: pass 2 reads s1 from L2)
+            if (FULL || base < nz) {
 #pragma unroll
                 for (int g = 3; g >= 0; --g) {
                     int o[4];
 #pragma unroll
                     for (int u = 3; u >= 0; --u) {
                         const int e = 4 * g + u;
-                        if (mm & (1u << e)) r = base + e;
+                        if (mm & (1u << e)) rrel = e;
                         const uint32_t le = mm & ((2u << e) - 1u);
-                        const int lv = le ? base + 31 - __clz(le) : l;
-                        o[u] = (lv + r >= 2 * (base + e)) ? lv : r;   // ties -> lower k
+                        const int lv = le ? 31 - __clz(le) : lrel;
+                        o[u] = base + ((lv + rrel >= 2 * e) ? lv : rrel);
                     }
-                    const int j = lane * 4 + g;
-                    VX_ASSERT((j ^ ((j >> 3) & 7)) < 128, "pass-1 staging slot");
-                    stage[j ^ ((j >> 3) & 7)] = make_int4(o[0], o[1], o[2], o[3]);
+                    VX_ASSERT((((lane * 4 + g) ^ ((lane >> 1) & 7))) < 128, "pass-1 staging slot");
+                    asm volatile("st.shared.v4.s32 [%0], {%1, %2, %3, %4};" ::"r"(sbase + ((st_idx ^ (uint32_t)g) << 4)),
+                                 "r"(o[0]), "r"(o[1]), "r"(o[2]), "r"(o[3]) : "memory");
                 }
             }
             __syncwarp();
-            const int nu = min(128, (nz - c * 512) >> 2);   // 16-byte units of this chunk
+            const int nu = FULL ? 128 : min(128, (nz - c * 512) >> 2);   // 16-byte units of this chunk
 #pragma unroll
             for (int g = 0; g < 4; ++g) {
                 const int j = g * 32 + lane;
                 VX_ASSERT(c * 512 + 4 * j < nz || j >= nu, "pass-1 store inside the line");
-                if (j < nu) dst[c * 128 + j] = stage[j ^ ((j >> 3) & 7)];
+                if (FULL || j < nu) {
+                    int4 v;
+                    asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
+                                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                                 : "r"(sbase + (((uint32_t)(g * 32) + (ld_idx ^ (uint32_t)((g & 1) * 4))) << 4)) : "memory");
+                    dst[c * 128 + j] = v;
+                }
             }
             __syncwarp();
         }
@@ -1963,11 +1975,13 @@ cudaError_t launch_pass1(const uint8_t *occ, int32_t *s1, long long nslices, int
     else if (vec && nz <= 256) k_pass1_v4<2, 2><<<grid2, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny, xs, hdr, ls);
     else if (vec && nz <= 512 && xs && VX_P1_LPW512 == 2) k_pass1_v4<4, 2><<<grid2, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny, xs, hdr, ls);
     else if (vec && nz % 16 == 0 && nz <= 512 && VX_P1_X16)   // persistent: 6 CTAs of 8 warps per SM
-        k_pass1_x16<1><<<(unsigned)std::min<long long>(grid, (long long)num_sms() * 6), 256, 0, st>>>(
+        (nz % 512 == 0 ? k_pass1_x16<1, true> : k_pass1_x16<1, false>)
+            <<<(unsigned)std::min<long long>(grid, (long long)num_sms() * 6), 256, 0, st>>>(
             occ, s1, nlines, nz, sflag, ny, xs, hdr, ls);
     else if (vec && nz <= 512) k_pass1_v4<4, 1><<<grid, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny, xs, hdr, ls);
     else if (vec && nz % 16 == 0 && nz <= 1024 && VX_P1_X16)
-        k_pass1_x16<2><<<(unsigned)std::min<long long>(grid, (long long)num_sms() * 6), 256, 0, st>>>(
+        (nz % 512 == 0 ? k_pass1_x16<2, true> : k_pass1_x16<2, false>)
+            <<<(unsigned)std::min<long long>(grid, (long long)num_sms() * 6), 256, 0, st>>>(
             occ, s1, nlines, nz, sflag, ny, xs, hdr, ls);
     else if (vec && nz <= 1024) k_pass1_v4<8, 1><<<grid, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny, xs, hdr, ls);
     else if (vec && nz <= 2048) k_pass1_v4<16, 1><<<grid, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny, xs, hdr, ls);
