@@ -954,7 +954,7 @@ extern "C" int vx_edt_pass12_device(vx_ctx *c, const uint8_t *d_occ, int nx, int
         return fail(VX_EINVAL, "scratch too small");
     }
     int32_t *s1 = (int32_t *)d_scratch;
-    cudaError_t e = launch_pass1(d_occ, s1, nxl, ny, nz, c->stream);
+    cudaError_t e = launch_pass1(d_occ, s1, nxl, ny, nz, c->stream, nullptr, p.s1_16);
     if (e == cudaSuccess) e = launch_pass2(s1, d_s2, (unsigned char *)d_scratch + s1b, p, nxl, c->stream);
     if (e != cudaSuccess) return cuda_fail(e, "pass12");
     c->launches += 2;
@@ -1006,7 +1006,7 @@ extern "C" int vx_edt_pass12_scatter(vx_ctx *c, const uint8_t *d_occ, int nx, in
     int32_t *s1 = (int32_t *)d_scratch;
     SparseRows sp;
     if ((rc = slab_rows(c, &sp))) return rc;
-    cudaError_t e = launch_pass1(d_occ, s1, nxl, ny, nz, c->stream, &sp);
+    cudaError_t e = launch_pass1(d_occ, s1, nxl, ny, nz, c->stream, &sp, p.s1_16);
     if (e != cudaSuccess) return cuda_fail(e, "pass12_scatter (pass 1)");
     e = launch_pass2_scatter(s1, tab, (unsigned char *)d_scratch + s1b, p, nxl, c->stream, &sp);
     if (e != cudaSuccess) return cuda_fail(e, "pass12_scatter (pass 2)");
@@ -1319,7 +1319,7 @@ static cudaError_t edt_passes(vx_cycle *cy, const vx_grid *src, int32_t *site, b
             cy->ctx->launches += 2;
         }
     }
-    if (e == cudaSuccess) e = launch_pass1(occ, s1, p.nx, p.ny, p.nz, st, sparse ? &sp : nullptr);
+    if (e == cudaSuccess) e = launch_pass1(occ, s1, p.nx, p.ny, p.nz, st, sparse ? &sp : nullptr, p.s1_16);
     if (marks) cy->mark(5);
     if (e == cudaSuccess) e = launch_pass2(s1, s2, gs, p, p.nx, st, sparse ? &sp : nullptr);
     if (marks) cy->mark(6);

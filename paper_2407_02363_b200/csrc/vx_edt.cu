@@ -126,12 +126,28 @@ __device__ __forceinline__ int pick(int k, int l, int r) {
     return (k - l <= r - k) ? l : r;
 }
 
+__device__ __forceinline__ uint32_t pack16(int a, int b) {
+    return (uint32_t)(uint16_t)a | ((uint32_t)(uint16_t)b << 16);
+}
+
+// s1 element type: int32, or int16 when pass 2 stages its tiles by TMA
+// (EdtPlan::s1_16; pass 2 widens them in registers).  Four consecutive values
+// stored at 4-element unit q: one 16-byte (int32) or 8-byte (int16) store.
+template <typename T>
+__device__ __forceinline__ void store4(T *line, int q, int a, int b, int c, int d) {
+    if constexpr (sizeof(T) == 4) {
+        reinterpret_cast<int4 *>(line)[q] = make_int4(a, b, c, d);
+    } else {
+        reinterpret_cast<uint2 *>(line)[q] = make_uint2(pack16(a, b), pack16(c, d));
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Pass 1, vector path: nz % 4 == 0, nz <= 128 * CMAX.  One warp per line;
 // lane owns 4 consecutive voxels of each 128-voxel chunk.
 // ---------------------------------------------------------------------------
-template <int CMAX>
-__device__ __forceinline__ void pass1_line(const uint32_t (&nib)[CMAX], int4 *__restrict__ dst, int nq,
+template <int CMAX, typename T>
+__device__ __forceinline__ void pass1_line(const uint32_t (&nib)[CMAX], T *__restrict__ dst, int nq,
                                            int lane) {
     // The nearest occupied k before / after this lane's 4 voxels comes from
     // the nearest lane holding any site: a ballot names the lanes with sites,
@@ -185,15 +201,15 @@ __device__ __forceinline__ void pass1_line(const uint32_t (&nib)[CMAX], int4 *__
             if ((nb >> e) & 1u) r = base + e;
             o[e] = pick(base + e, lv[e], r);
         }
-        if (q < nq) dst[q] = make_int4(o[0], o[1], o[2], o[3]);
+        if (q < nq) store4(dst, q, o[0], o[1], o[2], o[3]);
     }
 }
 
 // LPW lines per warp: all their loads are issued before any line is scanned
 // (memory-level parallelism for the streaming read).
-template <int CMAX, int LPW>
+template <int CMAX, int LPW, typename T>
 __global__ void __launch_bounds__(256) k_pass1_v4(const uint8_t *__restrict__ occ,
-                                                  int32_t *__restrict__ s1,
+                                                  T *__restrict__ s1,
                                                   long long nlines, int nz,
                                                   const uint8_t *__restrict__ sflag, int ny,
                                                   const int *__restrict__ xs, const int *__restrict__ hdr,
@@ -233,7 +249,7 @@ __global__ void __launch_bounds__(256) k_pass1_v4(const uint8_t *__restrict__ oc
 #pragma unroll
     for (int l = 0; l < LPW; ++l) {
         if (!act[l]) continue;
-        int4 *dst = reinterpret_cast<int4 *>(s1 + lines[l] * nz);
+        T *dst = s1 + lines[l] * nz;
         uint32_t any = 0;
 #pragma unroll
         for (int c = 0; c < CMAX; ++c) any |= nib[l][c];
@@ -243,7 +259,7 @@ __global__ void __launch_bounds__(256) k_pass1_v4(const uint8_t *__restrict__ oc
 #pragma unroll
             for (int c = 0; c < CMAX; ++c) {
                 const int q = c * 32 + lane;
-                if (q < nq) dst[q] = make_int4(-1, -1, -1, -1);
+                if (q < nq) store4(dst, q, -1, -1, -1, -1);
             }
             continue;
         }
@@ -272,8 +288,8 @@ __global__ void __launch_bounds__(256) k_pass1_v4(const uint8_t *__restrict__ oc
 // comes from a running scan over the lane's 16 voxels, seeded by the nearest
 // site in the lanes before / after (ballot + one shuffle); the answer is l if
 // k - l <= r - k (edt.py:217-224; l + r >= 2k), with missing sides at -/+2^30.
-template <int CH, bool FULL>
-__global__ void __launch_bounds__(256, 6) k_pass1_x16(const uint8_t *__restrict__ occ, int32_t *__restrict__ s1,
+template <int CH, bool FULL, typename T>
+__global__ void __launch_bounds__(256, 6) k_pass1_x16(const uint8_t *__restrict__ occ, T *__restrict__ s1,
                                                    long long nlines, int nz, const uint8_t *__restrict__ sflag,
                                                    int ny, const int *__restrict__ xs, const int *__restrict__ hdr,
                                                    int *__restrict__ linestat) {
@@ -311,18 +327,23 @@ __global__ void __launch_bounds__(256, 6) k_pass1_x16(const uint8_t *__restrict_
         unsigned any = 0;
 #pragma unroll
         for (int c = 0; c < CH; ++c) any |= msk[c];
+        // 16-byte units: 4 (int32) or 8 (int16) values; UPC units per 512-voxel chunk
+        constexpr int VPU = 16 / (int)sizeof(T), UPC = 512 / VPU;
         int4 *dst = reinterpret_cast<int4 *>(s1 + L * nz);
         if (!__any_sync(VX_FULL_MASK, any != 0u)) {   // empty line: no site anywhere (edt.py:212)
             ++nempty;
-            const int nu = nz >> 2;   // 16-byte units of the line (coalesced rows)
+            const int nu = nz / VPU;   // 16-byte units of the line (coalesced rows)
             for (int j = lane; j < nu; j += 32) dst[j] = make_int4(-1, -1, -1, -1);
             continue;
         }
         // this warp's staging block; per lane, the XOR-swizzled 16-byte slots it
         // writes (units lane*4 + g) and reads (units g*32 + lane), as shared addresses
         const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(s_stage[threadIdx.x >> 5]);
-        const uint32_t st_idx = (uint32_t)((lane * 4) ^ ((lane >> 1) & 7));   // unit (lane*4 + g) ^ g's swizzle
-        const uint32_t ld_idx = (uint32_t)(lane ^ (lane >> 3));               // unit (g*32 + lane) ^ swizzle
+        // int32: the lane writes units lane*4 + g (g < 4); int16: units lane*2 + h
+        // (h < 2); units j live at slot j ^ ((j >> 3) & 7); reads take units g*32 + lane
+        const uint32_t st_idx = VPU == 4 ? (uint32_t)((lane * 4) ^ ((lane >> 1) & 7))
+                                         : (uint32_t)((lane * 2) ^ ((lane >> 2) & 7));
+        const uint32_t ld_idx = (uint32_t)(lane ^ (lane >> 3));
         // warp-uniform carries: last site before chunk c, first site after it
         unsigned bal[CH];
         int lastc[CH], firstc[CH];
@@ -362,6 +383,7 @@ __global__ void __launch_bounds__(256, 6) k_pass1_x16(const uint8_t *__restrict_
             // 16-byte units: conflict-free both ways) so that the global stores
             // are 512-byte coalesced rows (plain stores: pass 2 reads s1 from L2)
             if (FULL || base < nz) {
+                int o8[8];   // int16: two groups per 16-byte unit
 #pragma unroll
                 for (int g = 3; g >= 0; --g) {
                     int o[4];
@@ -373,23 +395,34 @@ __global__ void __launch_bounds__(256, 6) k_pass1_x16(const uint8_t *__restrict_
                         const int lv = le ? 31 - __clz(le) : lrel;
                         o[u] = base + ((lv + rrel >= 2 * e) ? lv : rrel);
                     }
-                    VX_ASSERT((((lane * 4 + g) ^ ((lane >> 1) & 7))) < 128, "pass-1 staging slot");
-                    asm volatile("st.shared.v4.s32 [%0], {%1, %2, %3, %4};" ::"r"(sbase + ((st_idx ^ (uint32_t)g) << 4)),
-                                 "r"(o[0]), "r"(o[1]), "r"(o[2]), "r"(o[3]) : "memory");
+                    if constexpr (VPU == 4) {
+                        VX_ASSERT((((lane * 4 + g) ^ ((lane >> 1) & 7))) < UPC, "pass-1 staging slot");
+                        asm volatile("st.shared.v4.s32 [%0], {%1, %2, %3, %4};" ::"r"(sbase + ((st_idx ^ (uint32_t)g) << 4)),
+                                     "r"(o[0]), "r"(o[1]), "r"(o[2]), "r"(o[3]) : "memory");
+                    } else {
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) o8[4 * (g & 1) + u] = o[u];
+                        if ((g & 1) == 0) {   // groups g, g+1 complete unit lane*2 + g/2
+                            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};"
+                                         ::"r"(sbase + ((st_idx ^ (uint32_t)(g >> 1)) << 4)),
+                                         "r"(pack16(o8[0], o8[1])), "r"(pack16(o8[2], o8[3])),
+                                         "r"(pack16(o8[4], o8[5])), "r"(pack16(o8[6], o8[7])) : "memory");
+                        }
+                    }
                 }
             }
             __syncwarp();
-            const int nu = FULL ? 128 : min(128, (nz - c * 512) >> 2);   // 16-byte units of this chunk
+            const int nu = FULL ? UPC : min(UPC, (nz - c * 512) / VPU);   // 16-byte units of this chunk
 #pragma unroll
-            for (int g = 0; g < 4; ++g) {
+            for (int g = 0; g < UPC / 32; ++g) {
                 const int j = g * 32 + lane;
-                VX_ASSERT(c * 512 + 4 * j < nz || j >= nu, "pass-1 store inside the line");
+                VX_ASSERT(c * 512 + VPU * j < nz || j >= nu, "pass-1 store inside the line");
                 if (FULL || j < nu) {
                     int4 v;
                     asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
                                  : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
                                  : "r"(sbase + (((uint32_t)(g * 32) + (ld_idx ^ (uint32_t)((g & 1) * 4))) << 4)) : "memory");
-                    dst[c * 128 + j] = v;
+                    dst[c * UPC + j] = v;
                 }
             }
             __syncwarp();
@@ -413,8 +446,9 @@ __global__ void __launch_bounds__(256, 6) k_pass1_x16(const uint8_t *__restrict_
 
 // Pass 1, generic path (any nz): 32-voxel chunks with ballots; the forward
 // sweep parks `l` in the output, the backward sweep combines.
+template <typename T>
 __global__ void __launch_bounds__(256) k_pass1_generic(const uint8_t *__restrict__ occ,
-                                                       int32_t *__restrict__ s1,
+                                                       T *__restrict__ s1,
                                                        long long nlines, int nz,
                                                        const uint8_t *__restrict__ sflag, int ny) {
     const int lane = threadIdx.x & 31;
@@ -422,7 +456,7 @@ __global__ void __launch_bounds__(256) k_pass1_generic(const uint8_t *__restrict
     if (line >= nlines) return;
     if (sflag && !sflag[(uint32_t)line / (uint32_t)ny]) return;
     const uint8_t *src = occ + line * nz;
-    int32_t *dst = s1 + line * nz;
+    T *dst = s1 + line * nz;
     int carry = -1;
     for (int base = 0; base < nz; base += 32) {
         const int k = base + lane;
@@ -485,6 +519,7 @@ struct ColParams {
     int ring_cap;          // largest search radius before a tile is handed back
     int ring_budget;       // mean window steps per 4-row block above which a tile is handed back
     uint32_t kinv;         // key of a row without a candidate (stays above every reachable key)
+    int s16;               // pass 2: s1 holds int16 line sites (EdtPlan::s1_16)
 };
 
 template <int PASS, bool S2W, bool EW, int FW>
@@ -982,6 +1017,34 @@ __global__ void __launch_bounds__(kColThreads, kColMinBlocks) k_column_smem(cons
     column_tile<PASS, S2W, EW, FW, false, SCAT>(in, out, stk, meta, P, blockIdx.x, &sc);
 }
 
+// int16 s1 (EdtPlan::s1_16): the tile arrived packed (2 bytes per value) at the
+// start of shared memory and is widened in place to 32-bit words cv(value, row).
+// Widened row y covers packed rows 2y and 2y+1, so (L = 32 B rows): (1) rows
+// >= L/2 widen directly -- their words land past the packed tile; (2) rows
+// < L/2 are read into registers (two per word) before a barrier and written
+// after it.  Each thread (column kk, band b) takes 16 rows in each step.
+// Ends with a barrier.
+template <int TW, typename CV>
+__device__ __forceinline__ void widen16(unsigned char *smem, CV cv) {
+    const uint16_t *src = reinterpret_cast<const uint16_t *>(smem) + threadIdx.x;
+    uint32_t *dst = reinterpret_cast<uint32_t *>(smem) + threadIdx.x;
+    const int hi0 = (int)blockDim.y * 16 + (int)threadIdx.y * 16;   // upper half: rows L/2 + 16 b ...
+#pragma unroll 8
+    for (int y = hi0; y < hi0 + 16; ++y) dst[y * TW] = cv((int)(int16_t)src[y * TW], y);
+    const int lo = (int)threadIdx.y * 16;                            // lower half: rows 16 b ...
+    uint32_t v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+        v[i] = (uint32_t)src[(lo + 2 * i) * TW] | ((uint32_t)src[(lo + 2 * i + 1) * TW] << 16);
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        dst[(lo + 2 * i) * TW] = cv((int)(int16_t)(v[i] & 0xffffu), lo + 2 * i);
+        dst[(lo + 2 * i + 1) * TW] = cv((int)(int16_t)(v[i] >> 16), lo + 2 * i + 1);
+    }
+    __syncthreads();
+}
+
 // TMA-staged variant (narrow 32-bit codes, nz % 4 == 0): one elected thread
 // issues the bulk tensor loads of the whole 32-column tile into the stack
 // region; every row of the column is in flight at once.
@@ -1033,9 +1096,10 @@ __device__ __forceinline__ void col_tma_run(const CUtensorMap *tmap, const CUten
         if (threadIdx.x == 0 && threadIdx.y == 0) {
             mbar_init(bar, 1);
             const int nbox = P.rows_alloc / P.boxh;
-            mbar_expect_tx(bar, (uint32_t)(P.rows_alloc * TW * sizeof(EntT)));
+            const int esz = PASS == 2 && P.s16 ? 2 : (int)sizeof(EntT);   // int16 s1: packed tile
+            mbar_expect_tx(bar, (uint32_t)(P.rows_alloc * TW * esz));
             for (int q = 0; q < nbox; ++q) {
-                void *dst = stk + (size_t)q * P.boxh * TW;
+                void *dst = smem + (size_t)q * P.boxh * TW * esz;
                 if constexpr (PASS == 2) {
                     if constexpr (VX_P2_EVICT_FIRST)   // s1 is read once: keep s2 in L2 for pass 3
                         tma_load_3d_ef(dst, tmap, bar, kt * TW, q * P.boxh, (int)outer);
@@ -1051,6 +1115,9 @@ __device__ __forceinline__ void col_tma_run(const CUtensorMap *tmap, const CUten
     }
     __syncthreads();
     mbar_wait(bar, 0);
+    if constexpr (PASS == 2) {
+        if (P.s16) widen16<TW>(smem, [](int v, int) { return (uint32_t)v; });
+    }
     column_tile<PASS, false, false, FW, true, SCAT, CMP, TW>(in, out, stk, meta, P, tile, sc);
 #ifdef VX_PHASE_TIMING
     VX_PT(5);
@@ -1102,13 +1169,14 @@ __device__ __forceinline__ bool ring_tile(const typename Col<PASS, false, false,
     int *s_fail = reinterpret_cast<int *>(bar + 1);
     const int scene = PASS == 2 ? 0 : (int)(outer / P.nyl);
     const int jl = PASS == 2 ? 0 : (int)(outer - (long long)scene * P.nyl);
+    const bool s16 = PASS == 2 && P.s16;   // int16 s1: packed tile, widened into keys below
     if (threadIdx.x == 0 && threadIdx.y == 0) {
         *s_fail = 0;
         mbar_init(bar, 1);
         const int nbox = P.rows_alloc / P.boxh;
-        mbar_expect_tx(bar, (uint32_t)(P.rows_alloc * TW * 4));
+        mbar_expect_tx(bar, (uint32_t)(P.rows_alloc * TW * (s16 ? 2 : 4)));
         for (int q = 0; q < nbox; ++q) {
-            void *dst = key + (size_t)q * P.boxh * TW;
+            void *dst = smem + (size_t)q * P.boxh * TW * (s16 ? 2 : 4);
             if constexpr (PASS == 2) tma_load_3d(dst, &tmap, bar, kt * TW, q * P.boxh, (int)outer);
             else tma_load_4d(dst, &tmap, bar, kt * TW, jl, q * P.boxh, scene);
         }
@@ -1134,7 +1202,14 @@ __device__ __forceinline__ bool ring_tile(const typename Col<PASS, false, false,
     mbar_wait(bar, 0);
     // the tile's values -> search keys, in place (each thread its band's rows)
     uint32_t *col = key + kk;
-    if (colok) {
+    if (s16) {   // pass 2 from int16 s1: the band's values through registers, then keys
+        const uint32_t kinv = P.kinv;
+        widen16<TW>(smem, [=](int v, int y) -> uint32_t {
+            if (v < 0) return kinv;
+            const int dz = k - v;
+            return ((uint32_t)(dz * dz) << rb) | (uint32_t)y;
+        });
+    } else if (colok) {
 #pragma unroll 4
         for (int y = lo; y < hi; ++y) {
             VX_ASSERT(y >= 0 && y < P.rows_alloc, "ring key row");
@@ -1168,8 +1243,10 @@ __device__ __forceinline__ bool ring_tile(const typename Col<PASS, false, false,
         // per block is cheaper in the banded kernel -- hand it back early
         const int budget = P.ring_budget;
         int spent = -2 * budget;
-        const InT *src = in + base;
-        const uint32_t ustride4 = (uint32_t)stride * (uint32_t)sizeof(InT);   // row byte offsets fit 32 bits
+        // the winners' codes are re-read from the input (int16 or int32 s1 in pass 2)
+        const int esz = s16 ? 2 : (int)sizeof(InT);
+        const char *srcb = reinterpret_cast<const char *>(in) + base * esz;
+        const uint32_t ustride4 = (uint32_t)stride * (uint32_t)esz;   // row byte offsets fit 32 bits
         RowOut<OutT, SCAT> dst;
         dst.begin(out, base, stride, lo, &sc, outer, k, P.nz);
         // four query rows per block share one window: step s reads rows
@@ -1265,8 +1342,8 @@ __device__ __forceinline__ bool ring_tile(const typename Col<PASS, false, false,
                 const int row = (int)(bb[i] & rmask);
                 VX_ASSERT(row >= 0 && row < P.L && bb[i] < P.kinv, "ring winner row");
                 wrow[i] = row;
-                wcode[i] = __ldg(reinterpret_cast<const InT *>(reinterpret_cast<const char *>(src) +
-                                                              (unsigned long long)(uint32_t)row * ustride4));
+                const char *pc = srcb + (unsigned long long)(uint32_t)row * ustride4;
+                wcode[i] = s16 ? (InT)(int)__ldg(reinterpret_cast<const short *>(pc)) : __ldg(reinterpret_cast<const InT *>(pc));
             }
         }
         if (q0 >= hi) emit_pending(q0 - R);
@@ -1632,6 +1709,7 @@ ColParams col_params(const EdtPlan &p, int pass, long long nouter, int nyl, int 
     P.mcount = nullptr;
     P.sflag3 = nullptr;
     P.ring_min = 0x7fffffff;
+    P.s16 = pass == 2 && p.s1_16;
     P.rhdr = nullptr;
     P.fslot = pass == 2 ? 0 : 1;
     P.nkt2 = (p.nz + p.tw2 - 1) / p.tw2;
@@ -1686,13 +1764,14 @@ bool make_tmap(CUtensorMap *m, const void *in, const EdtPlan &p, int pass, long 
                int boxh, int boxw = 32) {
     auto enc = tmap_encoder();
     if (!enc) return false;
+    const int es = pass == 2 && p.s1_16 ? 2 : 4;   // int16 line sites (EdtPlan::s1_16)
     cuuint64_t dims[4], strides[3];
     cuuint32_t box[4], estr[4] = {1, 1, 1, 1};
     cuuint32_t rank;
     if (pass == 2) {
         rank = 3;
         dims[0] = p.nz; dims[1] = p.ny; dims[2] = (cuuint64_t)nouter;
-        strides[0] = (cuuint64_t)p.nz * 4; strides[1] = (cuuint64_t)p.ny * p.nz * 4;
+        strides[0] = (cuuint64_t)p.nz * es; strides[1] = (cuuint64_t)p.ny * p.nz * es;
         box[0] = (cuuint32_t)boxw; box[1] = boxh; box[2] = 1;
     } else {
         rank = 4;
@@ -1702,7 +1781,7 @@ bool make_tmap(CUtensorMap *m, const void *in, const EdtPlan &p, int pass, long 
         strides[2] = (cuuint64_t)p.nx * nyl * p.nz * 4;
         box[0] = (cuuint32_t)boxw; box[1] = 1; box[2] = boxh; box[3] = 1;
     }
-    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, rank, const_cast<void *>(in), dims, strides, box, estr,
+    CUresult r = enc(m, es == 2 ? CU_TENSOR_MAP_DATA_TYPE_UINT16 : CU_TENSOR_MAP_DATA_TYPE_UINT32, rank, const_cast<void *>(in), dims, strides, box, estr,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
@@ -1805,7 +1884,8 @@ cudaError_t launch_col(const void *in, void *out, void *gstack, const EdtPlan &p
             }
         }
     }
-    if (P.xs || P.B > kMaxBands) return cudaErrorNotSupported;   // TMA-staged kernel only
+    // TMA-staged kernel only: occupied-slice lists, 32 bands, int16 s1
+    if (P.xs || P.B > kMaxBands || P.s16) return cudaErrorNotSupported;
     P.rows_alloc = P.L;
     if (!gs) {
         const size_t smem = (size_t)P.L * 32 * sizeof(typename C::EntT) + (size_t)(3 * P.B * 32 + 32) * 4;
@@ -1944,13 +2024,23 @@ bool make_plan(int nx, int ny, int nz, EdtPlan *p, int force_global_stack) {
     q.s1_bytes = (n * 4 + 255) & ~(size_t)255;
     q.s2_bytes = (n * (q.s2_wide ? 8 : 4) + 255) & ~(size_t)255;
     q.gstack_bytes = gs;
+    // pass 1 writes int16 line sites when pass 2 stages its tiles by TMA and
+    // widens them in shared memory: half the bytes of
+    // pass 1's writes and of pass 2's tile loads.  Needs 16-byte rows (nz % 8)
+    // and sites below 2^15; VX_S1_16=0 keeps int32
+    const char *s16 = getenv("VX_S1_16");
+    // (pass-2 columns: L = ny a power of two in [64, 1024] in bands of 32 rows --
+    // the in-place widening, widen16, relies on that shape)
+    q.s1_16 = q.tma2 && !q.e3_wide && q.W2 == 32 && ny >= 64 && ny <= 1024 && (ny & (ny - 1)) == 0 &&
+              nz % 8 == 0 && nz <= 32767 && !(s16 && atoi(s16) == 0);
     *p = q;
     return true;
 }
 
 
-cudaError_t launch_pass1(const uint8_t *occ, int32_t *s1, long long nslices, int ny, int nz,
-                         cudaStream_t st, const SparseRows *sp) {
+template <typename T>
+cudaError_t launch_pass1_t(const uint8_t *occ, T *s1, long long nslices, int ny, int nz,
+                           cudaStream_t st, const SparseRows *sp) {
     const long long nlines = nslices * ny;
     if (nlines == 0) return cudaSuccess;
     const uint8_t *sflag = sp ? sp->sflag : nullptr;
@@ -1971,22 +2061,31 @@ cudaError_t launch_pass1(const uint8_t *occ, int32_t *s1, long long nslices, int
         cudaError_t e = cudaMemsetAsync(ls, 0, 16, st);
         if (e != cudaSuccess) return e;
     }
-    if (vec && nz <= 128) k_pass1_v4<1, 2><<<grid2, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny, xs, hdr, ls);
-    else if (vec && nz <= 256) k_pass1_v4<2, 2><<<grid2, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny, xs, hdr, ls);
-    else if (vec && nz <= 512 && xs && VX_P1_LPW512 == 2) k_pass1_v4<4, 2><<<grid2, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny, xs, hdr, ls);
+    if (vec && nz <= 128) k_pass1_v4<1, 2, T><<<grid2, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny, xs, hdr, ls);
+    else if (vec && nz <= 256) k_pass1_v4<2, 2, T><<<grid2, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny, xs, hdr, ls);
+    else if (vec && nz <= 512 && xs && VX_P1_LPW512 == 2) k_pass1_v4<4, 2, T><<<grid2, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny, xs, hdr, ls);
     else if (vec && nz % 16 == 0 && nz <= 512 && VX_P1_X16)   // persistent: 6 CTAs of 8 warps per SM
-        (nz % 512 == 0 ? k_pass1_x16<1, true> : k_pass1_x16<1, false>)
+        (nz % 512 == 0 ? k_pass1_x16<1, true, T> : k_pass1_x16<1, false, T>)
             <<<(unsigned)std::min<long long>(grid, (long long)num_sms() * 6), 256, 0, st>>>(
             occ, s1, nlines, nz, sflag, ny, xs, hdr, ls);
-    else if (vec && nz <= 512) k_pass1_v4<4, 1><<<grid, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny, xs, hdr, ls);
+    else if (vec && nz <= 512) k_pass1_v4<4, 1, T><<<grid, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny, xs, hdr, ls);
     else if (vec && nz % 16 == 0 && nz <= 1024 && VX_P1_X16)
-        (nz % 512 == 0 ? k_pass1_x16<2, true> : k_pass1_x16<2, false>)
+        (nz % 512 == 0 ? k_pass1_x16<2, true, T> : k_pass1_x16<2, false, T>)
             <<<(unsigned)std::min<long long>(grid, (long long)num_sms() * 6), 256, 0, st>>>(
             occ, s1, nlines, nz, sflag, ny, xs, hdr, ls);
-    else if (vec && nz <= 1024) k_pass1_v4<8, 1><<<grid, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny, xs, hdr, ls);
-    else if (vec && nz <= 2048) k_pass1_v4<16, 1><<<grid, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny, xs, hdr, ls);
-    else k_pass1_generic<<<grid, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny);
+    else if (vec && nz <= 1024) k_pass1_v4<8, 1, T><<<grid, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny, xs, hdr, ls);
+    else if (vec && nz <= 2048) k_pass1_v4<16, 1, T><<<grid, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny, xs, hdr, ls);
+    else k_pass1_generic<T><<<grid, 256, 0, st>>>(occ, s1, nlines, nz, sflag, ny);
     return cudaGetLastError();
+}
+
+cudaError_t launch_pass1(const uint8_t *occ, void *s1, long long nslices, int ny, int nz,
+                         cudaStream_t st, const SparseRows *sp, bool s16) {
+    if (s16) {   // int16 line sites (EdtPlan::s1_16)
+        if (nz % 8 != 0 || nz > 32767) return cudaErrorInvalidValue;
+        return launch_pass1_t(occ, static_cast<int16_t *>(s1), nslices, ny, nz, st, sp);
+    }
+    return launch_pass1_t(occ, static_cast<int32_t *>(s1), nslices, ny, nz, st, sp);
 }
 
 cudaError_t launch_pass2(const int32_t *s1, void *s2, void *gstack, const EdtPlan &p,
@@ -2210,14 +2309,14 @@ cudaError_t edt_device_batched(const uint8_t *occ, int32_t *site, void *scratch,
         SparseRows spf = sp;
         if (nscenes > 1) spf.xs = nullptr, spf.hdr = nullptr;
         const long long nsl = (long long)p.nx * nscenes;
-        if (e == cudaSuccess) e = launch_pass1(occ, s1, nsl, p.ny, p.nz, st, &spf);
+        if (e == cudaSuccess) e = launch_pass1(occ, s1, nsl, p.ny, p.nz, st, &spf, p.s1_16);
         if (e == cudaSuccess) e = launch_pass2(s1, s2, gs, p, nsl, st, &sp);
         // pass 3 of the sparse path: s1 is dead by now and serves as the
         // spill slab of the per-warp column stacks (single scene)
         if (e == cudaSuccess) e = launch_pass3(s2, site, s1, p, nscenes, 0, p.ny, st, &sp);
         return e;
     }
-    e = launch_pass1(occ, s1, (long long)p.nx * nscenes, p.ny, p.nz, st);
+    e = launch_pass1(occ, s1, (long long)p.nx * nscenes, p.ny, p.nz, st, nullptr, p.s1_16);
     if (e != cudaSuccess) return e;
     e = launch_pass2(s1, s2, gs, p, (long long)p.nx * nscenes, st);
     if (e != cudaSuccess) return e;

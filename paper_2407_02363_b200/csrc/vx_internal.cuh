@@ -44,6 +44,7 @@ struct EdtPlan {
     size_t smem2, smem3;   // dynamic smem bytes per CTA
     size_t s1_bytes, s2_bytes, gstack_bytes;  // scratch layout
     int gstack_ctas;       // persistent CTAs when a global stack is used
+    bool s1_16;            // pass-1 output (line sites) as int16: pass 2 widens its TMA tiles
 };
 
 bool make_plan(int nx, int ny, int nz, EdtPlan *p, int force_global_stack);
@@ -73,8 +74,9 @@ struct SparseRows {
 
 // Pass launchers (stream-ordered, no host sync).  Return cudaError_t.
 // nslices: number of (ny, nz) slices stacked along i (scenes * local nx).
-cudaError_t launch_pass1(const uint8_t *occ, int32_t *s1, long long nslices, int ny, int nz,
-                         cudaStream_t st, const SparseRows *sp = nullptr);
+// s16: int16 output (EdtPlan::s1_16; pass 2 of the same plan reads it)
+cudaError_t launch_pass1(const uint8_t *occ, void *s1, long long nslices, int ny, int nz,
+                         cudaStream_t st, const SparseRows *sp = nullptr, bool s16 = false);
 cudaError_t launch_pass2(const int32_t *s1, void *s2, void *gstack, const EdtPlan &p,
                          long long nslices, cudaStream_t st, const SparseRows *sp = nullptr);
 // pass 2 with the fused exchange epilogue (slab mode)
