@@ -14,7 +14,8 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libvx.so")
+# VX_LIB: another build of the same library (tuning experiments, tools/variant_bench.sh)
+LIB_PATH = os.environ.get("VX_LIB") or os.path.join(_HERE, "libvx.so")
 
 VX_OK = 0
 VX_EINVAL = -22

@@ -87,6 +87,9 @@ constexpr bool kP3XW = VX_P3_XW != 0;
 #ifndef VX_STREAM_U
 #define VX_STREAM_U 16
 #endif
+#ifndef VX_P3S_ENDS
+#define VX_P3S_ENDS 1   // k_pass3_stream: store-only rows before the warp's first and after its last switch
+#endif
 #ifndef VX_STREAM_MAX_ROWS
 #define VX_STREAM_MAX_ROWS 256   // occupied slices up to which pass 3 runs one warp per tile
 #endif
@@ -1468,14 +1471,16 @@ __global__ void __launch_bounds__(kWarpCtaThreads, 1) k_pass3_stream(const uint3
                                                                      int32_t *__restrict__ out,
                                                                      uint32_t *__restrict__ ovf, const ColParams P) {
     extern __shared__ __align__(128) unsigned char smem[];
+    constexpr int U = VX_STREAM_U;   // candidate rows in flight per lane
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int m = __ldg(P.hdr);
     if (m > P.stream_max) return;
     const bool all_rows = m == P.L;
+    const int mp = (m + U - 1) / U * U;   // the list padded to whole batches (-1 = no row)
     uint32_t *sst = reinterpret_cast<uint32_t *>(smem) + (size_t)w * kStreamCap * 32 + lane;
     // candidate rows, staged once per CTA (every tile of the pass scans the same list)
     int *rows_s = reinterpret_cast<int *>(smem + (size_t)nw * kStreamCap * 32 * 4);
-    for (int t = threadIdx.x; t < m; t += blockDim.x) rows_s[t] = all_rows ? t : __ldg(P.xs + t);
+    for (int t = threadIdx.x; t < mp; t += blockDim.x) rows_s[t] = t < m ? (all_rows ? t : __ldg(P.xs + t)) : -1;
     __syncthreads();
     const long long gw = (long long)blockIdx.x * nw + w;
     uint32_t *gst = ovf + gw * (long long)max(P.L - kStreamCap, 0) * 32 + lane - (long long)kStreamCap * 32;
@@ -1485,7 +1490,8 @@ __global__ void __launch_bounds__(kWarpCtaThreads, 1) k_pass3_stream(const uint3
         if (i < kStreamCap) sst[i * 32] = e;
         else gst[(long long)i * 32] = e;
     };
-    // entry: (x << yzb) | s2 code (y << zb | z); F = x^2 + (j - y)^2 + (k - z)^2.
+    // Stack entry (x << eb) | code: F = x^2 + (j - y)^2 + (k - z)^2 decodes and
+    // the walk's sites need no re-read.
     // C512: the 512^3 single-scene grid, whose strides and shifts are constants
     const uint32_t eb = C512 ? 18u : (uint32_t)P.yzb;
     const uint32_t zb = C512 ? 9u : (uint32_t)P.zb, zmask = C512 ? 511u : P.zmask, ymask = C512 ? 511u : P.ymask;
@@ -1494,6 +1500,7 @@ __global__ void __launch_bounds__(kWarpCtaThreads, 1) k_pass3_stream(const uint3
     constexpr FT kNever = sizeof(FT) == 4 ? (FT)0x7fffffff : (FT)0x7fffffffffffffffLL;
     const long long step = (long long)gridDim.x * nw;
     const int nkt = C512 ? 16 : P.nkt;
+    const uint32_t ssp = (uint32_t)splane;   // row offsets fit 32 bits (int32 sites)
     for (long long tile = gw; tile < P.ntiles; tile += step) {
         const int kt = (int)(tile % nkt);
         const long long outer = tile / nkt;
@@ -1501,125 +1508,161 @@ __global__ void __launch_bounds__(kWarpCtaThreads, 1) k_pass3_stream(const uint3
         const int jl = (int)(outer - (long long)scene * P.nyl);
         const int jq = C512 ? jl : P.j0 + jl;
         const int k = kt * 32 + lane;
-        if (k >= nz) continue;   // lanes only; no warp-wide sync below
+        const unsigned am = C512 ? 0xffffffffu : __ballot_sync(0xffffffffu, k < nz);
+        if (k >= nz) continue;   // lanes only; the votes below use am
         const long long base = (long long)scene * P.nvox + (long long)jl * nz + k;
         const uint32_t *src = in + base;
         VX_PTW(tile, 0);
         VX_PTW(tile, 1);
-        auto wof = [&](uint32_t v) -> FT {   // (j - y)^2 + (k - z)^2 of an s2 code
-            const FT dy = (FT)(jq - (int)((v >> zb) & ymask)), dz = (FT)(k - (int)(v & zmask));
-            return dy * dy + dz * dz;
-        };
-        auto Fof = [&](uint32_t e) -> FT {
-            const FT x = (FT)(int)(e >> eb);
-            return x * x + wof(e);
+        auto wof = [&](uint32_t v) -> uint32_t {   // (j - y)^2 + (k - z)^2 of an s2 code
+            const uint32_t dy = (uint32_t)(jq - (int)((v >> zb) & ymask)), dz = (uint32_t)(k - (int)(v & zmask));
+            return dy * dy + dz * dz;   // < 2^wb (mod-2^32 arithmetic is exact)
         };
         int n = 0, ya = 0, yb = 0;
         FT Fa = 0, Fb = 0;
-        auto consume = [&](uint32_t v, int yc) {
+        // SPILL: some lane's stack may pass kStreamCap in this batch (checked
+        // once per batch of U rows: a batch grows a stack by at most U); the
+        // other batches touch shared memory only, with no per-access branch
+        auto consume = [&](uint32_t v, int yc, auto spill) {
+            constexpr bool SPILL = decltype(spill)::value;
             if (v == 0xffffffffu) return;
-            const FT wc = wof(v);
+            const uint32_t wc = wof(v);
             const uint32_t ec = ((uint32_t)yc << eb) | v;
-            const FT Fc = (FT)yc * (FT)yc + wc;
+            const FT Fc = (FT)yc * (FT)yc + (FT)wc;
             while (n >= 2 && dominated<FT, PT>(ya, Fa, yb, Fb, yc, Fc)) {
                 --n;
                 yb = ya;
                 Fb = Fa;
                 if (n >= 2) {
-                    const uint32_t e = ent(n - 2);
+                    const uint32_t e = SPILL ? ent(n - 2) : sst[(n - 2) * 32];
                     ya = (int)(e >> eb);
-                    Fa = Fof(e);
+                    Fa = (FT)ya * (FT)ya + (FT)wof(e);
                 }
             }
-            put(n, ec);
+            if (SPILL) put(n, ec);
+            else sst[n * 32] = ec;
             ya = yb;
             Fa = Fb;
             yb = yc;
             Fb = Fc;
             ++n;
         };
-        constexpr int U = VX_STREAM_U;   // candidate rows in flight per lane
-        const uint32_t ssp = (uint32_t)splane;   // row offsets fit 32 bits (int32 sites)
-        int t0 = 0;
-        for (; t0 + U <= m; t0 += U) {
+        // whole batches of U rows (the padded tail loads nothing)
+        for (int t0 = 0; t0 < mp; t0 += U) {
             uint32_t v[U];
             int yr[U];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 yr[u] = rows_s[t0 + u];
-                v[u] = cand_load(src + (uint32_t)yr[u] * ssp);
+                v[u] = yr[u] >= 0 ? cand_load(src + (uint32_t)yr[u] * ssp) : 0xffffffffu;
             }
+            if (__any_sync(am, n + U > kStreamCap)) {
 #pragma unroll
-            for (int u = 0; u < U; ++u) consume(v[u], yr[u]);
-        }
-        for (; t0 < m; ++t0) {
-            const int yr = rows_s[t0];
-            consume(cand_load(src + (uint32_t)yr * ssp), yr);
+                for (int u = 0; u < U; ++u) consume(v[u], yr[u], std::true_type());
+            } else {
+#pragma unroll
+                for (int u = 0; u < U; ++u) consume(v[u], yr[u], std::false_type());
+            }
         }
 #ifdef VX_PHASE_TIMING
         {   // hull size (max over the warp's columns) for tools/phase_timing
             int hmax = n;
-            const unsigned am = __activemask();
             for (int d = 16; d; d >>= 1) hmax = max(hmax, __shfl_xor_sync(am, hmax, d));
             if (lane == __ffs(am) - 1 && g_phase_buf) g_phase_buf[(size_t)tile * 8 + 7] = (unsigned long long)hmax;
         }
 #endif
         VX_PTW(tile, 2);
-        // ---- queries: first minimiser at every row, stepped walk
+        // ---- queries: first minimiser at every row, stepped walk (edt.py:300-317)
         int32_t *dst = out + base;
-        if (n == 0) {
-            for (int y = 0; y < L; ++y, dst += splane) *dst = -1;
-        } else {
-            auto site_of = [&](uint32_t e) -> int32_t {   // edt.py:417
-                const long long x = (long long)(e >> eb);
-                return (int32_t)(x * plane + (long long)((e >> zb) & ymask) * nz + (long long)(e & zmask));
-            };
-            int pos = 0;
-            uint32_t cur = ent(0);
-            int yc = (int)(cur >> eb);
-            FT Fc = Fof(cur);
-            int32_t ocur = site_of(cur);
-            bool has = n > 1;
-            uint32_t sent = 0;
-            int ys = 0;
-            FT Fs = 0;
+        auto xof = [&](uint32_t e) -> int { return (int)(e >> eb); };
+        auto Fof = [&](uint32_t e) -> FT {
+            const FT x = (FT)(int)(e >> eb);
+            return x * x + (FT)wof(e);
+        };
+        auto site_of = [&](uint32_t e) -> int32_t {   // edt.py:417
+            return (int32_t)((long long)(e >> eb) * plane + (long long)((e >> zb) & ymask) * nz + (long long)(e & zmask));
+        };
+        int pos = 0, yc = 0, ys = 0;
+        FT Fc = 0, Fs = 0;
+        int32_t ocur = -1;   // no candidate in the column (edt.py:295-299)
+        uint32_t sent = 0;
+        bool has = false;
+        if (n > 0) {
+            const uint32_t c0 = ent(0);
+            yc = xof(c0);
+            Fc = Fof(c0);
+            ocur = site_of(c0);
+            has = n > 1;
             if (has) {
                 sent = ent(1);
-                ys = (int)(sent >> eb);
+                ys = xof(sent);
                 Fs = Fof(sent);
             }
-            FT dN = has ? Fs - Fc : kNever;
-            FT tt = has ? (FT)2 * (FT)(ys - yc) : (FT)0;
-            FT rhs = 0;
-#pragma unroll kWalkUnroll
-            for (int y = 0; y < L; ++y) {
-                if (dN < rhs) {   // successor strictly closer at row y (edt.py:311)
-                    do {
-                        cur = sent;
-                        yc = ys;
-                        Fc = Fs;
-                        ++pos;
-                        has = pos + 1 < n;
-                        if (has) {
-                            sent = ent(pos + 1);
-                            ys = (int)(sent >> eb);
-                            Fs = Fof(sent);
-                        }
-                    } while (has && better<FT>(ys, Fs, yc, Fc, y));
-                    ocur = site_of(cur);
-                    dN = has ? Fs - Fc : kNever;
-                    tt = has ? (FT)2 * (FT)(ys - yc) : (FT)0;
-                    rhs = (FT)y * tt;
-                }
-#if VX_STREAM_STCS
-                __stcs(dst, ocur);   // evict-first: the sites are not re-read by this pass
-#else
-                *dst = ocur;
-#endif
-                dst += splane;
-                rhs += tt;
-            }
         }
+        FT dN = has ? Fs - Fc : kNever;
+        FT tt = has ? (FT)2 * (FT)(ys - yc) : (FT)0;
+        // rows before the warp's first switch are stores only: the successor is
+        // strictly closer from row dN / tt + 1 on (dN < y * tt, tt > 0)
+        int y0 = L;
+        if (has) y0 = dN < 0 ? 0 : (int)min((FT)L, dN / tt + 1);
+        y0 = VX_P3S_ENDS ? __reduce_min_sync(am, y0) : 0;
+        int y = 0;
+#if VX_STREAM_STCS
+#define VX_P3ST(p, v) __stcs((p), (v))   // evict-first: the sites are not re-read by this pass
+#else
+#define VX_P3ST(p, v) (*(p) = (v))
+#endif
+        for (; y + 4 <= y0; y += 4, dst += 4 * splane) {
+            VX_P3ST(dst, ocur);
+            VX_P3ST(dst + splane, ocur);
+            VX_P3ST(dst + 2 * splane, ocur);
+            VX_P3ST(dst + 3 * splane, ocur);
+        }
+        for (; y < y0; ++y, dst += splane) VX_P3ST(dst, ocur);
+        FT rhs = (FT)y * tt;
+        auto row = [&](int yy) {
+            if (dN < rhs) {   // successor strictly closer at row yy (edt.py:311)
+                uint32_t cur;
+                do {
+                    cur = sent;
+                    yc = ys;
+                    Fc = Fs;
+                    ++pos;
+                    has = pos + 1 < n;
+                    if (has) {
+                        sent = ent(pos + 1);
+                        ys = xof(sent);
+                        Fs = Fof(sent);
+                    }
+                } while (has && better<FT>(ys, Fs, yc, Fc, yy));
+                ocur = site_of(cur);
+                dN = has ? Fs - Fc : kNever;
+                tt = has ? (FT)2 * (FT)(ys - yc) : (FT)0;
+                rhs = (FT)yy * tt;
+            }
+            VX_P3ST(dst, ocur);
+            dst += splane;
+            rhs += tt;
+        };
+        // rows where some lane may still switch; once every lane sits on its
+        // last vertex the rest are stores only
+        for (; y + kWalkUnroll <= L; y += kWalkUnroll) {
+            if (VX_P3S_ENDS && !__any_sync(am, has)) break;
+#pragma unroll
+            for (int u = 0; u < kWalkUnroll; ++u) row(y + u);
+        }
+        if (__any_sync(am, has)) {
+            for (; y < L; ++y) row(y);
+        } else {
+            for (; y + 4 <= L; y += 4, dst += 4 * splane) {
+                VX_P3ST(dst, ocur);
+                VX_P3ST(dst + splane, ocur);
+                VX_P3ST(dst + 2 * splane, ocur);
+                VX_P3ST(dst + 3 * splane, ocur);
+            }
+            for (; y < L; ++y, dst += splane) VX_P3ST(dst, ocur);
+        }
+#undef VX_P3ST
         VX_PTW(tile, 3);
         VX_PTW(tile, 4);
         VX_PTW(tile, 5);
@@ -1640,6 +1683,15 @@ int pow2ceil(int v) {
 }
 
 constexpr size_t kSmemLimit = 227 * 1024;
+
+// k_pass3_stream: its stack entries fit 32 bits, and its dynamic shared
+// memory (the warps' stacks plus the row list padded to whole batches)
+inline bool stream_bits_ok(const EdtPlan &p) {
+    return p.xb + p.yb + p.zb <= 32;
+}
+inline size_t stream_smem(int L) {
+    return (size_t)VX_STREAM_WARPS * kStreamCap * 32 * 4 + (size_t)(L + VX_STREAM_U) * 4;
+}
 
 // windowed search (ring_tile): VX_RING=0 disables it, VX_RING_CAP sets the
 // largest search radius (rows) before a tile goes back to the banded kernel,
@@ -1824,8 +1876,8 @@ cudaError_t launch_col(const void *in, void *out, void *gstack, const EdtPlan &p
                     // only with tiles enough for >= 16 warps per SM: each warp walks
                     // its tile alone, so small grids keep the banded kernel
                     const int mode = sp ? sp->p3_mode : 0;
-                    const size_t ssm = (size_t)VX_STREAM_WARPS * kStreamCap * 32 * 4 + (size_t)P.L * 4;   // stacks + row list
-                    if (mode != 2 && cmp && gstack && nouter == nyl && p.xb + p.yb + p.zb <= 32 &&
+                    const size_t ssm = stream_smem(P.L);   // stacks + row list
+                    if (mode != 2 && cmp && gstack && nouter == nyl && stream_bits_ok(p) &&
                         spill <= (long long)p.s1_bytes && P.ntiles >= (long long)stream_min_tiles() && ssm <= kSmemLimit) {
                         const char *sm = getenv("VX_STREAM_MAX");
                         P.stream_max = mode == 1 ? 0x7fffffff : sm ? atoi(sm) : std::min(kStreamMaxRows, P.L / 2);
@@ -2247,9 +2299,8 @@ int pass3_mode_hint(const EdtPlan &p, int m) {
     const long long spill = std::min<long long>(ntiles, (long long)num_sms() * VX_STREAM_WARPS) *
                             std::max(p.nx - kStreamCap, 0) * 32 * 4;
     const bool ok = p.tma2 && p.tma3 && !p.gstack3 && !p.s2_wide && !p.e3_wide &&
-                    p.xb + p.yb + p.zb <= 32 && spill <= (long long)p.s1_bytes &&
-                    ntiles >= (long long)stream_min_tiles() &&
-                    (size_t)VX_STREAM_WARPS * kStreamCap * 32 * 4 + (size_t)p.nx * 4 <= kSmemLimit;
+                    stream_bits_ok(p) && spill <= (long long)p.s1_bytes &&
+                    ntiles >= (long long)stream_min_tiles() && stream_smem(p.nx) <= kSmemLimit;
     if (!ok) return 2;
     const char *sm = getenv("VX_STREAM_MAX");
     const int smax = sm ? atoi(sm) : std::min(kStreamMaxRows, p.nx / 2);
