@@ -87,6 +87,9 @@ constexpr bool kP3XW = VX_P3_XW != 0;
 #ifndef VX_STREAM_U
 #define VX_STREAM_U 16
 #endif
+#ifndef VX_P3S_WPF
+#define VX_P3S_WPF 1    // k_pass3_stream walk: the vertex after the successor loaded a switch ahead
+#endif
 #ifndef VX_P3S_ENDS
 #define VX_P3S_ENDS 1   // k_pass3_stream: store-only rows before the warp's first and after its last switch
 #endif
@@ -1599,6 +1602,9 @@ __global__ void __launch_bounds__(kWarpCtaThreads, 1) k_pass3_stream(const uint3
                 Fs = Fof(sent);
             }
         }
+#if VX_P3S_WPF
+        uint32_t snext = n > 2 ? ent(2) : 0u;   // the successor's successor, loaded a switch ahead
+#endif
         FT dN = has ? Fs - Fc : kNever;
         FT tt = has ? (FT)2 * (FT)(ys - yc) : (FT)0;
         // rows before the warp's first switch are stores only: the successor is
@@ -1630,7 +1636,12 @@ __global__ void __launch_bounds__(kWarpCtaThreads, 1) k_pass3_stream(const uint3
                     ++pos;
                     has = pos + 1 < n;
                     if (has) {
+#if VX_P3S_WPF
+                        sent = snext;
+                        if (pos + 2 < n) snext = ent(pos + 2);
+#else
                         sent = ent(pos + 1);
+#endif
                         ys = xof(sent);
                         Fs = Fof(sent);
                     }
