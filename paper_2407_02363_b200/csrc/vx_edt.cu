@@ -82,13 +82,16 @@ constexpr bool kP3XW = VX_P3_XW != 0;
 #define VX_P2_EVICT_FIRST 0
 #endif
 #ifndef VX_STREAM_CAP
-#define VX_STREAM_CAP 55   // shared-memory stack entries per column (k_pass3_stream; 32 warps x 55 x 128 B)
+#define VX_STREAM_CAP 63   // shared-memory stack entries per column (k_pass3_stream; 28 warps x 63 x 128 B)
 #endif
 #ifndef VX_STREAM_U
 #define VX_STREAM_U 16
 #endif
 #ifndef VX_P3S_WPF
 #define VX_P3S_WPF 1    // k_pass3_stream walk: the vertex after the successor loaded a switch ahead
+#endif
+#ifndef VX_P3S_DYN
+#define VX_P3S_DYN 1    // k_pass3_stream: tiles after the first from an atomic counter
 #endif
 #ifndef VX_P3S_ENDS
 #define VX_P3S_ENDS 1   // k_pass3_stream: store-only rows before the warp's first and after its last switch
@@ -1422,7 +1425,7 @@ __global__ void __launch_bounds__(kColThreads, kColMinBlocks) k_column_gstack(co
 }
 
 #ifndef VX_STREAM_WARPS
-#define VX_STREAM_WARPS 32
+#define VX_STREAM_WARPS 28
 #endif
 constexpr int kWarpCtaThreads = 32 * VX_STREAM_WARPS;   // k_pass3_stream CTA: one per SM
 
@@ -1504,7 +1507,19 @@ __global__ void __launch_bounds__(kWarpCtaThreads, 1) k_pass3_stream(const uint3
     const long long step = (long long)gridDim.x * nw;
     const int nkt = C512 ? 16 : P.nkt;
     const uint32_t ssp = (uint32_t)splane;   // row offsets fit 32 bits (int32 sites)
+#if VX_P3S_DYN
+    // tiles after each warp's first come from a counter (hdr[32], zeroed with
+    // the occupied-slice list): deep-hull tiles do not hold up a static share
+    int *tctr = const_cast<int *>(P.hdr) + 32;
+    auto next_tile = [&]() -> long long {
+        int t = 0;
+        if (lane == 0) t = atomicAdd(tctr, 1);
+        return step + __shfl_sync(0xffffffffu, t, 0);
+    };
+    for (long long tile = gw; tile < P.ntiles; tile = next_tile()) {
+#else
     for (long long tile = gw; tile < P.ntiles; tile += step) {
+#endif
         const int kt = (int)(tile % nkt);
         const long long outer = tile / nkt;
         const int scene = C512 ? 0 : (int)(outer / P.nyl);
@@ -2228,6 +2243,7 @@ __global__ void __launch_bounds__(1024) k_slice_list(const uint8_t *__restrict__
     }
     if (threadIdx.x == 0) {
         hdr[0] = base_s;
+        if (gridDim.x == 1) hdr[32] = 0;   // single scene: k_pass3_stream's tile counter
         if (m_mirror) *(volatile int *)m_mirror = base_s;   // host-mapped hint
     }
 }

@@ -244,7 +244,7 @@ def _stream_grid(seed, deep):
     """(256, 512, 160): 2560 pass-3 tiles (>= 16 per SM) and m <= L/2 occupied
     slices, so pass 3 takes the one-warp kernel.  deep: every occupied slice
     carries the same sites, so every column's hull keeps all m candidates
-    (m > the 55 shared-memory entries: the global spill path)."""
+    (m > the 63 shared-memory entries: the global spill path)."""
     rng = np.random.default_rng(seed)
     occ = np.zeros((256, 512, 160), np.uint8)
     xs = np.sort(rng.choice(256, 100 if deep else 60, replace=False))
@@ -282,6 +282,29 @@ def test_pass3_one_warp_kernel_multi_tile(deep, monkeypatch):
     for x in xs:
         occ[x][rng.random((1536, 128)) < 0.001] = 1
         if deep:
+            occ[x, pts[:, 0], pts[:, 1]] = 1
+    want = O.pba_edt_site(occ)
+    assert np.array_equal(pba_edt(occ).site, want)
+    monkeypatch.setenv("VX_STREAM_MAX", "-1")   # banded kernel only
+    assert np.array_equal(pba_edt(occ).site, want)
+
+
+@pytest.mark.parametrize("m", [1, 15, 16, 17, 33, 100])
+def test_pass3_one_warp_kernel_batches_and_ragged_tiles(m, monkeypatch):
+    """k_pass3_stream's batch edges and partial warps: occupied-slice counts
+    around the 16-row candidate batches (the padded list's predicated tail,
+    the once-per-batch spill vote) and nz = 150, whose last k-tile leaves 10
+    lanes idle (the warp votes and the first-switch minimum then run on a
+    partial mask); half the slices carry shared sites, so some columns have
+    late first switches and long hulls.  Equal to the oracle and to the
+    banded kernel."""
+    rng = np.random.default_rng(100 + m)
+    occ = np.zeros((200, 512, 150), np.uint8)
+    xs = np.sort(rng.choice(200, m, replace=False))
+    pts = rng.integers(0, [512, 150], size=(30, 2))
+    for n, x in enumerate(xs):
+        occ[x][rng.random((512, 150)) < 0.001] = 1
+        if n % 2 == 0:
             occ[x, pts[:, 0], pts[:, 1]] = 1
     want = O.pba_edt_site(occ)
     assert np.array_equal(pba_edt(occ).site, want)
