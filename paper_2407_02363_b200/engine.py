@@ -86,6 +86,9 @@ class MapCycle:
         self._world = _lib.PinnedArray((2, S, 3), np.float64)
         self._dist = _lib.PinnedArray((2, S), np.float64)
         self._s = 0
+        L = _lib.load()
+        self._step_staged, self._prefetch, self._wait = L.vx_cycle_step_staged, L.vx_cycle_prefetch, L.vx_cycle_wait
+        self._hit_key, self._hit32 = None, 0.0
 
     def close(self):
         if self._h is not None:
@@ -109,9 +112,14 @@ class MapCycle:
         if isinstance(points, StagedCloud):
             if points.cycle is not self:
                 raise ValueError("StagedCloud belongs to another MapCycle")
-            _lib.check(_lib.load().vx_cycle_step_staged(
-                self._h, points.ticket, _lib.ptr(T), float(np.float32(hit_logodds)),
-                float(occupancy_threshold), _lib.ptr(c), c.shape[0], 1 if sync else 0))
+            # the per-tick call: plain integer addresses (ctypes converts them
+            # for the c_void_p parameters), the float32 hit cached
+            if hit_logodds != self._hit_key:
+                self._hit_key, self._hit32 = hit_logodds, float(np.float32(hit_logodds))
+            rc = self._step_staged(self._h, points.ticket, T.ctypes.data, self._hit32,
+                                   float(occupancy_threshold), c.ctypes.data, c.shape[0], 1 if sync else 0)
+            if rc:
+                _lib.check(rc)
             pts = points.array
         else:
             pts = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 3)
@@ -131,8 +139,9 @@ class MapCycle:
         and stepping with a consumed or invalidated ticket raises."""
         pts = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 3)
         t = ctypes.c_uint64()
-        _lib.check(_lib.load().vx_cycle_prefetch(self._h, _lib.ptr(pts), pts.shape[0],
-                                                 ctypes.byref(t)))
+        rc = self._prefetch(self._h, pts.ctypes.data, pts.shape[0], ctypes.byref(t))
+        if rc:
+            _lib.check(rc)
         self._pf = getattr(self, "_pf", [])[-1:] + [pts]   # alive until the upload ran
         return StagedCloud(self, int(t.value), pts)
 
@@ -143,8 +152,9 @@ class MapCycle:
         lin = np.empty((2, s), np.int32)
         world = np.empty((2, s, 3), np.float64)
         dist = np.empty((2, s), np.float64)
-        _lib.check(_lib.load().vx_cycle_wait(self._h, ctypes.byref(res), _lib.ptr(lin),
-                                             _lib.ptr(world), _lib.ptr(dist)))
+        rc = self._wait(self._h, ctypes.byref(res), lin.ctypes.data, world.ctypes.data, dist.ctypes.data)
+        if rc:
+            _lib.check(rc)
         st = res.stats
         return {"inserted": st.inserted, "robot_skipped": st.robot_skipped,
                 "out_of_bounds": st.out_of_bounds, "self_recomputed": bool(res.self_recomputed),
