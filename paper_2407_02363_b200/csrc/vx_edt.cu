@@ -1694,6 +1694,14 @@ __global__ void __launch_bounds__(kWarpCtaThreads, 1) k_pass3_stream(const uint3
         VX_PTW(tile, 5);
         VX_PTW(tile, 6);
     }
+#if VX_P3S_DYN
+    // the last warp out re-arms the counter (hdr[33] counts finished warps), so
+    // a later launch on the same list starts from zero as well
+    if (lane == 0 && atomicAdd(tctr + 1, 1) == (int)(gridDim.x * nw) - 1) {
+        tctr[0] = 0;
+        tctr[1] = 0;
+    }
+#endif
 }
 
 int bits_of(long long v) {  // bits to hold values 0..v
@@ -2243,7 +2251,7 @@ __global__ void __launch_bounds__(1024) k_slice_list(const uint8_t *__restrict__
     }
     if (threadIdx.x == 0) {
         hdr[0] = base_s;
-        if (gridDim.x == 1) hdr[32] = 0;   // single scene: k_pass3_stream's tile counter
+        if (gridDim.x == 1) hdr[32] = hdr[33] = 0;   // single scene: k_pass3_stream's tile counters
         if (m_mirror) *(volatile int *)m_mirror = base_s;   // host-mapped hint
     }
 }

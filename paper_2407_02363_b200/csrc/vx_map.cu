@@ -330,7 +330,7 @@ __global__ void k_finalize(float *__restrict__ cells, uint8_t *__restrict__ occ,
     }
     if (threadIdx.x == 0) {
         hdr[0] = base_s;
-        hdr[32] = 0;   // the one-warp pass 3's tile counter (vx_edt.cu k_pass3_stream)
+        hdr[32] = hdr[33] = 0;   // the one-warp pass 3's tile counters (vx_edt.cu k_pass3_stream)
         if (m_mirror) *(volatile int *)m_mirror = base_s;   // host-mapped hint
     }
 }
